@@ -1,0 +1,237 @@
+"""Oracle pins P7-P10: prolongation R0^T (eq:R0T P:144-147, Remark 3.2 P:153-159), the additive
+Schwarz operator (Lemma 5.8, Assumptions P:522-546, Thm TosWil),
+PCG / Lanczos and the condition-number scaling laws (Remark 6.6 P:700-710)."""
+import copy
+import math
+
+import numpy as np
+import pytest
+
+import dgas_gen as g
+import oracle as O
+
+
+def test_P7b_nested_Q_closed_form():
+    # config 1: 8x8 coarse tiles of squares, q = 1, any p: Q block of fine cell at tile position (i,j):
+    # [[1/m, sqrt3(2i+1-m)/m^2, sqrt3(2j+1-m)/m^2], [0, 1/m^2, 0], [0, 0, 1/m^2]]; rows >= 3 zero.
+    for p in (1, 2):
+        P = g.config(1)
+        o = O.Oracle(P, p=p)
+        o.setup_schwarz(q=None) if False else o.setup_schwarz()
+        G = o.G()
+        m = 8
+        n = 16
+        for cell in [0, 9, 63, 100, 255]:
+            ci, cj = cell % n, cell // n
+            i, j = ci % m, cj % m
+            ref = np.zeros((o.np_, 3))
+            ref[0] = [1 / m, math.sqrt(3) * (2 * i + 1 - m) / m ** 2, math.sqrt(3) * (2 * j + 1 - m) / m ** 2]
+            ref[1, 1] = 1 / m ** 2
+            ref[2, 2] = 1 / m ** 2
+            assert np.abs(G[cell] - ref).max() < 1e-14, cell
+
+
+def _Q_dense(o):
+    f, c, _, _ = o._ov
+    Q = np.zeros((o.N, o.N0))
+    G = o.G()
+    for k in range(o.n_ov):
+        Q[f[k] * o.np_:(f[k] + 1) * o.np_, c[k] * o.nq_:(c[k] + 1) * o.nq_] += G[k]
+    return Q
+
+
+def _coarse_const(o):
+    """coarse coefficients of the constant 1: (psi_b, 1)_{D_J} with psi orthonormal on D_J."""
+    c1 = np.zeros(o.N0)
+    f, c, ptr, xy = o._ov
+    # (1, psi_J,b) = sum over pieces of int psi; psi_0 = 1/sqrt|D_J| and others orthogonal to 1
+    areas = np.zeros(o.n_coarse)
+    for k in range(o.n_ov):
+        poly = xy[ptr[k]:ptr[k + 1]]
+        areas[c[k]] += 0.5 * np.sum(poly[:, 0] * np.roll(poly[:, 1], -1) - np.roll(poly[:, 0], -1) * poly[:, 1])
+    c1[0::o.nq_] = np.sqrt(areas)
+    return c1, areas
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_P7_constant_reproduction(cfg):
+    # Q maps the coarse representation of 1 to the fine representation of 1 (nested and non-nested)
+    P = g.config(cfg, scale="small")
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    Q = _Q_dense(o)
+    c1, areas = _coarse_const(o)
+    assert abs(areas.sum() - 1.0) < 1e-12
+    one_h = o.project(1) * 0  # fine coefficients of 1: sqrt|kappa| in mode 0
+    for c in range(P.n_cells):
+        poly = P.xy[P.cell_vtx[P.cell_ptr[c]:P.cell_ptr[c + 1]]]
+        one_h[c * o.np_] = np.sqrt(0.5 * np.sum(poly[:, 0] * np.roll(poly[:, 1], -1) - np.roll(poly[:, 0], -1) * poly[:, 1]))
+    tol = 1e-12 if P.nested else 1e-10
+    assert np.abs(Q @ c1 - one_h).max() < tol
+
+
+def test_P7_nested_injection_and_split_pieces():
+    # Remark 3.2: nested => R0^T = natural injection: Q c equals the exact re-expansion of the coarse
+    # polynomial on each fine cell (pointwise). Also: splitting every fine cell into two pieces of the
+    # same coarse element (a "non-nested" description of a nested pair) gives the same Q.
+    P = g.config(2, scale="small")
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    Q = _Q_dense(o)
+    rng = np.random.default_rng(3)
+    cvec = rng.normal(size=o.N0)
+    fine = Q @ cvec
+    # evaluate both at random points inside some fine cells
+    f, cc, ptr, xy = o._ov
+    for cell in [0, 17, 100, 255]:
+        poly = P.xy[P.cell_vtx[P.cell_ptr[cell]:P.cell_ptr[cell + 1]]]
+        pts = poly.mean(0) + 0.2 * (poly[:2] - poly.mean(0))
+        phi, _, _ = o.eval_basis(cell, pts)
+        uh = phi @ fine[cell * o.np_:(cell + 1) * o.np_]
+        J = P.parent[cell]
+        Cc, bb = o.coarse_basis(J)
+        xi = 2 * (pts[:, 0] - bb[0]) / (bb[1] - bb[0]) - 1
+        eta = 2 * (pts[:, 1] - bb[2]) / (bb[3] - bb[2]) - 1
+        L = np.polynomial.legendre.Legendre.basis
+        graw = np.stack([L(1)(xi) * 0 + 1, L(1)(xi), L(1)(eta)], 1)  # q = 1 graded order
+        uH = (graw @ Cc.T) @ cvec[J * o.nq_:(J + 1) * o.nq_]
+        assert np.abs(uh - uH).max() < 1e-12
+    # split pieces
+    nf, ncf, nptr, nxy = [], [], [0], []
+    for cell in range(P.n_cells):
+        poly = P.xy[P.cell_vtx[P.cell_ptr[cell]:P.cell_ptr[cell + 1]]]
+        k = len(poly)
+        a = poly[:k // 2 + 1]
+        b = np.concatenate([poly[k // 2:], poly[:1]])
+        for piece in (a, b):
+            nf.append(cell); ncf.append(P.parent[cell]); nxy.extend(piece.tolist()); nptr.append(len(nxy))
+    o2 = O.Oracle(P)
+    o2.setup_schwarz(coarse=(P.n_coarse, np.array(nf), np.array(ncf), np.array(nptr), np.array(nxy)))
+    Q2 = _Q_dense(o2)
+    assert np.abs(Q2 - Q).max() < 1e-12
+
+
+def test_P8_schwarz_properties_cfg1():
+    P = g.config(1)
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    A = o.dense_A()
+    M = o.dense_precond()
+    # (i) symmetry, (ii) SPD
+    assert np.abs(M - M.T).max() <= 1e-12 * np.abs(M).max()
+    assert np.linalg.eigvalsh(0.5 * (M + M.T))[0] > 0
+    # (vi) trace identity: tr(P^-1 A) = N + N0 (each exact subspace solve is a projection of rank dim V_i)
+    assert abs(np.trace(M @ A) - (o.N + o.N0)) < 1e-8 * o.N
+    # (vii) 1 <= lambda_max(P^-1 A) <= 1 + rho(I + Adj_face); config 1's face graph is a 4-cycle => <= 4
+    ev = np.sort(np.linalg.eigvals(M @ A).real)
+    assert ev[-1] >= 1 - 1e-10 and ev[-1] <= 4 + 1e-10
+    # projections: P_i E_i v = E_i v  (local parts are A-orthogonal projections)
+    Pad = M @ A
+    rng = np.random.default_rng(0)
+    v = rng.normal(size=o.N)
+    # apply of A v restricted to... linearity
+    z1 = o.apply(v); z2 = o.apply(2 * v)
+    assert np.abs(z2 - 2 * z1).max() < 1e-12 * np.abs(z1).max()
+    # Lanczos K (rtol 1e-14) <= dense K and within 5%
+    b = o.rhs()
+    res = o.pcg(b, rtol=1e-14, maxit=2000)
+    Kd = ev[-1] / ev[0]
+    assert res["cond"] <= Kd * (1 + 1e-8)
+    assert res["cond"] >= 0.95 * Kd
+
+
+def test_P8_exactness_limits():
+    P = g.config(1)
+    # single subdomain, no coarse: P^-1 = A^-1 -> 1 iteration, K = 1
+    o = O.Oracle(P, part=np.zeros(P.n_cells, np.int32), n_sub=1)
+    o.setup_schwarz(use_coarse=False)
+    res = o.pcg(o.rhs(), rtol=1e-8)
+    assert res["iters"] == 1 and abs(res["cond"] - 1) < 1e-8
+    # coarse space = fine space (T_H = T_h, q = p), coarse only -> A^-1
+    P2 = copy.copy(P)
+    P2.parent = np.arange(P.n_cells, dtype=np.int32)
+    P2.n_coarse = P.n_cells
+    o2 = O.Oracle(P2)
+    o2.setup_schwarz(use_local=False)
+    res2 = o2.pcg(o2.rhs(), rtol=1e-8)
+    assert res2["iters"] == 1
+
+
+def test_P8_decomposition_identity():
+    # Lemma 5.8: unique non-overlapping decomposition => sum_i E_i E_i^T = I: with A_i = A restricted
+    # and the coarse part off, P^-1 A v = v for block-diagonal A (one subdomain per cell-block)
+    P = g.config(2, scale="small")
+    o = O.Oracle(P)
+    o.setup_schwarz(use_coarse=False)
+    rng = np.random.default_rng(2)
+    r = rng.normal(size=o.N)
+    z = o.apply(r)
+    # on each subdomain, A_i z_i = r_i exactly
+    A = o.dense_A()
+    for s in range(P.n_sub):
+        idx = np.concatenate([np.arange(c * o.np_, (c + 1) * o.np_) for c in np.where(P.part == s)[0]])
+        assert np.abs(A[np.ix_(idx, idx)] @ z[idx] - r[idx]).max() < 1e-9 * np.abs(r).max()
+
+
+def test_P9_lanczos_diag14():
+    # diag(1,4), b=(1,1), M=I: alpha0 = 0.4, beta0 = 0.36, alpha1 = 0.625 (hand-checked) -> Ritz {1,4}
+    lmin, lmax, K = O.lanczos([0.4, 0.625], [0.36])
+    assert abs(lmin - 1) < 1e-13 and abs(lmax - 4) < 1e-13 and abs(K - 4) < 1e-12
+
+
+def test_P9_pcg_matches_dense_solve():
+    P = g.config(1)
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    b = o.rhs()
+    res = o.pcg(b, rtol=1e-12)
+    x = np.linalg.solve(o.dense_A(), b)
+    assert np.linalg.norm(res["x"] - x) <= 1e-9 * np.linalg.norm(x)
+    # residual history decreases to below rtol, checked on the Euclidean norm
+    assert res["resid"][-1] <= 1e-12
+
+
+def test_R30_long_double_sensitivity_small_cfg4():
+    # fp64 apply vs long-double apply (R30) on the config-4-style problem with rho jumps
+    P = g.config(4, scale="small")
+    o = O.Oracle(P)
+    o.setup_schwarz(long_double=True)
+    r = g.normal(11, o.N)
+    z = o.apply(r); zl = o.apply(r, long_double=True)
+    assert np.linalg.norm(z - zl) <= 1e-11 * np.linalg.norm(zl)
+
+
+def _K(P, **kw):
+    o = O.Oracle(P, part=np.arange(P.n_cells, dtype=np.int32), n_sub=P.n_cells)  # paper regime T_HH = T_h
+    o.setup_schwarz(**kw)
+    res = o.pcg(o.rhs(), rtol=1e-12, maxit=3000)
+    return res["cond"]
+
+
+def test_P10_scaling_fixed_H_refine_h():
+    # nested Cartesian, p = q = 1, T_HH = T_h, fixed coarse 2x2 (H = 1/2): K = O(H^2/h^2)
+    Ks, r = [], []
+    for n in (8, 16, 32):
+        P = g.generate(0, n, sub_mode=0, sub_tile=1, coarse_mode=2, coarse_tile=n // 2, p=1, q=1)
+        Ks.append(_K(P)); r.append(n / 2)
+    slope = np.polyfit(np.log(r), np.log(Ks), 1)[0]
+    assert 1.4 <= slope <= 2.2, (Ks, slope)
+
+
+def test_P10_scaling_fixed_ratio():
+    # fixed H/h = 4: K approximately constant (diagonals of Table ASPCG_P1_poly), < 1.6x variation
+    Ks = []
+    for n in (8, 16, 32):
+        P = g.generate(0, n, sub_mode=0, sub_tile=1, coarse_mode=2, coarse_tile=4, p=1, q=1)
+        Ks.append(_K(P))
+    assert max(Ks) / min(Ks) < 1.6, Ks
+
+
+def test_P10_p_scaling_nested():
+    # nested, q = p: K = O(p) for fixed meshes (Remark 6.6 p^2/q term, Ex.5 P:1040): slope in [0.6, 1.4]
+    Ks, ps = [], []
+    for p in (1, 2, 3, 4):
+        P = g.generate(0, 8, sub_mode=0, sub_tile=1, coarse_mode=2, coarse_tile=2, p=p, q=p)
+        Ks.append(_K(P)); ps.append(p)
+    slope = np.polyfit(np.log(ps), np.log(Ks), 1)[0]
+    assert 0.6 <= slope <= 1.4, (Ks, slope)
