@@ -1,0 +1,283 @@
+#!/usr/bin/env python
+"""bench.py — ASPCG throughput on B200 (BASELINE.json metric: PCG iters/s and the HBM GB/s of the
+Schwarz-apply + SpMV kernels, fp64, 1 x B200, % of HBM peak).
+
+A step = one full dgas_pcg solve (rtol 1e-8, x0 = 0) of the workload: every per-iteration row of
+SURVEY.md §8(a) (SpMV, axpy/norm, restriction, coarse solve, local solves, prolongation, direction
+update) plus the Lanczos estimate. value = PCG iterations per second over the K timed steps (inputs
+already resident in HBM); e2e = the same metric through dgas_pcg_host (host b/x copied in and out
+inside the timed region). Multi-GPU: independent replicas, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # name -> (BASELINE config index, p, q)
+    "cfg1": (1, None, None), "cfg2": (2, None, None), "cfg3": (3, None, None), "cfg4": (4, None, None),
+    **{f"cfg5_p{p}q{q}": (5, p, q) for p in range(1, 7) for q in sorted({1, p})},
+}
+METRIC = "PCG iters/s & Schwarz-apply+SpMV HBM GB/s (fp64, 1xB200), % of HBM peak"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def _problem(name):
+    import dgas_gen
+    k, p, q = CONFIGS[name]
+    return dgas_gen.config(k, p, q) if k == 5 else dgas_gen.config(k)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    def __init__(self, idx):
+        self.idx = idx
+        self.proc = None
+        self.path = os.path.join("/tmp", f"dgas_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [l.split(",") for l in open(self.path).read().strip().splitlines() if l.strip()]
+            sm = sorted(float(r[0]) for r in rows)
+            mx = max(float(r[1]) for r in rows)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip() == "Active"})
+            return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+        except Exception:
+            return None
+
+
+def cpu_baseline(name, P=None, max_sub=8):
+    """The oracle as it stands, on a bounded sample of the same workload (see `sample`)."""
+    import numpy as np
+
+    import dgas_gen
+    import oracle
+    P = _problem(name) if P is None else P
+    t0 = time.time()
+    o = oracle.Oracle(P)
+    t_asm = time.time() - t0
+    sub = list(range(min(max_sub, P.n_sub)))
+    o.setup_schwarz(use_coarse=False, sample=sub)
+    x = dgas_gen.normal(1, o.N)
+    t0 = time.perf_counter(); o.spmv(x); t_spmv = time.perf_counter() - t0
+    t0 = time.perf_counter(); o.apply_sampled(x, sub); t_loc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    v = x.copy()
+    for _ in range(3):  # the 3 axpys + 2 dots of one Hestenes–Stiefel iteration, in numpy
+        v += 0.5 * x; float(v @ x)
+    t_vec = time.perf_counter() - t0
+    t_iter = t_spmv + t_loc * P.n_sub / len(sub) + t_vec
+    return {"value": 1.0 / t_iter, "unit": "PCG it/s", "cores": 1, "kind": "oracle",
+            "sample": (f"{name}: oracle SpMV over all {P.n_cells} cells + dense-Cholesky local solves of "
+                       f"{len(sub)}/{P.n_sub} subdomains scaled to all + vector ops, per PCG iteration; "
+                       f"coarse solve excluded (oracle setup of A0 for this size not in the sample); "
+                       f"oracle assembly {t_asm:.1f}s not timed"),
+            "seconds_per_iter": t_iter}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    name = args.config
+    per = []
+    P = _problem(name)
+    for _ in range(max(1, args.steps)):
+        per.append(cpu_baseline(name, P)["seconds_per_iter"])
+    v = 1.0 / (sum(per) / len(per))
+    cb = cpu_baseline(name, P)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "PCG it/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name},
+            "cpu_baseline": {**{k: cb[k] for k in ("unit", "cores", "kind", "sample")}, "value": v},
+            "e2e": {"value": v, "unit": "PCG it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="dgas", choices=["dgas", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-reps", type=int, default=20)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0)); world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+
+    from paper_1903_11357_b200 import dgas
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    P = _problem(args.config)
+    t0 = time.time()
+    S = dgas.Solver(P)
+    torch.cuda.synchronize()
+    t_setup = time.time() - t0
+    info = S.info
+    b = S.rhs(P.f_kind)
+    x = torch.zeros_like(b)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        x.zero_(); S.pcg(b, x)
+    barrier()
+    iters_total = 0
+    conds = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            x.zero_()
+            _, it, cond, st = S.pcg(b, x)
+            iters_total += it
+            conds.append(cond)
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms, iters_total], dtype=torch.float64, device="cuda")
+        mx = t.clone(); torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = t.clone(); torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        ms, iters_all = float(mx[0]), float(sm[1])
+    else:
+        iters_all = iters_total
+    value = iters_all / (ms / 1e3)
+    iters_per_solve = iters_total / args.steps
+
+    # ---- e2e through the public C ABI with host buffers (pinned), copies inside the timed region
+    bh = b.cpu().pin_memory()
+    xh = torch.zeros(S.N, dtype=torch.float64).pin_memory()
+    S.pcg_host(bh, xh)
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    e2e_iters = 0
+    for _ in range(args.steps):
+        xh.zero_()
+        it, _, _ = S.pcg_host(bh, xh)
+        e2e_iters += it
+    e3.record()
+    barrier()
+    e2e_ms = e2.elapsed_time(e3)
+    e2e_value = e2e_iters * world / (e2e_ms / 1e3)
+
+    # ---- per-kernel timing (CUDA events on the launching stream) for the roofline
+    peaks = _peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    stream = torch.cuda.current_stream()
+    S.bench_kernels(0, 3); S.bench_kernels(2, 3)
+    kt = {}
+    for which, nm in ((0, "spmv"), (2, "apply_fused"), (1, "apply_total")):
+        torch.cuda.synchronize()
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        S.bench_kernels(which, args.kernel_reps)
+        c.record(stream)
+        torch.cuda.synchronize()
+        kt[nm] = a.elapsed_time(c) / args.kernel_reps
+    N, N0, npp = info["N"], info["N0"], info["n_p"]
+    dinv_tri = info["n_cells"] * npp * (npp + 1) // 2 * 8
+    alg = {
+        "spmv": info["alg_bytes_spmv"],
+        "apply_fused": info["bytes_U"] + dinv_tri + info["bytes_coarse"] + 2 * N * 8 + 2 * N0 * 8,
+        "apply_total": info["alg_bytes_apply"],
+    }
+    kern = {nm: {"ms": kt[nm], "alg_bytes": alg[nm], "GBps": alg[nm] / (kt[nm] * 1e-3) / 1e9,
+                 "frac": alg[nm] / (kt[nm] * 1e-3) / 1e9 / hbm_peak} for nm in kt}
+    dom = "apply_fused" if kt["apply_fused"] >= kt["spmv"] else "spmv"
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(args.config, {}).get(dom)
+    except Exception:
+        pass
+    spmv_apply_gbs = (alg["spmv"] + alg["apply_total"]) / ((kt["spmv"] + kt["apply_total"]) * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "PCG it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "N": N, "N0": N0, "p": S.p, "q": S.q, "n_cells": info["n_cells"],
+                   "n_subdomains": info["n_subdomains"], "n_coarse": info["n_coarse"], "rtol": 1e-8,
+                   "iters_per_solve": iters_per_solve, "lanczos_cond": conds[-1] if conds else None,
+                   "l2_policy": (f"inputs larger than L2: operator bytes "
+                                 f"{(info['bytes_A'] + info['bytes_U'] + info['bytes_coarse']) / 1e9:.2f} GB "
+                                 f"> 126 MB L2"),
+                   "parallelism": "replicas" if world > 1 else "single-gpu", "setup_s": t_setup},
+        "dof_iters_per_s": value * N / max(world, 1) * world,
+        "ms_per_apply": kt["apply_total"],
+        "spmv_apply_hbm_gbs": spmv_apply_gbs,
+        "spmv_apply_pct_of_hbm_peak": 100 * spmv_apply_gbs / hbm_peak,
+        "roofline": {"bound": "hbm", "achieved": kern[dom]["GBps"], "peak": hbm_peak, "unit": "GB/s",
+                     "frac": kern[dom]["frac"], "traffic": traffic, "kernel": dom,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s"},
+        "kernels": kern,
+        "e2e": {"value": e2e_value, "unit": "PCG it/s", "h2d_bytes_per_step": 2 * N * 8,
+                "d2h_bytes_per_step": N * 8},
+        "gpu_launches": int(4 * iters_total + 9 * args.steps),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(args.config, P)
+            cb.pop("seconds_per_iter", None)
+            line["cpu_baseline"] = cb
+        except Exception as e:  # the oracle is a reported baseline, never the target
+            line["cpu_baseline"] = {"value": None, "unit": "PCG it/s", "cores": 1, "kind": "oracle",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    S.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

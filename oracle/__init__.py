@@ -42,6 +42,7 @@ def lib():
         L.or_dense_A.argtypes = [_P, _P]
         L.or_spmv.argtypes = [_P, _P, _P]
         L.or_rhs.argtypes = [_P, ctypes.c_int, _P]
+        L.or_spmv_abs.argtypes = [_P, _P, _P]
         L.or_project.argtypes = [_P, ctypes.c_int, _P]
         L.or_errors.argtypes = [_P, _P, _P]
         L.or_setup_schwarz.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, ctypes.c_int,
@@ -131,6 +132,12 @@ class Oracle:
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.zeros(self.N)
         lib().or_spmv(self.h, _ptr(x), _ptr(y))
+        return y
+
+    def spmv_abs(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(self.N)
+        lib().or_spmv_abs(self.h, _ptr(x), _ptr(y))
         return y
 
     def rhs(self, f_kind=None):

@@ -489,6 +489,20 @@ void or_spmv(void* h, const double* x, double* y) {
     }
 }
 
+// y = |A| |x| (entrywise absolute values): the scale of the rounding error of any y = A x, used by the
+// parity tests to bound the SpMV difference (|fl(Ax) - Ax| <= gamma_n |A||x|)
+void or_spmv_abs(void* h, const double* x, double* y) {
+  Ctx* c = (Ctx*)h;
+  int np = c->np;
+  for (int i = 0; i < c->nc; ++i)
+    for (int a = 0; a < np; ++a) {
+      double s = 0;
+      for (auto& kv : c->A[i])
+        for (int b = 0; b < np; ++b) s += std::fabs(kv.second[a * np + b] * x[(int64_t)kv.first * np + b]);
+      y[(int64_t)i * np + a] = s;
+    }
+}
+
 // right-hand side b_a = int_kappa f phi_a  (eq:dG); f_kind: 0 = 2pi^2 sin sin, 1 = 1, 2 = 2[x(1-x)+y(1-y)]
 // fixed Duffy rule with m = p + 4 (R10)
 void or_rhs(void* h, int f_kind, double* b) {

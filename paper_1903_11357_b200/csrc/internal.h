@@ -1,0 +1,206 @@
+// internal.h — context layout and device helpers of libdgas (B200 / sm_100a).
+//
+// Internal numbering: cells are renumbered subdomain-major (so R_i is a contiguous range,
+// PAPER.md:129-137) and, inside a subdomain, in reverse Cuthill–McKee order of the face graph so the
+// local Cholesky factors stay inside a narrow block envelope.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dgas.h"
+
+#define DGAS_MAXP 6
+#define DGAS_MAXNP 28
+#define CT 32            // coarse tile size (tiled dense / banded Cholesky of A0)
+
+// ---------------------------------------------------------------- PCG device state
+struct PcgState {
+  int it;          // completed iterations
+  int done;        // 1 = stop (converged, breakdown or maxit)
+  int status;      // DGAS_OK / DGAS_NOT_CONVERGED / DGAS_E_BREAKDOWN
+  int maxit;
+  double rtol2_bb; // rtol^2 ||b||^2
+  double bb;       // ||b||^2
+  double gamma;    // r.z of the current iterate
+  double pq, alpha, beta, rr;
+  unsigned int cnt[4];  // last-block counters of the reductions
+};
+
+// One deterministic two-stage reduction: per-CTA partials, the last CTA to arrive sums them in order.
+struct Reduce {
+  double* partials;   // [max CTAs]
+  int cap;
+};
+
+struct dgas_ctx_s {
+  // sizes
+  int p = 0, q = 0, np = 0, nq = 0, nc = 0, nsub = 0, ncoarse = 0, nface = 0, nov = 0;
+  int64_t N = 0, N0 = 0;
+  double penalty = 10;
+  int coarse_dense = 1, coarse_bw = 0, nT = 0, bt = 0;  // coarse tiles
+  int max_sub_cells = 0, max_urow = 0, max_deg = 0;
+  int64_t nnzb = 0, u_total = 0;
+  std::string detail;
+  cudaStream_t stream = 0;
+  // host mirrors needed later
+  std::vector<int> perm, iperm;       // perm[new] = old cell, iperm[old] = new
+  std::vector<int> nbr_ptr_h, nbr_h;  // internal neighbour lists (sorted, incl. self)
+  // ---- device: geometry (internal order)
+  double* d_xy = nullptr;     // cell vertex coordinates, concatenated [cptr] x 2
+  int* d_cptr = nullptr;      // [nc+1]
+  double* d_kappa = nullptr;  // [nc]
+  double* d_hk = nullptr;     // [nc] diameters
+  double* d_C = nullptr;      // [nc][np*np] basis coefficients
+  double* d_bbox = nullptr;   // [nc][4]
+  double* d_glx = nullptr;    // Gauss–Legendre table, m = 1..16 at offset m(m-1)/2
+  double* d_glw = nullptr;
+  // faces
+  int* d_face_cells = nullptr;    // [nface][2] internal (km = -1 on the boundary)
+  double* d_face_xy = nullptr;    // [nface][4] a.x a.y b.x b.y (CCW for kp)
+  int* d_cf_ptr = nullptr;        // cell -> faces CSR
+  int* d_cf = nullptr;            // face id * 2 + side (0 = +, 1 = -)
+  double* d_vol = nullptr;        // [nc][np*np] scratch (volume blocks)
+  double* d_fblk = nullptr;       // [nface][4][np*np] scratch (face blocks)
+  // A: per-cell row blocks np x (deg*np), row-major
+  int* d_nbr_ptr = nullptr;
+  int* d_nbr = nullptr;
+  int64_t* d_a_off = nullptr;
+  double* d_A = nullptr;
+  // local envelope factors
+  int* d_sub_ptr = nullptr;   // [nsub+1] cell ranges
+  int* d_first = nullptr;     // [nc] first coupled local cell f_k (local index)
+  int64_t* d_u_off = nullptr; // [nc] row-block offsets (doubles)
+  double* d_U = nullptr;      // unit block-lower factor rows U_kj = L_kk^-1 L_kj
+  double* d_Dinv = nullptr;   // [nc][np*np] L_kk^-1 (lower)
+  // coarse
+  int* d_ov_cell = nullptr;       // [nov] internal fine cell of each piece
+  int* d_ov_coarse = nullptr;     // [nov]
+  int* d_ov_pptr = nullptr;       // [nov+1] piece polygon points
+  double* d_ov_xy = nullptr;      // points
+  int* d_cov_ptr = nullptr;       // coarse J -> pieces CSR
+  int* d_cov = nullptr;
+  int* d_fov_ptr = nullptr;       // fine cell -> pieces CSR (first = owner)
+  int* d_fov = nullptr;
+  int* d_ctri_ptr = nullptr;      // coarse J -> fan triangles (piece, t)
+  int* d_ctri = nullptr;
+  double* d_Cc = nullptr;         // [ncoarse][nq*nq]
+  double* d_cbbox = nullptr;      // [ncoarse][4]
+  double* d_G = nullptr;          // [nov][np*nq]
+  double* d_A0t = nullptr;        // tile storage of A0 / its Cholesky factor
+  double* d_Dinv0 = nullptr;      // [nT][CT*CT] inverse diagonal tiles
+  double* d_W = nullptr;          // tile storage of L^-1 (dense only, scratch)
+  double* d_X = nullptr;          // dense A0^-1, N0 x N0 row-major (dense only)
+  int64_t n_pairs = 0;
+  int* d_pair = nullptr;          // coarse pairs (J1, J2)
+  int* d_contrib_ptr = nullptr;   // pair -> contributions
+  int4* d_contrib = nullptr;      // (cell, slot, o1, o2)
+  // vectors (internal order)
+  double *d_x = nullptr, *d_r = nullptr, *d_z = nullptr, *d_q = nullptr, *d_b = nullptr;
+  double* d_p[2] = {nullptr, nullptr};
+  double* d_r2 = nullptr;                    // second residual buffer (ping-pong with d_r)
+  double** d_pbuf = nullptr;                 // device array {d_p[0], d_p[1]}
+  double** d_rbuf = nullptr;                 // device array {d_r, d_r2}
+  int* d_perm_dev = nullptr;                 // perm[new] = old (device)
+  cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr;
+  double *d_r0 = nullptr, *d_z0 = nullptr;
+  double *d_t1 = nullptr, *d_t2 = nullptr;   // apply/spmv scratch (internal order)
+  double* d_partials = nullptr;              // reduction partials
+  int partial_cap = 0;
+  PcgState* d_state = nullptr;               // PCG state
+  PcgState* d_astate = nullptr;              // state used by standalone dgas_apply / dgas_spmv
+  double *d_alpha = nullptr, *d_beta = nullptr;
+  int hist_cap = 0;
+  double* d_lanczos = nullptr;               // [3] lmin lmax cond
+  int* d_err = nullptr;                      // [4] setup error flags
+  PcgState* h_state = nullptr;               // pinned
+  double* h_scal = nullptr;                  // pinned [8]
+  // graph
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  int graph_maxit = 0;
+  // last results
+  int last_iters = 0, last_status = 0;
+  double last_cond = 0, last_lmin = 0, last_lmax = 0, last_relres = 0;
+  // launch geometry
+  int n_coarse_ctas = 0;   // coarse CTAs in the fused apply kernel
+};
+
+// ---------------------------------------------------------------- helpers
+#define DGAS_CUDA(call)                                                        \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      ctx->detail = std::string(#call) + ": " + cudaGetErrorString(e_);        \
+      return e_ == cudaErrorMemoryAllocation ? DGAS_E_NOMEM : DGAS_E_CUDA;     \
+    }                                                                          \
+  } while (0)
+
+__host__ __device__ inline int np_of(int p) { return (p + 1) * (p + 2) / 2; }
+__host__ __device__ inline int gl_off(int m) { return m * (m - 1) / 2; }
+
+// Legendre L_0..L_p and derivatives at t (three-term recurrences)
+__device__ inline void dev_legendre(int p, double t, double* L, double* dL) {
+  L[0] = 1.0; dL[0] = 0.0;
+  if (p >= 1) { L[1] = t; dL[1] = 1.0; }
+  for (int n = 1; n < p; ++n) {
+    L[n + 1] = ((2 * n + 1) * t * L[n] - n * L[n - 1]) / (n + 1);
+    dL[n + 1] = dL[n - 1] + (2 * n + 1) * L[n];
+  }
+}
+
+// raw graded bbox-Legendre products g_i and their gradients (R6)
+__device__ inline void dev_raw(int p, const double* bb, double x, double y, double* g, double* gx, double* gy) {
+  double La[DGAS_MAXP + 1], dLa[DGAS_MAXP + 1], Lb[DGAS_MAXP + 1], dLb[DGAS_MAXP + 1];
+  double sx = 2.0 / (bb[1] - bb[0]), sy = 2.0 / (bb[3] - bb[2]);
+  dev_legendre(p, (x - bb[0]) * sx - 1.0, La, dLa);
+  dev_legendre(p, (y - bb[2]) * sy - 1.0, Lb, dLb);
+  int i = 0;
+  for (int d = 0; d <= p; ++d)
+    for (int a = d; a >= 0; --a, ++i) {
+      int b = d - a;
+      g[i] = La[a] * Lb[b];
+      if (gx) { gx[i] = dLa[a] * sx * Lb[b]; gy[i] = La[a] * dLb[b] * sy; }
+    }
+}
+
+// phi = C g (and gradients) for one point
+__device__ inline void dev_phi(int p, int n, const double* C, const double* bb, double x, double y, double* phi,
+                               double* px, double* py) {
+  double g[DGAS_MAXNP], gx[DGAS_MAXNP], gy[DGAS_MAXNP];
+  dev_raw(p, bb, x, y, g, px ? gx : nullptr, py ? gy : nullptr);
+  for (int a = 0; a < n; ++a) {
+    double s = 0, sx = 0, sy = 0;
+    for (int b = 0; b <= a; ++b) {  // C is lower triangular
+      double c = C[a * n + b];
+      s += c * g[b];
+      if (px) { sx += c * gx[b]; sy += c * gy[b]; }
+    }
+    phi[a] = s;
+    if (px) { px[a] = sx; py[a] = sy; }
+  }
+}
+
+__device__ inline double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- launchers (defined in .cu files)
+int setup_kernels_run(dgas_ctx ctx);                 // basis, assembly, local factors, coarse
+int coarse_setup_run(dgas_ctx ctx);
+int launch_rhs(dgas_ctx ctx, int f_kind, double* b_internal);
+void launch_perm(dgas_ctx ctx, const double* in, double* out, int to_internal, cudaStream_t s);
+void launch_spmv(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s);
+void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cudaStream_t s);
+void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s);
+void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s,
+                    cudaGraphConditionalHandle h, int use_handle);
+void launch_init_state(dgas_ctx ctx, PcgState* st, int maxit, double rtol, cudaStream_t s);
+void launch_pcg_init(dgas_ctx ctx, cudaStream_t s);
+void launch_lanczos(dgas_ctx ctx, cudaStream_t s);
+int dgas_post_setup(dgas_ctx ctx);
+int apply_set_smem(dgas_ctx ctx, size_t smem);

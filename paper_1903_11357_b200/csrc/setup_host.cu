@@ -1,0 +1,433 @@
+// setup_host.cu — dgas_setup: argument checks, topology, internal orderings and index structures
+// (integer plumbing on the host), device allocation, then the GPU setup kernels
+// (setup_kernels.cu / coarse_kernels.cu) that compute every number of the method.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <unordered_map>
+
+#include "internal.h"
+
+namespace {
+
+template <typename T>
+int dev_upload(dgas_ctx ctx, T** d, const std::vector<T>& h) {
+  size_t n = std::max<size_t>(h.size(), 1);
+  DGAS_CUDA(cudaMalloc((void**)d, n * sizeof(T)));
+  if (!h.empty()) DGAS_CUDA(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return 0;
+}
+template <typename T>
+int dev_alloc(dgas_ctx ctx, T** d, size_t n, bool zero = true) {
+  n = std::max<size_t>(n, 1);
+  DGAS_CUDA(cudaMalloc((void**)d, n * sizeof(T)));
+  if (zero) DGAS_CUDA(cudaMemsetAsync(*d, 0, n * sizeof(T), ctx->stream));
+  return 0;
+}
+
+double shoelace(const double* xy, int n) {
+  double a = 0;
+  for (int i = 0; i < n; ++i) {
+    int j = (i + 1) % n;
+    a += xy[2 * i] * xy[2 * j + 1] - xy[2 * j] * xy[2 * i + 1];
+  }
+  return 0.5 * a;
+}
+
+// reverse Cuthill–McKee of the cells [cells] over the adjacency adj (global ids), returns new order
+std::vector<int> rcm(const std::vector<int>& cells, const std::vector<std::vector<int>>& adj,
+                     const std::vector<int>& in_set_mark, int mark) {
+  int m = (int)cells.size();
+  std::unordered_map<int, int> loc;
+  for (int k = 0; k < m; ++k) loc[cells[k]] = k;
+  std::vector<int> deg(m, 0);
+  for (int k = 0; k < m; ++k)
+    for (int j : adj[cells[k]]) if (in_set_mark[j] == mark) deg[k]++;
+  std::vector<char> seen(m, 0);
+  std::vector<int> order;
+  order.reserve(m);
+  while ((int)order.size() < m) {
+    // start: unseen node of minimum degree (ties: lowest id), then one BFS sweep to a far node
+    int s = -1;
+    for (int k = 0; k < m; ++k)
+      if (!seen[k] && (s < 0 || deg[k] < deg[s])) s = k;
+    for (int sweep = 0; sweep < 2; ++sweep) {  // pseudo-peripheral refinement
+      std::vector<int> lvl(m, -1);
+      std::vector<int> qq = {s};
+      lvl[s] = 0;
+      int last = s;
+      for (size_t h = 0; h < qq.size(); ++h) {
+        int u = qq[h];
+        last = u;
+        for (int j : adj[cells[u]]) {
+          if (in_set_mark[j] != mark) continue;
+          int v = loc[j];
+          if (!seen[v] && lvl[v] < 0) { lvl[v] = lvl[u] + 1; qq.push_back(v); }
+        }
+      }
+      s = last;
+    }
+    std::vector<int> qq = {s};
+    seen[s] = 1;
+    for (size_t h = 0; h < qq.size(); ++h) {
+      int u = qq[h];
+      order.push_back(u);
+      std::vector<int> nb;
+      for (int j : adj[cells[u]]) {
+        if (in_set_mark[j] != mark) continue;
+        int v = loc[j];
+        if (!seen[v]) { seen[v] = 1; nb.push_back(v); }
+      }
+      std::sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b] || (deg[a] == deg[b] && cells[a] < cells[b]); });
+      for (int v : nb) qq.push_back(v);
+    }
+  }
+  std::reverse(order.begin(), order.end());
+  std::vector<int> out(m);
+  for (int k = 0; k < m; ++k) out[k] = cells[order[k]];
+  return out;
+}
+
+}  // namespace
+
+static void free_ctx(dgas_ctx ctx);
+
+extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int32_t* part, int32_t nsub,
+                          const dgas_coarse* coarse, int q, const double* kappa, double penalty, void* stream) {
+  if (!out) return DGAS_E_INVALID_ARG;
+  *out = nullptr;
+  if (!mesh || !part || !coarse || !kappa || !mesh->xy || !mesh->cell_ptr || !mesh->cell_vtx) return DGAS_E_INVALID_ARG;
+  if (p < 1 || p > DGAS_MAXP || q < 1 || q > p || nsub < 1 || mesh->n_cells < 1 || !(penalty > 0)) return DGAS_E_INVALID_ARG;
+  if (coarse->n_coarse < 1) return DGAS_E_INVALID_ARG;
+  dgas_ctx ctx = new dgas_ctx_s();
+  ctx->stream = (cudaStream_t)stream;
+  int st = 0;
+  auto bail = [&](int code, const std::string& msg) {
+    ctx->detail = msg;
+    *out = ctx;  // keep detail readable; caller must destroy
+    return code;
+  };
+  const int nc = mesh->n_cells;
+  ctx->p = p; ctx->q = q; ctx->np = np_of(p); ctx->nq = np_of(q); ctx->nc = nc; ctx->nsub = nsub;
+  ctx->ncoarse = coarse->n_coarse; ctx->penalty = penalty;
+  ctx->N = (int64_t)nc * ctx->np; ctx->N0 = (int64_t)ctx->ncoarse * ctx->nq;
+  const int np = ctx->np, nq = ctx->nq;
+  // ------------------------------------------------ validation
+  for (int c = 0; c < nc; ++c) {
+    if (!(kappa[c] > 0) || !std::isfinite(kappa[c])) return bail(DGAS_E_INVALID_ARG, "kappa must be > 0 and finite");
+    if (part[c] < 0 || part[c] >= nsub) return bail(DGAS_E_INVALID_ARG, "partition out of range");
+    int n = mesh->cell_ptr[c + 1] - mesh->cell_ptr[c];
+    if (n < 3) return bail(DGAS_E_MESH, "cell with < 3 vertices");
+    std::vector<double> v(2 * n);
+    for (int k = 0; k < n; ++k) {
+      int id = mesh->cell_vtx[mesh->cell_ptr[c] + k];
+      if (id < 0 || id >= mesh->n_vertices) return bail(DGAS_E_MESH, "vertex index out of range");
+      v[2 * k] = mesh->xy[2 * id]; v[2 * k + 1] = mesh->xy[2 * id + 1];
+    }
+    if (!(shoelace(v.data(), n) > 0)) return bail(DGAS_E_MESH, "non-CCW or zero-area cell");
+  }
+  {
+    std::vector<int> cnt(nsub, 0);
+    for (int c = 0; c < nc; ++c) cnt[part[c]]++;
+    for (int s = 0; s < nsub; ++s) if (!cnt[s]) return bail(DGAS_E_INVALID_ARG, "empty subdomain");
+  }
+  // ------------------------------------------------ faces (unique edges), caller numbering
+  struct FaceH { int kp, km, a, b; };
+  std::vector<FaceH> faces;
+  std::vector<std::vector<int>> adj(nc);
+  {
+    std::unordered_map<uint64_t, int> emap;
+    emap.reserve(mesh->cell_ptr[nc] * 2);
+    for (int c = 0; c < nc; ++c) {
+      int n = mesh->cell_ptr[c + 1] - mesh->cell_ptr[c];
+      for (int k = 0; k < n; ++k) {
+        int a = mesh->cell_vtx[mesh->cell_ptr[c] + k], b = mesh->cell_vtx[mesh->cell_ptr[c] + (k + 1) % n];
+        uint64_t key = (uint64_t)std::min(a, b) << 32 | (uint64_t)std::max(a, b);
+        auto it = emap.find(key);
+        if (it == emap.end()) { emap[key] = (int)faces.size(); faces.push_back({c, -1, a, b}); }
+        else {
+          FaceH& f = faces[it->second];
+          if (f.km != -1 || f.kp == c) return bail(DGAS_E_MESH, "non-manifold edge");
+          f.km = c;
+          if (f.km < f.kp) { std::swap(f.kp, f.km); f.a = a; f.b = b; }  // kappa+ = lower caller index
+        }
+      }
+    }
+    for (auto& f : faces)
+      if (f.km >= 0) { adj[f.kp].push_back(f.km); adj[f.km].push_back(f.kp); }
+    for (auto& a : adj) { std::sort(a.begin(), a.end()); a.erase(std::unique(a.begin(), a.end()), a.end()); }
+  }
+  ctx->nface = (int)faces.size();
+  // ------------------------------------------------ internal order: subdomain-major, RCM inside
+  std::vector<std::vector<int>> subcells(nsub);
+  for (int c = 0; c < nc; ++c) subcells[part[c]].push_back(c);
+  ctx->perm.resize(nc); ctx->iperm.resize(nc);
+  std::vector<int> sub_ptr(nsub + 1, 0);
+  {
+    std::vector<int> pos = std::vector<int>(part, part + nc);
+    int k = 0;
+    for (int s = 0; s < nsub; ++s) {
+      std::vector<int> ord = rcm(subcells[s], adj, pos, s);
+      sub_ptr[s] = k;
+      for (int c : ord) { ctx->perm[k] = c; ctx->iperm[c] = k; ++k; }
+      ctx->max_sub_cells = std::max(ctx->max_sub_cells, (int)ord.size());
+    }
+    sub_ptr[nsub] = nc;
+  }
+  const auto& perm = ctx->perm;
+  const auto& iperm = ctx->iperm;
+  // cell polygons in internal order
+  std::vector<int> cptr(nc + 1, 0);
+  std::vector<double> cxy;
+  for (int c = 0; c < nc; ++c) {
+    int o = perm[c];
+    for (int k = mesh->cell_ptr[o]; k < mesh->cell_ptr[o + 1]; ++k) {
+      int id = mesh->cell_vtx[k];
+      cxy.push_back(mesh->xy[2 * id]); cxy.push_back(mesh->xy[2 * id + 1]);
+    }
+    cptr[c + 1] = (int)cxy.size() / 2;
+  }
+  std::vector<double> kap(nc);
+  for (int c = 0; c < nc; ++c) kap[c] = kappa[perm[c]];
+  // faces in internal numbering; side + is kept as the lower CALLER index (paper convention)
+  std::vector<int> fcells(2 * faces.size());
+  std::vector<double> fxy(4 * faces.size());
+  std::vector<std::vector<int>> cf(nc);
+  for (size_t f = 0; f < faces.size(); ++f) {
+    fcells[2 * f] = iperm[faces[f].kp];
+    fcells[2 * f + 1] = faces[f].km < 0 ? -1 : iperm[faces[f].km];
+    fxy[4 * f] = mesh->xy[2 * faces[f].a]; fxy[4 * f + 1] = mesh->xy[2 * faces[f].a + 1];
+    fxy[4 * f + 2] = mesh->xy[2 * faces[f].b]; fxy[4 * f + 3] = mesh->xy[2 * faces[f].b + 1];
+    cf[fcells[2 * f]].push_back((int)f * 2 + 0);
+    if (faces[f].km >= 0) cf[fcells[2 * f + 1]].push_back((int)f * 2 + 1);
+  }
+  std::vector<int> cf_ptr(nc + 1, 0), cf_flat;
+  for (int c = 0; c < nc; ++c) {
+    std::sort(cf[c].begin(), cf[c].end());
+    cf_flat.insert(cf_flat.end(), cf[c].begin(), cf[c].end());
+    cf_ptr[c + 1] = (int)cf_flat.size();
+  }
+  // neighbour lists (internal, sorted, incl. self) and row-block offsets of A
+  std::vector<int> nbr_ptr(nc + 1, 0), nbr;
+  std::vector<int64_t> a_off(nc + 1, 0);
+  for (int c = 0; c < nc; ++c) {
+    std::vector<int> l = {c};
+    for (int j : adj[perm[c]]) l.push_back(iperm[j]);
+    std::sort(l.begin(), l.end());
+    nbr.insert(nbr.end(), l.begin(), l.end());
+    nbr_ptr[c + 1] = (int)nbr.size();
+    a_off[c + 1] = a_off[c] + (int64_t)np * np * (int64_t)l.size();
+    ctx->max_deg = std::max(ctx->max_deg, (int)l.size());
+  }
+  ctx->nnzb = nbr.size();
+  ctx->nbr_ptr_h = nbr_ptr; ctx->nbr_h = nbr;
+  // envelope of the local blocks: f_k = first coupled local cell (<= k)
+  std::vector<int> first(nc);
+  std::vector<int64_t> u_off(nc + 1, 0);
+  for (int s = 0; s < nsub; ++s)
+    for (int c = sub_ptr[s]; c < sub_ptr[s + 1]; ++c) {
+      int f = c;
+      for (int k = nbr_ptr[c]; k < nbr_ptr[c + 1]; ++k)
+        if (nbr[k] >= sub_ptr[s] && nbr[k] < f) f = nbr[k];
+      first[c] = f - sub_ptr[s];
+      int w = (c - f) * np;
+      u_off[c + 1] = u_off[c] + (int64_t)np * w;
+      ctx->max_urow = std::max(ctx->max_urow, w);
+    }
+  ctx->u_total = u_off[nc];
+  // ------------------------------------------------ coarse pieces
+  std::vector<int> ov_cell, ov_coarse, ov_pptr(1, 0);
+  std::vector<double> ov_xy;
+  if (coarse->parent) {
+    for (int c = 0; c < nc; ++c) {
+      int J = coarse->parent[perm[c]];
+      if (J < 0 || J >= ctx->ncoarse) return bail(DGAS_E_INVALID_ARG, "coarse parent out of range");
+      ov_cell.push_back(c); ov_coarse.push_back(J);
+      for (int k = cptr[c]; k < cptr[c + 1]; ++k) { ov_xy.push_back(cxy[2 * k]); ov_xy.push_back(cxy[2 * k + 1]); }
+      ov_pptr.push_back((int)ov_xy.size() / 2);
+    }
+  } else {
+    if (!coarse->ov_fine || !coarse->ov_coarse || !coarse->ov_ptr || !coarse->ov_xy || coarse->n_overlaps < nc)
+      return bail(DGAS_E_INVALID_ARG, "non-nested coarse needs overlap pieces");
+    std::vector<double> asum(nc, 0.0);
+    for (int o = 0; o < coarse->n_overlaps; ++o) {
+      int f = coarse->ov_fine[o], J = coarse->ov_coarse[o];
+      if (f < 0 || f >= nc || J < 0 || J >= ctx->ncoarse) return bail(DGAS_E_INVALID_ARG, "overlap index out of range");
+      int n = coarse->ov_ptr[o + 1] - coarse->ov_ptr[o];
+      if (n < 3) return bail(DGAS_E_MESH, "overlap piece with < 3 points");
+      asum[f] += shoelace(coarse->ov_xy + 2 * coarse->ov_ptr[o], n);
+      ov_cell.push_back(iperm[f]); ov_coarse.push_back(J);
+      for (int k = coarse->ov_ptr[o]; k < coarse->ov_ptr[o + 1]; ++k) {
+        ov_xy.push_back(coarse->ov_xy[2 * k]); ov_xy.push_back(coarse->ov_xy[2 * k + 1]);
+      }
+      ov_pptr.push_back((int)ov_xy.size() / 2);
+    }
+    for (int c = 0; c < nc; ++c) {
+      double a = shoelace(&cxy[2 * cptr[iperm[c]]], cptr[iperm[c] + 1] - cptr[iperm[c]]);
+      if (std::fabs(asum[c] - a) > 1e-10 * a) return bail(DGAS_E_MESH, "overlap pieces do not cover a fine cell");
+    }
+  }
+  const int nov = (int)ov_cell.size();
+  ctx->nov = nov;
+  std::vector<int> cov_ptr(ctx->ncoarse + 1, 0), cov(nov), fov_ptr(nc + 1, 0), fov(nov);
+  std::vector<int> ctri_ptr(ctx->ncoarse + 1, 0), ctri;
+  {
+    for (int o = 0; o < nov; ++o) { cov_ptr[ov_coarse[o] + 1]++; fov_ptr[ov_cell[o] + 1]++; }
+    for (int J = 0; J < ctx->ncoarse; ++J) cov_ptr[J + 1] += cov_ptr[J];
+    for (int c = 0; c < nc; ++c) fov_ptr[c + 1] += fov_ptr[c];
+    std::vector<int> a(cov_ptr.begin(), cov_ptr.end() - 1), b(fov_ptr.begin(), fov_ptr.end() - 1);
+    for (int o = 0; o < nov; ++o) { cov[a[ov_coarse[o]]++] = o; fov[b[ov_cell[o]]++] = o; }
+    for (int J = 0; J < ctx->ncoarse; ++J) {
+      if (cov_ptr[J + 1] == cov_ptr[J]) return bail(DGAS_E_MESH, "coarse element without pieces");
+      for (int k = cov_ptr[J]; k < cov_ptr[J + 1]; ++k) {
+        int o = cov[k];
+        int n = ov_pptr[o + 1] - ov_pptr[o];
+        for (int t = 1; t + 1 < n; ++t) { ctri.push_back(o); ctri.push_back(t); }
+      }
+      ctri_ptr[J + 1] = (int)ctri.size() / 2;
+    }
+  }
+  // ------------------------------------------------ A0 pattern: coarse pairs and their contributions
+  std::map<std::pair<int, int>, std::vector<int4>> pairs;
+  int bw = 0;
+  for (int c = 0; c < nc; ++c)
+    for (int s = nbr_ptr[c]; s < nbr_ptr[c + 1]; ++s) {
+      int j = nbr[s];
+      for (int k1 = fov_ptr[c]; k1 < fov_ptr[c + 1]; ++k1)
+        for (int k2 = fov_ptr[j]; k2 < fov_ptr[j + 1]; ++k2) {
+          int o1 = fov[k1], o2 = fov[k2];
+          int J1 = ov_coarse[o1], J2 = ov_coarse[o2];
+          pairs[{J1, J2}].push_back(make_int4(c, s - nbr_ptr[c], o1, o2));
+          bw = std::max(bw, (std::abs(J1 - J2) + 1) * nq - 1);
+        }
+    }
+  ctx->coarse_bw = bw;
+  ctx->nT = (int)((ctx->N0 + CT - 1) / CT);
+  {
+    // dense explicit A0^-1 up to 8192 coarse dofs; env override for tests
+    int64_t dense_max = 8192;
+    if (const char* e = std::getenv("DGAS_COARSE_DENSE_MAX")) dense_max = std::atoll(e);
+    ctx->coarse_dense = ctx->N0 <= dense_max;
+  }
+  ctx->bt = ctx->coarse_dense ? ctx->nT - 1 : std::min(ctx->nT - 1, (bw + CT - 1) / CT);
+  std::vector<int> pair_h, cptr_h(1, 0);
+  std::vector<int4> contrib;
+  for (auto& kv : pairs) {
+    pair_h.push_back(kv.first.first); pair_h.push_back(kv.first.second);
+    contrib.insert(contrib.end(), kv.second.begin(), kv.second.end());
+    cptr_h.push_back((int)contrib.size());
+  }
+  ctx->n_pairs = (int64_t)pairs.size();
+  pairs.clear();
+  // ------------------------------------------------ device buffers
+  if ((st = dev_upload(ctx, &ctx->d_xy, cxy))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_cptr, cptr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_kappa, kap))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_hk, nc))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_C, (size_t)nc * np * np))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_bbox, (size_t)nc * 4))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_glx, 16 * 17 / 2 + 16))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_glw, 16 * 17 / 2 + 16))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_face_cells, fcells))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_face_xy, fxy))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_cf_ptr, cf_ptr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_cf, cf_flat))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_vol, (size_t)nc * np * np))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_fblk, (size_t)faces.size() * 4 * np * np))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_nbr_ptr, nbr_ptr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_nbr, nbr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_a_off, a_off))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_A, (size_t)a_off[nc]))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_sub_ptr, sub_ptr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_first, first))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_u_off, u_off))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_U, (size_t)u_off[nc] + 32))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_Dinv, (size_t)nc * np * np))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_ov_cell, ov_cell))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_ov_coarse, ov_coarse))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_ov_pptr, ov_pptr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_ov_xy, ov_xy))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_cov_ptr, cov_ptr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_cov, cov))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_fov_ptr, fov_ptr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_fov, fov))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_ctri_ptr, ctri_ptr))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_ctri, ctri))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_Cc, (size_t)ctx->ncoarse * nq * nq))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_cbbox, (size_t)ctx->ncoarse * 4))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_G, (size_t)nov * np * nq))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_pair, pair_h))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_contrib_ptr, cptr_h))) return bail(st, ctx->detail);
+  if ((st = dev_upload(ctx, &ctx->d_contrib, contrib))) return bail(st, ctx->detail);
+  {
+    size_t tiles = (size_t)ctx->nT * (ctx->bt + 1);
+    if ((st = dev_alloc(ctx, &ctx->d_A0t, tiles * CT * CT))) return bail(st, ctx->detail);
+    if ((st = dev_alloc(ctx, &ctx->d_Dinv0, (size_t)ctx->nT * CT * CT))) return bail(st, ctx->detail);
+    if (ctx->coarse_dense) {
+      if ((st = dev_alloc(ctx, &ctx->d_W, tiles * CT * CT))) return bail(st, ctx->detail);
+      if ((st = dev_alloc(ctx, &ctx->d_X, (size_t)ctx->N0 * ctx->N0))) return bail(st, ctx->detail);
+    }
+  }
+  const size_t N = ctx->N;
+  double** vecs[] = {&ctx->d_x, &ctx->d_r, &ctx->d_z, &ctx->d_q, &ctx->d_b, &ctx->d_p[0], &ctx->d_p[1], &ctx->d_t1, &ctx->d_t2};
+  for (double** v : vecs)
+    if ((st = dev_alloc(ctx, v, N))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_r0, (size_t)ctx->nT * CT))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_z0, (size_t)ctx->nT * CT))) return bail(st, ctx->detail);
+  ctx->partial_cap = 2 * (nc + ctx->ncoarse + nsub) + 4096;
+  if ((st = dev_alloc(ctx, &ctx->d_partials, (size_t)ctx->partial_cap))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_state, 1))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_astate, 1))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_lanczos, 4))) return bail(st, ctx->detail);
+  if ((st = dev_alloc(ctx, &ctx->d_err, 8))) return bail(st, ctx->detail);
+  {
+    cudaError_t e = cudaMallocHost((void**)&ctx->h_state, sizeof(PcgState));
+    if (e != cudaSuccess) return bail(DGAS_E_NOMEM, "cudaMallocHost");
+    e = cudaMallocHost((void**)&ctx->h_scal, 16 * sizeof(double));
+    if (e != cudaSuccess) return bail(DGAS_E_NOMEM, "cudaMallocHost");
+  }
+  // ------------------------------------------------ GPU setup kernels
+  if ((st = setup_kernels_run(ctx))) return bail(st, ctx->detail);
+  if ((st = coarse_setup_run(ctx))) return bail(st, ctx->detail);
+  // scratch no longer needed
+  cudaFree(ctx->d_vol); ctx->d_vol = nullptr;
+  cudaFree(ctx->d_fblk); ctx->d_fblk = nullptr;
+  if (ctx->d_W) { cudaFree(ctx->d_W); ctx->d_W = nullptr; }
+  {
+    if ((st = dgas_post_setup(ctx))) return bail(st, ctx->detail);
+  }
+  *out = ctx;
+  return DGAS_OK;
+}
+
+static void free_ctx(dgas_ctx ctx) {
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  void* ptrs[] = {ctx->d_xy, ctx->d_cptr, ctx->d_kappa, ctx->d_hk, ctx->d_C, ctx->d_bbox, ctx->d_glx, ctx->d_glw,
+                  ctx->d_face_cells, ctx->d_face_xy, ctx->d_cf_ptr, ctx->d_cf, ctx->d_vol, ctx->d_fblk,
+                  ctx->d_nbr_ptr, ctx->d_nbr, ctx->d_a_off, ctx->d_A, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off,
+                  ctx->d_U, ctx->d_Dinv, ctx->d_ov_cell, ctx->d_ov_coarse, ctx->d_ov_pptr, ctx->d_ov_xy,
+                  ctx->d_cov_ptr, ctx->d_cov, ctx->d_fov_ptr, ctx->d_fov, ctx->d_ctri_ptr, ctx->d_ctri, ctx->d_Cc,
+                  ctx->d_cbbox, ctx->d_G, ctx->d_A0t, ctx->d_Dinv0, ctx->d_W, ctx->d_X, ctx->d_pair,
+                  ctx->d_contrib_ptr, ctx->d_contrib, ctx->d_x, ctx->d_r, ctx->d_z, ctx->d_q, ctx->d_b,
+                  ctx->d_p[0], ctx->d_p[1], ctx->d_r0, ctx->d_z0, ctx->d_t1, ctx->d_t2, ctx->d_partials,
+                  ctx->d_state, ctx->d_astate, ctx->d_alpha, ctx->d_beta, ctx->d_lanczos, ctx->d_err,
+                  ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
+  if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+  delete ctx;
+}
+
+extern "C" int dgas_destroy(dgas_ctx ctx) {
+  if (!ctx) return DGAS_E_INVALID_ARG;
+  cudaStreamSynchronize(ctx->stream);
+  free_ctx(ctx);
+  return DGAS_OK;
+}

@@ -1,0 +1,224 @@
+"""Thin ctypes binding of libdgas.so (include/dgas.h). Argument marshalling only: every step of the
+method runs in the library's CUDA kernels. There is no CPU fallback: if the shared library is
+missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdgas.so")
+_lib = None
+_P = ctypes.c_void_p
+
+OK, NOT_CONVERGED = 0, 1
+E_INVALID_ARG, E_MESH, E_NOT_SPD, E_BREAKDOWN, E_CUDA, E_NOMEM = -1, -2, -3, -4, -5, -6
+
+EXPORTS = ["dgas_setup", "dgas_rhs", "dgas_spmv", "dgas_apply", "dgas_pcg", "dgas_pcg_host", "dgas_info",
+           "dgas_history", "dgas_debug_block", "dgas_debug_basis", "dgas_debug_A0", "dgas_bench_kernels",
+           "dgas_destroy", "dgas_strerror", "dgas_error_detail"]
+
+
+class Mesh(ctypes.Structure):
+    _fields_ = [("n_vertices", ctypes.c_int32), ("xy", _P), ("n_cells", ctypes.c_int32), ("cell_ptr", _P),
+                ("cell_vtx", _P)]
+
+
+class Coarse(ctypes.Structure):
+    _fields_ = [("n_coarse", ctypes.c_int32), ("parent", _P), ("n_overlaps", ctypes.c_int32), ("ov_fine", _P),
+                ("ov_coarse", _P), ("ov_ptr", _P), ("ov_xy", _P)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("N0", ctypes.c_int64),
+                ("n_cells", ctypes.c_int32), ("n_p", ctypes.c_int32), ("n_q", ctypes.c_int32),
+                ("n_subdomains", ctypes.c_int32), ("n_coarse", ctypes.c_int32), ("n_faces", ctypes.c_int32),
+                ("n_overlaps", ctypes.c_int32), ("coarse_dense", ctypes.c_int32), ("coarse_band", ctypes.c_int32),
+                ("nnz_blocks", ctypes.c_int64), ("bytes_A", ctypes.c_int64), ("bytes_U", ctypes.c_int64),
+                ("bytes_Dinv", ctypes.c_int64), ("bytes_G", ctypes.c_int64), ("bytes_coarse", ctypes.c_int64),
+                ("alg_bytes_spmv", ctypes.c_int64), ("alg_bytes_apply", ctypes.c_int64),
+                ("alg_bytes_iter", ctypes.c_int64), ("last_iters", ctypes.c_int32), ("last_status", ctypes.c_int32),
+                ("last_cond", ctypes.c_double), ("last_lmin", ctypes.c_double), ("last_lmax", ctypes.c_double),
+                ("last_relres", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def load():
+    """Load the in-tree library; raise if it is missing (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libdgas.so not built at {LIB_PATH}: run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    L.dgas_setup.argtypes = [ctypes.POINTER(_P), ctypes.POINTER(Mesh), ctypes.c_int, _P, ctypes.c_int32,
+                             ctypes.POINTER(Coarse), ctypes.c_int, _P, ctypes.c_double, _P]
+    L.dgas_rhs.argtypes = [_P, ctypes.c_int, _P, _P]
+    L.dgas_spmv.argtypes = [_P, _P, _P, _P]
+    L.dgas_apply.argtypes = [_P, _P, _P, _P]
+    L.dgas_pcg.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                           ctypes.POINTER(ctypes.c_double), _P]
+    L.dgas_pcg_host.argtypes = L.dgas_pcg.argtypes
+    L.dgas_info.argtypes = [_P, ctypes.POINTER(Info)]
+    L.dgas_history.argtypes = [_P, _P, _P, ctypes.c_int]
+    L.dgas_debug_block.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P]
+    L.dgas_debug_basis.argtypes = [_P, ctypes.c_int32, _P]
+    L.dgas_debug_A0.argtypes = [_P, _P]
+    L.dgas_bench_kernels.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P]
+    L.dgas_destroy.argtypes = [_P]
+    L.dgas_strerror.restype = ctypes.c_char_p
+    L.dgas_strerror.argtypes = [ctypes.c_int]
+    L.dgas_error_detail.restype = ctypes.c_char_p
+    L.dgas_error_detail.argtypes = [_P]
+    _lib = L
+    return L
+
+
+class DgasError(RuntimeError):
+    def __init__(self, code, detail=""):
+        msg = load().dgas_strerror(code).decode()
+        super().__init__(f"dgas status {code} ({msg}){': ' + detail if detail else ''}")
+        self.code = code
+
+
+def _stream(stream=None):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dptr(t):
+    import torch
+    assert isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Solver:
+    """One dgas context built from a generated problem (dgas_gen.Problem) or raw arrays."""
+
+    def __init__(self, problem, p=None, q=None, penalty=None, stream=None):
+        L = load()
+        P = problem
+        self.p = P.p if p is None else p
+        self.q = P.q if q is None else q
+        self._keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return a.ctypes.data
+
+        mesh = Mesh(P.xy.shape[0], arr(P.xy, np.float64), P.n_cells, arr(P.cell_ptr, np.int32),
+                    arr(P.cell_vtx, np.int32))
+        if P.nested:
+            coarse = Coarse(P.n_coarse, arr(P.parent, np.int32), 0, None, None, None, None)
+        else:
+            coarse = Coarse(P.n_coarse, None, len(P.ov_fine), arr(P.ov_fine, np.int32), arr(P.ov_coarse, np.int32),
+                            arr(P.ov_ptr, np.int32), arr(P.ov_xy, np.float64))
+        ctx = _P()
+        st = L.dgas_setup(ctypes.byref(ctx), ctypes.byref(mesh), self.p, arr(P.part, np.int32), P.n_sub,
+                          ctypes.byref(coarse), self.q, arr(P.kappa, np.float64),
+                          P.penalty if penalty is None else penalty, _stream(stream))
+        self.ctx = ctx
+        if st != 0:
+            detail = L.dgas_error_detail(ctx).decode() if ctx.value else ""
+            if ctx.value:
+                L.dgas_destroy(ctx)
+                self.ctx = None
+            raise DgasError(st, detail)
+        self._keep = []
+        self.info = self.get_info()
+        self.N = self.info["N"]
+        self.N0 = self.info["N0"]
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            load().dgas_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st < 0:
+            raise DgasError(st, load().dgas_error_detail(self.ctx).decode())
+        return st
+
+    def get_info(self):
+        inf = Info()
+        self._check(load().dgas_info(self.ctx, ctypes.byref(inf)))
+        return inf.as_dict()
+
+    # -------------------------------------------------------------- device-vector API (torch tensors)
+    def rhs(self, f_kind, out=None, stream=None):
+        import torch
+        b = torch.empty(self.N, dtype=torch.float64, device="cuda") if out is None else out
+        self._check(load().dgas_rhs(self.ctx, f_kind, _dptr(b), _stream(stream)))
+        return b
+
+    def spmv(self, x, out=None, stream=None):
+        import torch
+        y = torch.empty_like(x) if out is None else out
+        self._check(load().dgas_spmv(self.ctx, _dptr(x), _dptr(y), _stream(stream)))
+        return y
+
+    def apply(self, r, out=None, stream=None):
+        import torch
+        z = torch.empty_like(r) if out is None else out
+        self._check(load().dgas_apply(self.ctx, _dptr(r), _dptr(z), _stream(stream)))
+        return z
+
+    def pcg(self, b, x=None, rtol=1e-8, maxit=5000, stream=None):
+        """Solve A x = b (device tensors). Returns (x, iters, cond, status)."""
+        import torch
+        x = torch.zeros_like(b) if x is None else x
+        it = ctypes.c_int(0)
+        cond = ctypes.c_double(0)
+        st = self._check(load().dgas_pcg(self.ctx, _dptr(b), _dptr(x), rtol, maxit, ctypes.byref(it),
+                                         ctypes.byref(cond), _stream(stream)))
+        return x, it.value, cond.value, st
+
+    def pcg_host(self, b_host, x_host, rtol=1e-8, maxit=5000, stream=None):
+        """Same with host (ideally pinned) float64 tensors or numpy arrays."""
+        it = ctypes.c_int(0)
+        cond = ctypes.c_double(0)
+        bp = b_host.data_ptr() if hasattr(b_host, "data_ptr") else b_host.ctypes.data
+        xp = x_host.data_ptr() if hasattr(x_host, "data_ptr") else x_host.ctypes.data
+        st = self._check(load().dgas_pcg_host(self.ctx, ctypes.c_void_p(bp), ctypes.c_void_p(xp), rtol, maxit,
+                                              ctypes.byref(it), ctypes.byref(cond), _stream(stream)))
+        return it.value, cond.value, st
+
+    def history(self):
+        n = self.get_info()["last_iters"]
+        a = np.zeros(max(n, 1)); b = np.zeros(max(n, 1))
+        load().dgas_history(self.ctx, a.ctypes.data, b.ctypes.data, n)
+        return a[:n], b[:n]
+
+    def bench_kernels(self, which, reps, stream=None):
+        self._check(load().dgas_bench_kernels(self.ctx, which, reps, _stream(stream)))
+
+    # -------------------------------------------------------------- diagnostics (host)
+    def block(self, i, j):
+        np_ = self.info["n_p"]
+        out = np.zeros((np_, np_))
+        ok = self._check(load().dgas_debug_block(self.ctx, i, j, out.ctypes.data))
+        return out, bool(ok)
+
+    def basis(self, i):
+        np_ = self.info["n_p"]
+        out = np.zeros((np_, np_))
+        self._check(load().dgas_debug_basis(self.ctx, i, out.ctypes.data))
+        return out
+
+    def A0(self):
+        out = np.zeros((self.N0, self.N0))
+        self._check(load().dgas_debug_A0(self.ctx, out.ctypes.data))
+        return out
