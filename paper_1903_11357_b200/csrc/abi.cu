@@ -1,6 +1,7 @@
 // abi.cu — the remaining C-ABI entry points (include/dgas.h): rhs, spmv, apply, pcg (device-resident
 // loop: one CUDA graph whose WHILE conditional node runs PCG iterations until the device-side
 // convergence test clears the condition), info, history, diagnostics.
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -19,14 +20,75 @@ static int finish_setup_buffers(dgas_ctx ctx) {
   DGAS_CUDA(cudaMemcpyAsync(ctx->d_perm_dev, ctx->perm.data(), ctx->nc * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   DGAS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
   DGAS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking));
-  ctx->n_coarse_ctas = ctx->coarse_dense ? (int)std::min<int64_t>(296, std::max<int64_t>(1, ctx->N0 / 16)) : 1;
+  for (int i = 0; i < 3; ++i) {
+    DGAS_CUDA(cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking));
+    DGAS_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork[i], cudaEventDisableTiming));
+    DGAS_CUDA(cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming));
+  }
+  ctx->n_coarse_ctas = ctx->coarse_dense ? (int)std::min<int64_t>(592, std::max<int64_t>(1, ctx->N0 / 32)) : 1;
   {
-    size_t smem = (size_t)std::max(ctx->max_sub_cells * ctx->np, CT) * sizeof(double);
-    if (smem > 48 * 1024) {
-      // opt in to large dynamic shared memory for the fused apply kernel (all instantiations)
-      int st = apply_set_smem(ctx, smem);
-      if (st) return st;
+    // TMA ring of the local-solve CTAs: unit = CC columns of a row-block (about the average row-block
+    // for n_p = 15), S slots; 128-thread CTAs target ~55 KB (3-4 CTAs/SM), 256-thread ~110 KB.
+    // Invariant (else the forward/backward refill protocol would deadlock): a row-block spans at most
+    // S - 1 units, because the slots of a block are refilled only after that block's barrier.
+    ctx->ring_slots = 0;
+    {
+      // budget per CTA from the expected residency: all subdomains resident at once when possible
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const int T = local_threads(ctx->p);
+      const int per_sm = (ctx->nsub + nsm - 1) / nsm;
+      size_t b0 = per_sm <= 1 ? 200 * 1024 : per_sm <= 2 ? 105 * 1024 : per_sm <= 3 ? 70 * 1024 : 55 * 1024;
+      if (T == 256) b0 = std::max<size_t>(b0, 105 * 1024);
+      size_t budgets[2] = {b0, (size_t)200 * 1024};
+      size_t target = T == 128 ? 12 * 1024 : 24 * 1024;
+      if (const char* e = std::getenv("DGAS_APPLY_BUDGET_KB")) budgets[0] = budgets[1] = (size_t)std::atoi(e) * 1024;
+      if (const char* e = std::getenv("DGAS_APPLY_SLOT_KB")) target = (size_t)std::atoi(e) * 1024;
+      const int maxW = std::max(2, (ctx->max_urow + 1) / 2 * 2);
+      const size_t base = apply_smem_bytes(ctx);
+      const int CC0 = std::min(maxW, std::max(2, (int)(target / (8 * ctx->np)) / 2 * 2));
+      auto try_cc = [&](int CC, size_t budget) {
+        uint32_t sb = (uint32_t)(((((int64_t)CC * ctx->np + 1) / 2 * 2) * 8 + 127) / 128 * 128);
+        int S = (int)std::min<size_t>(64, (budget - std::min(budget, base)) / sb);
+        int units = (maxW + CC - 1) / CC;
+        if (S >= 3 && S >= units + 1) { ctx->ring_slots = S; ctx->slot_bytes = sb; ctx->ring_rows = CC; return true; }
+        return false;
+      };
+      for (size_t budget : budgets) {
+        bool ok = false;
+        for (int CC = CC0; CC >= 2 && !ok; CC -= 2) ok = try_cc(CC, budget);
+        for (int CC = CC0 + 2; CC <= maxW && !ok; CC += 2) ok = try_cc(CC, budget);
+        if (ok) break;
+      }
     }
+    if (ctx->ring_slots < 2) { ctx->detail = "subdomain row-block too large for shared memory"; return DGAS_E_INVALID_ARG; }
+    int st = apply_set_smem(ctx, apply_smem_bytes(ctx));
+    if (st) return st;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 3;  // measured best on B200 (tools/ab.sh): 3 CTAs/SM, 2-cell batches, ~64 KB rings
+    if (const char* e = std::getenv("DGAS_SPMV_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+    ctx->spmv_grid = std::min(ctx->nc, per_sm * nsm);
+    // SpMV ring: one slot per batch of G consecutive row-blocks of a CTA's cell range
+    {
+      const int G = spmv_batch_cells(ctx->p);
+      ctx->spmv_G = G;
+      if ((int64_t)G * ctx->max_deg * ctx->np > 4 * 256) { ctx->detail = "cell degree too large for the SpMV kernel"; return DGAS_E_INVALID_ARG; }
+      const int chunk = (ctx->nc + ctx->spmv_grid - 1) / ctx->spmv_grid;
+      int64_t mx = 0;
+      for (int c0 = 0; c0 < ctx->nc; c0 += chunk) {
+        const int c1 = std::min(ctx->nc, c0 + chunk);
+        for (int k0 = c0; k0 < c1; k0 += G) mx = std::max(mx, ctx->a_off_h[std::min(c1, k0 + G)] - ctx->a_off_h[k0]);
+      }
+      ctx->spmv_slot_bytes = (uint32_t)((mx * 8 + 127) / 128 * 128);
+      int64_t budget = 64 * 1024;
+      if (const char* e = std::getenv("DGAS_SPMV_BUDGET_KB")) budget = (int64_t)std::atoi(e) * 1024;
+      ctx->spmv_slots = (int)std::max<int64_t>(2, std::min<int64_t>(16, budget / ctx->spmv_slot_bytes));
+    }
+    st = spmv_set_smem(ctx, spmv_smem_bytes(ctx));
+    if (st) return st;
   }
   DGAS_CUDA(cudaStreamSynchronize(ctx->stream));
   return 0;
@@ -92,13 +154,38 @@ extern "C" int dgas_bench_kernels(dgas_ctx ctx, int which, int reps, void* strea
     if (which == 0) launch_spmv(ctx, 0, ctx->d_t1, ctx->d_t2, nullptr, s);
     else if (which == 1) apply_internal(ctx, s);
     else if (which == 2) launch_apply(ctx, 0, nullptr, ctx->d_t1, ctx->d_t2, s);
+    else if (which == 3) launch_local_only(ctx, ctx->d_t1, ctx->d_t2, s);
+    else if (which == 4) launch_coarse_only(ctx, s);
     else return DGAS_E_INVALID_ARG;
   }
   DGAS_CUDA(cudaGetLastError());
   return DGAS_OK;
 }
 
+static int build_graph_impl(dgas_ctx ctx, int maxit);
+
 static int build_graph(dgas_ctx ctx, int maxit) {
+  int st = build_graph_impl(ctx, maxit);
+  ctx->side_sel = 0;
+  if (st) {
+    // leave no capture open and no half-built graph behind
+    cudaGraph_t g = nullptr;
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(ctx->cap_stream2, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) cudaStreamEndCapture(ctx->cap_stream2, &g);
+    for (int i = 0; i < 3; ++i)
+      if (cudaStreamIsCapturing(ctx->side[i], &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) cudaStreamEndCapture(ctx->side[i], &g);
+    if (cudaStreamIsCapturing(ctx->cap_stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      cudaStreamEndCapture(ctx->cap_stream, &g);
+      if (g) cudaGraphDestroy(g);
+    }
+    if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
+    if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
+    cudaGetLastError();
+  }
+  return st;
+}
+
+static int build_graph_impl(dgas_ctx ctx, int maxit) {
   if (ctx->graph_exec && maxit <= ctx->hist_cap) return 0;
   if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
   if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
@@ -121,6 +208,7 @@ static int build_graph(dgas_ctx ctx, int maxit) {
   cudaGraphConditionalHandle h;
   DGAS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
   // init: r = b - A x0, r0 = Q^T r, z = P^-1 r, gamma_0 = r.z
+  ctx->side_sel = 1;
   launch_spmv(ctx, 0, ctx->d_x, ctx->d_q, nullptr, cs);
   launch_restrict(ctx, 2, st, nullptr, cs);
   launch_apply(ctx, 1, st, nullptr, ctx->d_z, cs);
@@ -135,12 +223,14 @@ static int build_graph(dgas_ctx ctx, int maxit) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   DGAS_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
   DGAS_CUDA(cudaStreamBeginCaptureToGraph(cs2, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  ctx->side_sel = 2;
   launch_spmv(ctx, 1, nullptr, ctx->d_q, st, cs2);
   launch_restrict(ctx, 1, st, nullptr, cs2);
   launch_apply(ctx, 2, st, nullptr, ctx->d_z, cs2);
   launch_prolong(ctx, 2, st, nullptr, ctx->d_z, cs2, h, 1);
   DGAS_CUDA(cudaGetLastError());
   DGAS_CUDA(cudaStreamEndCapture(cs2, &body));
+  ctx->side_sel = 0;
   launch_lanczos(ctx, cs);
   DGAS_CUDA(cudaStreamEndCapture(cs, &g));
   ctx->graph = g;
@@ -231,7 +321,7 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->bytes_U = ctx->u_total * 8;
   info->bytes_Dinv = (int64_t)ctx->nc * np * np * 8;
   info->bytes_G = (int64_t)ctx->nov * np * nq * 8;
-  info->bytes_coarse = ctx->coarse_dense ? ctx->N0 * ctx->N0 * 8
+  info->bytes_coarse = ctx->coarse_dense ? ctx->N0 * ctx->ldX * 8
                                          : (int64_t)ctx->nT * (ctx->bt + 1) * CT * CT * 8 + (int64_t)ctx->nT * CT * CT * 8;
   // algorithmic bytes: every operator entry read once, vectors once each
   info->alg_bytes_spmv = info->bytes_A + (2 * N) * 8 + (int64_t)ctx->nnzb * 4;
@@ -253,13 +343,11 @@ extern "C" int dgas_debug_block(dgas_ctx ctx, int32_t i, int32_t j, double* out)
   int deg = hi - lo, sl = -1;
   for (int k = lo; k < hi; ++k) if (ctx->nbr_h[k] == cj) sl = k - lo;
   if (sl < 0) return 0;
-  int64_t off = 0;
-  // row-block offset = sum of previous row sizes
-  for (int c = 0; c < ci; ++c) off += (int64_t)np * np * (ctx->nbr_ptr_h[c + 1] - ctx->nbr_ptr_h[c]);
+  const int64_t off = ctx->a_off_h[ci];
   std::vector<double> row((size_t)np * deg * np);
   DGAS_CUDA(cudaMemcpy(row.data(), ctx->d_A + off, row.size() * sizeof(double), cudaMemcpyDeviceToHost));
   for (int a = 0; a < np; ++a)
-    for (int b = 0; b < np; ++b) out[a * np + b] = row[(size_t)a * deg * np + sl * np + b];
+    for (int b = 0; b < np; ++b) out[a * np + b] = row[((size_t)sl * np + b) * np + a];
   return 1;
 }
 

@@ -143,15 +143,14 @@ __global__ void __launch_bounds__(128) k_A0(int n, int nqq, int bt, const int* p
   for (int k = cptr[pr]; k < cptr[pr + 1]; ++k) {
     int4 c4 = contrib[k];
     int cell = c4.x, sl = c4.y, o1 = c4.z, o2 = c4.w;
-    const int W = (nbr_ptr[cell + 1] - nbr_ptr[cell]) * n;
-    const double* Ab = A + a_off[cell] + sl * n;
+    const double* Ab = A + a_off[cell] + (size_t)sl * n * n;  // column-major block: (a, c) at c * n + a
     const double* G2 = G + (size_t)o2 * n * nqq;
     const double* G1 = G + (size_t)o1 * n * nqq;
     // T = A_ij G_o2  (n x nq)
     for (int e = threadIdx.x; e < n * nqq; e += blockDim.x) {
       int a = e / nqq, b = e % nqq;
       double v = 0;
-      for (int c = 0; c < n; ++c) v += Ab[(size_t)a * W + c] * G2[c * nqq + b];
+      for (int c = 0; c < n; ++c) v += Ab[(size_t)c * n + a] * G2[c * nqq + b];
       T[e] = v;
     }
     __syncthreads();
@@ -267,7 +266,7 @@ __global__ void __launch_bounds__(256) k_trtri_row(int I, int bt, const double* 
 }
 
 // X_IJ = sum_{K >= I} W_KI^T W_KJ (J <= I), written to the full row-major N0 x N0 matrix (both halves)
-__global__ void __launch_bounds__(256) k_lauum(int nT, int bt, int64_t N0, const double* Wt, double* X) {
+__global__ void __launch_bounds__(256) k_lauum(int nT, int bt, int64_t N0, int64_t ldX, const double* Wt, double* X) {
   int I = blockIdx.y, J = blockIdx.x;
   if (J > I) return;
   __shared__ double A[CT * (CT + 1)], B[CT * (CT + 1)];
@@ -288,7 +287,7 @@ __global__ void __launch_bounds__(256) k_lauum(int nT, int bt, int64_t N0, const
   }
   for (int e = threadIdx.x, s = 0; e < CT * CT; e += blockDim.x, ++s) {
     int64_t r = (int64_t)I * CT + e / CT, c = (int64_t)J * CT + e % CT;
-    if (r < N0 && c < N0) { X[r * N0 + c] = acc[s]; X[c * N0 + r] = acc[s]; }
+    if (r < N0 && c < N0) { X[r * ldX + c] = acc[s]; X[c * ldX + r] = acc[s]; }
   }
 }
 
@@ -320,7 +319,7 @@ int coarse_setup_run(dgas_ctx ctx) {
   DGAS_CUDA(cudaGetLastError());
   if (ctx->coarse_dense) {
     for (int I = 0; I < nT; ++I) k_trtri_row<<<I + 1, 256, 0, s>>>(I, bt, ctx->d_A0t, ctx->d_Dinv0, ctx->d_W);
-    k_lauum<<<dim3(nT, nT), 256, 0, s>>>(nT, bt, ctx->N0, ctx->d_W, ctx->d_X);
+    k_lauum<<<dim3(nT, nT), 256, 0, s>>>(nT, bt, ctx->N0, ctx->ldX, ctx->d_W, ctx->d_X);
     DGAS_CUDA(cudaGetLastError());
   }
   int herr[8];

@@ -48,6 +48,7 @@ struct dgas_ctx_s {
   // host mirrors needed later
   std::vector<int> perm, iperm;       // perm[new] = old cell, iperm[old] = new
   std::vector<int> nbr_ptr_h, nbr_h;  // internal neighbour lists (sorted, incl. self)
+  std::vector<int64_t> a_off_h;       // row-block offsets of A (doubles, 16-byte padded)
   // ---- device: geometry (internal order)
   double* d_xy = nullptr;     // cell vertex coordinates, concatenated [cptr] x 2
   int* d_cptr = nullptr;      // [nc+1]
@@ -92,7 +93,8 @@ struct dgas_ctx_s {
   double* d_A0t = nullptr;        // tile storage of A0 / its Cholesky factor
   double* d_Dinv0 = nullptr;      // [nT][CT*CT] inverse diagonal tiles
   double* d_W = nullptr;          // tile storage of L^-1 (dense only, scratch)
-  double* d_X = nullptr;          // dense A0^-1, N0 x N0 row-major (dense only)
+  double* d_X = nullptr;          // dense A0^-1, N0 x ldX row-major (dense only)
+  int64_t ldX = 0;
   int64_t n_pairs = 0;
   int* d_pair = nullptr;          // coarse pairs (J1, J2)
   int* d_contrib_ptr = nullptr;   // pair -> contributions
@@ -105,6 +107,9 @@ struct dgas_ctx_s {
   double** d_rbuf = nullptr;                 // device array {d_r, d_r2}
   int* d_perm_dev = nullptr;                 // perm[new] = old (device)
   cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr;
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};      // fork streams of the coarse solve
+  cudaEvent_t ev_fork[3] = {nullptr, nullptr, nullptr}, ev_join[3] = {nullptr, nullptr, nullptr};
+  int side_sel = 0;                                        // 0: direct calls, 1: init capture, 2: body capture
   double *d_r0 = nullptr, *d_z0 = nullptr;
   double *d_t1 = nullptr, *d_t2 = nullptr;   // apply/spmv scratch (internal order)
   double* d_partials = nullptr;              // reduction partials
@@ -126,6 +131,13 @@ struct dgas_ctx_s {
   double last_cond = 0, last_lmin = 0, last_lmax = 0, last_relres = 0;
   // launch geometry
   int n_coarse_ctas = 0;   // coarse CTAs in the fused apply kernel
+  int ring_slots = 2;      // TMA ring slots of the local-solve CTAs
+  uint32_t slot_bytes = 0; // bytes per slot (R rows of the widest U row-block, 128-aligned)
+  int ring_rows = 1;       // CC: columns of a row-block per stream unit
+  int spmv_slots = 2;
+  uint32_t spmv_slot_bytes = 0;
+  int spmv_grid = 0;
+  int spmv_G = 1;           // cells per SpMV batch (<= compile-time maximum)
 };
 
 // ---------------------------------------------------------------- helpers
@@ -204,3 +216,10 @@ void launch_pcg_init(dgas_ctx ctx, cudaStream_t s);
 void launch_lanczos(dgas_ctx ctx, cudaStream_t s);
 int dgas_post_setup(dgas_ctx ctx);
 int apply_set_smem(dgas_ctx ctx, size_t smem);
+size_t apply_smem_bytes(dgas_ctx ctx);
+size_t spmv_smem_bytes(dgas_ctx ctx);
+int spmv_batch_cells(int p);
+int local_threads(int p);
+void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s);
+void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);
+int spmv_set_smem(dgas_ctx ctx, size_t smem);

@@ -10,6 +10,8 @@
 #include <cfloat>
 
 #include "internal.h"
+#include "tma.cuh"
+#include <cstdlib>
 
 // ------------------------------------------------------------------ deterministic last-block sum
 template <int NT>
@@ -136,6 +138,172 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32) k_spmv(int mode, int nc, cons
   }
 }
 
+// ------------------------------------------------------------------ SpMV: persistent, batched, TMA ring
+// Each CTA owns a contiguous range of cell rows, processed in batches of G cells whose (contiguous,
+// column-major, 16-byte padded) row-blocks arrive by ONE cp.async.bulk per batch into a ring of S
+// shared-memory slots. Thread (g, a, q) of a batch computes the partial dot product of row a of cell
+// g over the columns col = q (mod SPTR); SPTR adjacent lanes finish it with shuffles. The input
+// columns of the next batch are gathered two batches ahead in a register pipeline (neighbour index,
+// then value), so no global load sits on the per-batch critical path.
+// mode 0: y = A x.  mode 1 (PCG): p_new = z + beta p_old (fused), q = A p_new, p.q -> alpha.
+#define SP_T 256
+#define SP_MAXE 4
+template <int NP>
+struct SpmvCfg {
+  static constexpr int TR = NP >= 21 ? 8 : 4;             // threads per row (adjacent lanes)
+  static constexpr int G = (SP_T / (NP * TR)) > 0 ? SP_T / (NP * TR) : 1;  // cells per batch
+};
+
+template <int NP>
+__global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, const int* __restrict__ nbr_ptr,
+                                                const int* __restrict__ nbr, const int64_t* __restrict__ a_off,
+                                                const double* __restrict__ A, const double* x, double* y,
+                                                const double* z, double* const* pbuf, PcgState* st,
+                                                double* partials, double* alpha_hist, int S, uint32_t slot_bytes,
+                                                int maxW, int G) {
+  constexpr int GMAX = SpmvCfg<NP>::G, SPTR = SpmvCfg<NP>::TR;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ double red[SP_T / 32];
+  __shared__ double wdot[SP_T / 32];
+  __shared__ double own[2][GMAX * NP];
+  int it = 0;
+  double beta = 0;
+  const double* pold = nullptr;
+  double* pnew = nullptr;
+  if (mode == 1) {
+    if (st->done) return;
+    it = st->it;
+    beta = it > 0 ? st->beta : 0.0;
+    pold = pbuf[it & 1];
+    pnew = pbuf[(it + 1) & 1];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c0 = min(nc, blockIdx.x * chunk), c1 = min(nc, c0 + chunk), ncell = c1 - c0;
+  const int nb = (ncell + G - 1) / G;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+  int64_t* ao_s = reinterpret_cast<int64_t*>(bars + 32);                  // a_off[c0 .. c1]
+  int* np_s = reinterpret_cast<int*>(ao_s + chunk + 2);                    // nbr_ptr[c0 .. c1]
+  const int xstride = G * ((maxW + 1) & ~1);
+  double* xs = reinterpret_cast<double*>(np_s + ((chunk + 2 + 3) & ~3));   // [2][G][maxW]
+  unsigned char* ring = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(xs + 2 * xstride) + 127) & ~(uintptr_t)127);
+  for (int k = threadIdx.x; k <= ncell; k += SP_T) { np_s[k] = nbr_ptr[c0 + k]; ao_s[k] = a_off[c0 + k]; }
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < S; ++t) mbar_init(&bars[t], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int bi) {
+    const int k0 = bi * G, k1 = min(ncell, k0 + G);
+    bulk_load(ring + (size_t)(bi % S) * slot_bytes, A + ao_s[k0], (uint32_t)((ao_s[k1] - ao_s[k0]) * 8), &bars[bi % S]);
+  };
+  if (threadIdx.x == 0)
+    for (int bi = 0; bi < nb && bi < S; ++bi) issue(bi);
+  auto colval = [&](int64_t id) -> double {
+    return mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
+  };
+  // gather stage A: entry e of batch bi -> (cell g, column col) -> global index (-1 if none)
+  int idxA[SP_MAXE], slotA[SP_MAXE];
+  auto stage_idx = [&](int bi, int* idx, int* slot) {
+    const int k0 = bi * G, k1 = min(ncell, k0 + G);
+    for (int t = 0; t < SP_MAXE; ++t) { idx[t] = -1; slot[t] = 0; }
+    if (bi >= nb) return;
+    int e = threadIdx.x, t = 0;
+    for (int k = k0; k < k1 && t < SP_MAXE; ++k) {
+      const int W = (np_s[k + 1] - np_s[k]) * NP;
+      while (e < W && t < SP_MAXE) {
+        idx[t] = __ldg(nbr + np_s[k] + e / NP) * NP + e % NP;
+        slot[t] = (k - k0) * ((maxW + 1) & ~1) + e;
+        e += SP_T; ++t;
+      }
+      e -= W;
+    }
+  };
+  int idxB[SP_MAXE], slotB[SP_MAXE], idxC[SP_MAXE], slotC[SP_MAXE];
+  double vB[SP_MAXE], vC[SP_MAXE];
+  auto publish = [&](int bi, const int* idx, const int* slot, const double* v) {  // values of batch bi -> xs
+    double* xn = xs + (bi & 1) * xstride;
+    const int nk0 = bi * G;
+    for (int t = 0; t < SP_MAXE; ++t)
+      if (idx[t] >= 0) {
+        xn[slot[t]] = v[t];
+        const int gg = slot[t] / ((maxW + 1) & ~1);
+        if (idx[t] / NP == c0 + nk0 + gg) own[bi & 1][gg * NP + idx[t] % NP] = v[t];
+      }
+  };
+  // prologue: batch 0 published, batch 1 values in registers (vB), batch 2 indices (idxC)
+  stage_idx(0, idxA, slotA);
+  for (int t = 0; t < SP_MAXE; ++t) vC[t] = idxA[t] >= 0 ? colval(idxA[t]) : 0.0;
+  publish(0, idxA, slotA, vC);
+  stage_idx(1, idxB, slotB);
+  for (int t = 0; t < SP_MAXE; ++t) vB[t] = idxB[t] >= 0 ? colval(idxB[t]) : 0.0;
+  stage_idx(2, idxC, slotC);
+  __syncthreads();
+  const int g = threadIdx.x / (NP * SPTR), a = (threadIdx.x / SPTR) % NP, q = threadIdx.x % SPTR;
+  uint32_t ph = 0;
+  double mydot = 0;
+  for (int bi = 0; bi < nb; ++bi) {
+    const int cur = bi & 1;
+    // values of batch bi+2 (in flight for two batch computes), indices of batch bi+3
+    for (int t = 0; t < SP_MAXE; ++t) vC[t] = idxC[t] >= 0 ? colval(idxC[t]) : 0.0;
+    stage_idx(bi + 3, idxA, slotA);
+    const int k0 = bi * G, kg = k0 + g;
+    mbar_wait(&bars[bi % S], (ph >> (bi % S)) & 1u);
+    ph ^= 1u << (bi % S);
+    if (g < G && kg < ncell) {
+      const int W = (np_s[kg + 1] - np_s[kg]) * NP;
+      const double* Ak = reinterpret_cast<const double*>(ring + (size_t)(bi % S) * slot_bytes) + (ao_s[kg] - ao_s[k0]) + a;
+      const double* xk = xs + cur * xstride + g * ((maxW + 1) & ~1);
+      double v0 = 0, v1 = 0;
+      int col = q;
+      for (; col + SPTR < W; col += 2 * SPTR) {
+        v0 += Ak[(size_t)col * NP] * xk[col];
+        v1 += Ak[(size_t)(col + SPTR) * NP] * xk[col + SPTR];
+      }
+      if (col < W) v0 += Ak[(size_t)col * NP] * xk[col];
+      double v = v0 + v1;
+#pragma unroll
+      for (int o = 1; o < SPTR; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (q == 0) {
+        const size_t id = (size_t)(c0 + kg) * NP + a;
+        y[id] = v;
+        if (mode == 1) {
+          const double pn = own[cur][g * NP + a];
+          pnew[id] = pn;
+          mydot += pn * v;
+        }
+      }
+    } else {
+      double v = 0;
+#pragma unroll
+      for (int o = 1; o < SPTR; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    publish(bi + 1, idxB, slotB, vB);  // xs[cur^1] is not read during batch bi
+    for (int t = 0; t < SP_MAXE; ++t) {
+      idxB[t] = idxC[t]; slotB[t] = slotC[t]; vB[t] = vC[t];
+      idxC[t] = idxA[t]; slotC[t] = slotA[t];
+    }
+    __syncthreads();  // batch bi+1 published; the ring slot of batch bi is free
+    if (threadIdx.x == 0 && bi + S < nb) issue(bi + S);
+  }
+  if (mode != 1) return;
+  mydot = warp_sum(mydot);
+  if (lane == 0) wdot[w] = mydot;
+  __syncthreads();
+  double tot[1] = {0};
+  if (threadIdx.x == 0)
+    for (int k = 0; k < SP_T / 32; ++k) tot[0] += wdot[k];
+  double res[1];
+  if (last_block<SP_T, 1>(tot, partials, &st->cnt[0], res, red)) {
+    if (threadIdx.x == 0) {
+      double pq = res[0];
+      st->pq = pq;
+      if (!(pq > 0) || !isfinite(pq)) { st->done = 1; st->status = DGAS_E_BREAKDOWN; }
+      else { st->alpha = st->gamma / pq; alpha_hist[it] = st->alpha; }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ update + restriction
 // mode 0: r0 = Q^T r_in (no update).  mode 1 (PCG iteration): r_new = r_old - alpha q (owner pieces
 // write r_new and x += alpha p_new), r.r -> convergence test, r0 = Q^T r_new.
@@ -222,136 +390,243 @@ __global__ void __launch_bounds__(RW * 32) k_restrict(int mode, const int* __res
   }
 }
 
-// ------------------------------------------------------------------ fused apply: coarse || local
-// blocks [0, ncc): coarse solve (dense: rows of X = A0^-1; banded: one CTA runs the tile sweeps)
-// blocks [ncc, ncc + nsub): exact local solve of subdomain s with the envelope factor:
-//   s = D^-1 r (parallel), U y = s (forward, row-oriented), U^T u = y (backward, column-oriented),
-//   z = D^-T u (parallel), where A_i = D U U^T D^T ... i.e. L = D^{-1}-scaled rows (see setup).
-#define AT 256
+// ------------------------------------------------------------------ coarse solve z0 = A0^-1 r0
+// dense: z0 = X r0 with the explicit inverse (warp per row, 4 x 16-byte streaming loads in flight per
+// lane); banded: one CTA runs the forward / backward tile sweeps of the band Cholesky factor.
+// Launched on a forked stream so it runs concurrently with the local solves (the paths join at I6).
+#define CO_T 256
+__global__ void __launch_bounds__(CO_T) k_coarse(int mode, int dense, int64_t N0, int64_t ldX, int nT, int bt,
+                                                 const double* __restrict__ X, const double* __restrict__ A0t,
+                                                 const double* __restrict__ Dinv0, const double* r0, double* z0,
+                                                 const PcgState* st) {
+  __shared__ double acc[CT];
+  if (mode >= 1 && st->done) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (dense) {
+    const int64_t rows_per = (N0 + gridDim.x - 1) / gridDim.x;
+    const int64_t r_lo = blockIdx.x * rows_per, r_hi = min(N0, r_lo + rows_per);
+    for (int64_t row = r_lo + w; row < r_hi; row += CO_T / 32) {
+      const double* xr = X + row * ldX;
+      double v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+      int64_t c = 2 * lane;
+      for (; c + 192 < N0; c += 256) {
+        const double2 a0 = __ldcs(reinterpret_cast<const double2*>(xr + c));
+        const double2 a1 = __ldcs(reinterpret_cast<const double2*>(xr + c + 64));
+        const double2 a2 = __ldcs(reinterpret_cast<const double2*>(xr + c + 128));
+        const double2 a3 = __ldcs(reinterpret_cast<const double2*>(xr + c + 192));
+        v0 += a0.x * __ldg(r0 + c) + a0.y * __ldg(r0 + c + 1);
+        v1 += a1.x * __ldg(r0 + c + 64) + a1.y * __ldg(r0 + c + 65);
+        v2 += a2.x * __ldg(r0 + c + 128) + a2.y * __ldg(r0 + c + 129);
+        v3 += a3.x * __ldg(r0 + c + 192) + a3.y * __ldg(r0 + c + 193);
+      }
+      for (; c < N0; c += 64) {
+        v0 += xr[c] * __ldg(r0 + c);
+        if (c + 1 < N0) v1 += xr[c + 1] * __ldg(r0 + c + 1);
+      }
+      const double v = warp_sum((v0 + v1) + (v2 + v3));
+      if (lane == 0) z0[row] = v;
+    }
+    return;
+  }
+  if (blockIdx.x != 0) return;
+  for (int64_t i = threadIdx.x; i < (int64_t)nT * CT; i += CO_T) z0[i] = i < N0 ? r0[i] : 0.0;
+  __syncthreads();
+  for (int I = 0; I < nT; ++I) {
+    for (int a = w; a < CT; a += CO_T / 32) {
+      double v = 0;
+      for (int K = max(0, I - bt); K < I; ++K) {
+        const double* t = A0t + ((size_t)I * (bt + 1) + (K - I + bt)) * CT * CT + a * CT;
+        v += t[lane] * z0[(size_t)K * CT + lane];
+      }
+      v = warp_sum(v);
+      if (lane == 0) acc[a] = z0[(size_t)I * CT + a] - v;
+    }
+    __syncthreads();
+    if (threadIdx.x < CT) {
+      const double* D = Dinv0 + (size_t)I * CT * CT + threadIdx.x * CT;
+      double v = 0;
+      for (int c = 0; c <= (int)threadIdx.x; ++c) v += D[c] * acc[c];
+      z0[(size_t)I * CT + threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+  for (int I = nT - 1; I >= 0; --I) {
+    if (threadIdx.x < CT) {
+      const int a = threadIdx.x;
+      double v = 0;
+      for (int c = a; c < CT; ++c) v += Dinv0[(size_t)I * CT * CT + c * CT + a] * z0[(size_t)I * CT + c];
+      acc[a] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < CT) z0[(size_t)I * CT + threadIdx.x] = acc[threadIdx.x];
+    __syncthreads();
+    const int K0 = max(0, I - bt);
+    for (int e = threadIdx.x; e < (I - K0) * CT; e += CO_T) {
+      int K = K0 + e / CT, col = e % CT;
+      const double* t = A0t + ((size_t)I * (bt + 1) + (K - I + bt)) * CT * CT + col;
+      double v = 0;
+      for (int a = 0; a < CT; ++a) v += t[a * CT] * acc[a];
+      z0[(size_t)K * CT + col] -= v;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ local solves z_i = A_i^-1 r_i
+// One CTA per subdomain: s = D^-1 r, U y = s (forward), U^T u = y (backward), z = D^-T u, with
+// A_i = L L^T, L = D_b^-1-scaled block envelope factor (setup_kernels.cu). Row-block U_k
+// (n x W_k, column-major) streams through a ring of S shared-memory slots by cp.async.bulk, in
+// units of CC columns; unit u lives in slot u % S. Forward consumes units in order and refills
+// slot u%S with unit u+S after the row-block's barrier; the last S units stay resident for the
+// backward sweep, which consumes units in reverse order and refills with unit u-S. One barrier per
+// row-block; the copies are issued by the CTA's last thread, idle in the forward step.
 template <int NP>
-__global__ void __launch_bounds__(AT) k_apply(int mode, int ncc, int dense, int64_t N0, int nT, int bt,
-                                              const double* __restrict__ X, const double* __restrict__ A0t,
-                                              const double* __restrict__ Dinv0, const double* r0, double* z0,
-                                              const int* __restrict__ sub_ptr, const int* __restrict__ first,
-                                              const int64_t* __restrict__ u_off, const double* __restrict__ U,
-                                              const double* __restrict__ Dinv, const double* r_in,
-                                              double* const* rbuf, double* z, PcgState* st) {
-  extern __shared__ double sm[];
-  // mode 0: r = r_in (standalone apply); 1: PCG init (rbuf[0]); 2: PCG iteration (rbuf[(it+1)&1])
+struct LocalCfg {
+  static constexpr int T = NP <= 15 ? 128 : 256;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(LocalCfg<NP>::T) k_local(int mode, const int* __restrict__ sub_ptr,
+                                                           const int* __restrict__ first,
+                                                           const int64_t* __restrict__ u_off,
+                                                           const double* __restrict__ U,
+                                                           const double* __restrict__ Dinv, const double* r_in,
+                                                           double* const* rbuf, double* z, const PcgState* st,
+                                                           int S, uint32_t slot_bytes, int ymax_cells, int CC) {
+  constexpr int T = LocalCfg<NP>::T;
+  extern __shared__ __align__(128) double sm[];
   const double* r = r_in;
   if (mode >= 1) {
     if (st->done) return;
     r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
   }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if ((int)blockIdx.x < ncc) {
-    if (dense) {
-      // z0 = X r0, warp per row
-      const int64_t rows_per = (N0 + ncc - 1) / ncc;
-      const int64_t r_lo = blockIdx.x * rows_per, r_hi = min(N0, r_lo + rows_per);
-      for (int64_t row = r_lo + w; row < r_hi; row += AT / 32) {
-        const double* xr = X + row * N0;
-        double v = 0;
-        for (int64_t c = lane; c < N0; c += 32) v += __ldcs(xr + c) * __ldg(r0 + c);
-        v = warp_sum(v);
-        if (lane == 0) z0[row] = v;
-      }
-    } else if (blockIdx.x == 0) {
-      // banded: forward L y = r0 then backward L^T x = y, by CT-row tiles (in place in z0)
-      for (int64_t i = threadIdx.x; i < (int64_t)nT * CT; i += AT) z0[i] = i < N0 ? r0[i] : 0.0;
-      __syncthreads();
-      double* acc = sm;  // CT
-      for (int I = 0; I < nT; ++I) {
-        for (int a = w; a < CT; a += AT / 32) {
-          double v = 0;
-          for (int K = max(0, I - bt); K < I; ++K) {
-            const double* t = A0t + ((size_t)I * (bt + 1) + (K - I + bt)) * CT * CT + a * CT;
-            v += t[lane] * z0[(size_t)K * CT + lane];
-          }
-          v = warp_sum(v);
-          if (lane == 0) acc[a] = z0[(size_t)I * CT + a] - v;
-        }
-        __syncthreads();
-        if (threadIdx.x < CT) {
-          const double* D = Dinv0 + (size_t)I * CT * CT + threadIdx.x * CT;
-          double v = 0;
-          for (int c = 0; c <= (int)threadIdx.x; ++c) v += D[c] * acc[c];
-          z0[(size_t)I * CT + threadIdx.x] = v;
-        }
-        __syncthreads();
-      }
-      for (int I = nT - 1; I >= 0; --I) {
-        if (threadIdx.x < CT) {
-          // x_I = D_I^T y_I
-          const int a = threadIdx.x;
-          double v = 0;
-          for (int c = a; c < CT; ++c) v += Dinv0[(size_t)I * CT * CT + c * CT + a] * z0[(size_t)I * CT + c];
-          acc[a] = v;
-        }
-        __syncthreads();
-        if (threadIdx.x < CT) z0[(size_t)I * CT + threadIdx.x] = acc[threadIdx.x];
-        __syncthreads();
-        // y_K -= L_IK^T x_I for K in [I-bt, I)
-        const int K0 = max(0, I - bt);
-        for (int e = threadIdx.x; e < (I - K0) * CT; e += AT) {
-          int K = K0 + e / CT, col = e % CT;
-          const double* t = A0t + ((size_t)I * (bt + 1) + (K - I + bt)) * CT * CT + col;
-          double v = 0;
-          for (int a = 0; a < CT; ++a) v += t[a * CT] * acc[a];
-          z0[(size_t)K * CT + col] -= v;
-        }
-        __syncthreads();
-      }
-    }
-    return;
-  }
-  // ---------------- local solve of subdomain s
-  const int s = blockIdx.x - ncc;
+  const int s = blockIdx.x;
   const int s0 = sub_ptr[s], m = sub_ptr[s + 1] - s0;
-  double* y = sm;
+  // layout (must match local_smem_offsets on the host): all offsets 8/128-byte aligned
+  const size_t off_us = 512 + (((size_t)(ymax_cells + 1) * 4 + 7) & ~(size_t)7);
+  const size_t off_uo = off_us + (((size_t)(ymax_cells + 2) * 4 + 7) & ~(size_t)7);
+  const size_t off_y = (off_uo + (size_t)ymax_cells * 8 + 127) & ~(size_t)127;
+  unsigned char* smb = reinterpret_cast<unsigned char*>(sm);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smb);
+  int* fk_s = reinterpret_cast<int*>(smb + 512);
+  int* us_s = reinterpret_cast<int*>(smb + off_us);                      // first unit of block k
+  int64_t* uo_s = reinterpret_cast<int64_t*>(smb + off_uo);
+  double* y = reinterpret_cast<double*>(smb + off_y);
+  unsigned char* ring = reinterpret_cast<unsigned char*>(y) + (((size_t)ymax_cells * NP * 8 + 127) & ~(size_t)127);
+  for (int k = threadIdx.x; k < m; k += T) { fk_s[k] = first[s0 + k]; uo_s[k] = u_off[s0 + k]; }
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < S; ++t) mbar_init(&bars[t], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // unit prefix: block k owns units [us_s[k], us_s[k+1])
+    int acc = 0;
+    us_s[0] = 0;
+    for (int k = 0; k < m; ++k) {
+      us_s[k] = acc;
+      acc += k == 0 ? 0 : ((k - fk_s[k]) * NP + CC - 1) / CC;
+    }
+    us_s[m] = acc;
+  }
+  __syncthreads();
+  const int nunits = us_s[m];
+  const int prod = T - 1;
+  if (threadIdx.x == 0)
+    for (int k = 1; k < m; ++k)
+      if (us_s[k + 1] - us_s[k] > S - 1) __trap();  // host guarantees it; never hang instead
+  auto unit_blk = [&](int u, int k, int& cA, int& cB) {
+    cA = (u - us_s[k]) * CC;
+    cB = min((k - fk_s[k]) * NP, cA + CC);
+  };
+  auto issue = [&](int u, int k) {
+    int cA, cB;
+    unit_blk(u, k, cA, cB);
+    const uint32_t nbytes = (uint32_t)((((int64_t)(cB - cA) * NP + 1) & ~1LL) * 8);
+    bulk_load(ring + (size_t)(u % S) * slot_bytes, U + uo_s[k] + (int64_t)cA * NP, nbytes, &bars[u % S]);
+  };
+  // block of unit u (units are few per block: walk from a hint)
+  auto blk_of = [&](int u, int hint) {
+    int k = hint;
+    while (us_s[k + 1] <= u) ++k;
+    while (us_s[k] > u) --k;
+    return k;
+  };
+  if (threadIdx.x == prod) {
+    int k = 1;
+    for (int u = 0; u < nunits && u < S; ++u) { k = blk_of(u, k); issue(u, k); }
+  }
+  uint64_t ph = 0;
   const double* rs = r + (size_t)s0 * NP;
-  for (int e = threadIdx.x; e < m * NP; e += AT) {
+  for (int e = threadIdx.x; e < m * NP; e += T) {
     const int k = e / NP, a = e % NP;
     const double* D = Dinv + ((size_t)(s0 + k) * NP + a) * NP;
     double v = 0;
-    for (int c = 0; c <= a; ++c) v += D[c] * rs[k * NP + c];
+    for (int c = 0; c <= a; ++c) v += __ldg(D + c) * rs[k * NP + c];
     y[e] = v;
   }
   __syncthreads();
+  // forward: thread (a, q) accumulates row a over columns col = q (mod 8) of every unit of U_k
+  const int fa = threadIdx.x >> 3, fq = threadIdx.x & 7;
+  int pk_hint = 1;
   for (int k = 1; k < m; ++k) {
-    const int fk = first[s0 + k], W = (k - fk) * NP;
-    if (W > 0) {
-      const double* Uk = U + u_off[s0 + k];
-      const double* yw = y + fk * NP;
-      for (int a = w; a < NP; a += AT / 32) {
-        double v = 0;
-        for (int col = lane; col < W; col += 32) v += __ldcs(Uk + a * W + col) * yw[col];
-        v = warp_sum(v);
-        if (lane == 0) y[k * NP + a] -= v;
+    const int u0 = us_s[k], u1 = us_s[k + 1];
+    if (u1 > u0) {
+      const double* yw = y + fk_s[k] * NP;
+      double v = 0;
+      for (int u = u0; u < u1; ++u) {
+        mbar_wait(&bars[u % S], (uint32_t)((ph >> (u % S)) & 1u));
+        ph ^= 1ull << (u % S);
+        int cA, cB;
+        unit_blk(u, k, cA, cB);
+        const double* Uc = reinterpret_cast<const double*>(ring + (size_t)(u % S) * slot_bytes);
+        if (fa < NP)
+          for (int col = cA + fq; col < cB; col += 8) v += Uc[(col - cA) * NP + fa] * yw[col];
       }
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      if (fa < NP && fq == 0) y[k * NP + fa] -= v;
     }
     __syncthreads();
+    if (threadIdx.x == prod)
+      for (int u = u0; u < u1; ++u)
+        if (u + S < nunits) { pk_hint = blk_of(u + S, pk_hint); issue(u + S, pk_hint); }
   }
+  // backward: u_k is final; y[f_k .. k) -= U_k^T u_k (thread per column)
+  pk_hint = m - 1;
   for (int k = m - 1; k > 0; --k) {
-    const int fk = first[s0 + k], W = (k - fk) * NP;
-    if (W > 0) {
-      const double* Uk = U + u_off[s0 + k];
+    const int u0 = us_s[k], u1 = us_s[k + 1];
+    if (u1 > u0) {
       const double* uk = y + k * NP;
-      for (int col = threadIdx.x; col < W; col += AT) {
-        double v = 0;
+      double* yw = y + fk_s[k] * NP;
+      for (int u = u1 - 1; u >= u0; --u) {
+        if (u < nunits - S) {
+          mbar_wait(&bars[u % S], (uint32_t)((ph >> (u % S)) & 1u));
+          ph ^= 1ull << (u % S);
+        }
+        int cA, cB;
+        unit_blk(u, k, cA, cB);
+        const double* Uc = reinterpret_cast<const double*>(ring + (size_t)(u % S) * slot_bytes);
+        for (int col = cA + threadIdx.x; col < cB; col += T) {
+          const double* uc = Uc + (size_t)(col - cA) * NP;
+          double v = 0;
 #pragma unroll
-        for (int a = 0; a < NP; ++a) v += Uk[a * W + col] * uk[a];
-        y[fk * NP + col] -= v;
+          for (int a = 0; a < NP; ++a) v += uc[a] * uk[a];
+          yw[col] -= v;
+        }
       }
     }
     __syncthreads();
+    if (threadIdx.x == prod)
+      for (int u = u1 - 1; u >= u0; --u)
+        if (u - S >= 0) { pk_hint = blk_of(u - S, pk_hint); issue(u - S, pk_hint); }
   }
   double* zs = z + (size_t)s0 * NP;
-  for (int e = threadIdx.x; e < m * NP; e += AT) {
+  for (int e = threadIdx.x; e < m * NP; e += T) {
     const int k = e / NP, a = e % NP;
     const double* D = Dinv + (size_t)(s0 + k) * NP * NP;
     double v = 0;
-    for (int c = a; c < NP; ++c) v += D[c * NP + a] * y[k * NP + c];
+    for (int c = a; c < NP; ++c) v += __ldg(D + c * NP + a) * y[k * NP + c];
     zs[e] = v;
   }
 }
@@ -515,11 +790,52 @@ void launch_perm(dgas_ctx ctx, const double* in, double* out, int to_internal, c
   k_perm<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ctx->nc, ctx->np, ctx->d_perm_dev, in, out, to_internal);
 }
 
+static int SpmvCfgMax(int p) {
+  int G = 1;
+  DISPATCH_P(p, (G = SpmvCfg<NP_>::G));
+  return G;
+}
+
+int spmv_batch_cells(int p) {
+  int G = 1;
+  DISPATCH_P(p, (G = SpmvCfg<NP_>::G));
+  G = std::min(G, 2);  // measured best on B200 (tools/ab.sh)
+  if (const char* e = std::getenv("DGAS_SPMV_G")) G = std::max(1, std::min(SpmvCfgMax(p), std::atoi(e)));
+  return G;
+}
+
+size_t spmv_smem_bytes(dgas_ctx ctx) {
+  const int chunk = (ctx->nc + ctx->spmv_grid - 1) / std::max(1, ctx->spmv_grid);
+  const int maxW = ctx->max_deg * ctx->np, G = spmv_batch_cells(ctx->p);
+  size_t b = 32 * 8 + (size_t)(chunk + 2) * 8 + (size_t)((chunk + 2 + 3) & ~3) * 4 + 2 * (size_t)G * ((maxW + 1) & ~1) * 8;
+  return ((b + 127) & ~(size_t)127) + (size_t)ctx->spmv_slots * ctx->spmv_slot_bytes + 128;
+}
+
 void launch_spmv(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s) {
-  unsigned grid = (ctx->nc + SPMV_WARPS - 1) / SPMV_WARPS;
-  DISPATCH_P(ctx->p, (k_spmv<NP_><<<grid, SPMV_WARPS * 32, 0, s>>>(mode, ctx->nc, ctx->d_nbr_ptr, ctx->d_nbr,
-                                                                    ctx->d_a_off, ctx->d_A, x, y, ctx->d_z,
-                                                                    ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha)));
+  const int grid = ctx->spmv_grid, chunk = (ctx->nc + grid - 1) / grid;
+  const size_t smem = spmv_smem_bytes(ctx);
+  DISPATCH_P(ctx->p, (k_spmv3<NP_><<<grid, SP_T, smem, s>>>(mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr,
+                                                            ctx->d_a_off, ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st,
+                                                            ctx->d_partials, ctx->d_alpha, ctx->spmv_slots,
+                                                            ctx->spmv_slot_bytes, ctx->max_deg * ctx->np,
+                                                            ctx->spmv_G)));
+}
+
+int spmv_set_smem(dgas_ctx ctx, size_t smem) {
+  cudaError_t e = cudaSuccess;
+  int dev = 0, mx = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if ((int)smem > mx) { ctx->detail = "SpMV kernel needs more shared memory than available"; return DGAS_E_INVALID_ARG; }
+  DISPATCH_P(ctx->p, ({
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, k_spmv3<NP_>);
+    if (e == cudaSuccess && (size_t)mx < smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_spmv3<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
+  }));
+  if (e != cudaSuccess) { ctx->detail = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
+  return 0;
 }
 
 void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cudaStream_t s) {
@@ -529,12 +845,47 @@ void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cuda
                                             ctx->d_b, ctx->d_r0, st, ctx->d_partials))));
 }
 
+size_t apply_smem_bytes(dgas_ctx ctx) {
+  const size_t mc = ctx->max_sub_cells, n = ctx->np;
+  const size_t off_us = 512 + ((mc + 1) * 4 + 7) / 8 * 8;
+  const size_t off_uo = off_us + ((mc + 2) * 4 + 7) / 8 * 8;
+  const size_t off_y = (off_uo + mc * 8 + 127) / 128 * 128;
+  const size_t ybytes = (mc * n * 8 + 127) / 128 * 128;
+  return off_y + ybytes + (size_t)ctx->ring_slots * ctx->slot_bytes + 128;
+}
+
+int local_threads(int p) {
+  int t = 128;
+  DISPATCH_P(p, (t = LocalCfg<NP_>::T));
+  return t;
+}
+
+// z = P^-1 r minus the prolongation: coarse solve on the side stream || local solves on s
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
-  size_t smem = (size_t)std::max(ctx->max_sub_cells * ctx->np, CT) * sizeof(double);
-  DISPATCH_P(ctx->p, (k_apply<NP_><<<ctx->n_coarse_ctas + ctx->nsub, AT, smem, s>>>(
-                         mode, ctx->n_coarse_ctas, ctx->coarse_dense, ctx->N0, ctx->nT, ctx->bt, ctx->d_X, ctx->d_A0t,
-                         ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U,
-                         ctx->d_Dinv, r, ctx->d_rbuf, z, st)));
+  cudaStream_t side = ctx->side[ctx->side_sel];
+  cudaEvent_t ef = ctx->ev_fork[ctx->side_sel], ej = ctx->ev_join[ctx->side_sel];
+  cudaEventRecord(ef, s);
+  cudaStreamWaitEvent(side, ef, 0);
+  k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, side>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt,
+                                                   ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
+  const size_t smem = apply_smem_bytes(ctx);
+  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T, smem, s>>>(
+                         mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
+                         st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+  cudaEventRecord(ej, side);
+  cudaStreamWaitEvent(s, ej, 0);
+}
+
+void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s) {
+  const size_t smem = apply_smem_bytes(ctx);
+  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T, smem, s>>>(
+                         0, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
+                         nullptr, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+}
+
+void launch_coarse_only(dgas_ctx ctx, cudaStream_t s) {
+  k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(0, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt, ctx->d_X,
+                                                ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, nullptr);
 }
 
 void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s,
@@ -556,9 +907,20 @@ void launch_lanczos(dgas_ctx ctx, cudaStream_t s) {
   k_lanczos<<<1, 256, 0, s>>>(ctx->d_state, ctx->d_alpha, ctx->d_beta, ctx->d_lanczos);
 }
 
+// The attribute is per function (shared by all contexts): always raise it to the opt-in maximum.
 int apply_set_smem(dgas_ctx ctx, size_t smem) {
   cudaError_t e = cudaSuccess;
-  DISPATCH_P(ctx->p, (e = cudaFuncSetAttribute(k_apply<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)));
+  int dev = 0, mx = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if ((int)smem > mx) { ctx->detail = "fused apply kernel needs more shared memory than available"; return DGAS_E_INVALID_ARG; }
+  DISPATCH_P(ctx->p, ({
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, k_local<NP_>);
+    if (e == cudaSuccess && (size_t)mx < smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_local<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
+  }));
   if (e != cudaSuccess) { ctx->detail = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
   return 0;
 }

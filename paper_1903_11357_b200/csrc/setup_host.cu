@@ -219,11 +219,11 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
     std::sort(l.begin(), l.end());
     nbr.insert(nbr.end(), l.begin(), l.end());
     nbr_ptr[c + 1] = (int)nbr.size();
-    a_off[c + 1] = a_off[c] + (int64_t)np * np * (int64_t)l.size();
+    a_off[c + 1] = a_off[c] + ((int64_t)np * np * (int64_t)l.size() + 1) / 2 * 2;  // 16-byte rows for TMA
     ctx->max_deg = std::max(ctx->max_deg, (int)l.size());
   }
   ctx->nnzb = nbr.size();
-  ctx->nbr_ptr_h = nbr_ptr; ctx->nbr_h = nbr;
+  ctx->nbr_ptr_h = nbr_ptr; ctx->nbr_h = nbr; ctx->a_off_h = a_off;
   // envelope of the local blocks: f_k = first coupled local cell (<= k)
   std::vector<int> first(nc);
   std::vector<int64_t> u_off(nc + 1, 0);
@@ -234,7 +234,7 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
         if (nbr[k] >= sub_ptr[s] && nbr[k] < f) f = nbr[k];
       first[c] = f - sub_ptr[s];
       int w = (c - f) * np;
-      u_off[c + 1] = u_off[c] + (int64_t)np * w;
+      u_off[c + 1] = u_off[c] + ((int64_t)np * w + 1) / 2 * 2;  // 16-byte rows for TMA
       ctx->max_urow = std::max(ctx->max_urow, w);
     }
   ctx->u_total = u_off[nc];
@@ -368,7 +368,8 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
     if ((st = dev_alloc(ctx, &ctx->d_Dinv0, (size_t)ctx->nT * CT * CT))) return bail(st, ctx->detail);
     if (ctx->coarse_dense) {
       if ((st = dev_alloc(ctx, &ctx->d_W, tiles * CT * CT))) return bail(st, ctx->detail);
-      if ((st = dev_alloc(ctx, &ctx->d_X, (size_t)ctx->N0 * ctx->N0))) return bail(st, ctx->detail);
+      ctx->ldX = (ctx->N0 + 1) / 2 * 2;  // even leading dimension: 16-byte aligned rows
+      if ((st = dev_alloc(ctx, &ctx->d_X, (size_t)ctx->N0 * ctx->ldX))) return bail(st, ctx->detail);
     }
   }
   const size_t N = ctx->N;
@@ -418,6 +419,11 @@ static void free_ctx(dgas_ctx ctx) {
                   ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (int i = 0; i < 3; ++i) {
+    if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
+    if (ctx->ev_fork[i]) cudaEventDestroy(ctx->ev_fork[i]);
+    if (ctx->ev_join[i]) cudaEventDestroy(ctx->ev_join[i]);
+  }
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);

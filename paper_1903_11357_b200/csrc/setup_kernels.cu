@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(128) k_gather_rows(int n, const int* nbr_ptr, 
       if (j == c) v += fblk[((size_t)f * 4 + side * 3) * n * n + a * n + b];
       else if (other == j) v += fblk[((size_t)f * 4 + side * 2 + (1 - side)) * n * n + a * n + b];
     }
-    row[(size_t)a * W + col] = v;
+    row[(size_t)col * n + a] = v;  // column-major row-block
   }
 }
 
@@ -299,22 +299,21 @@ __global__ void __launch_bounds__(256) k_local_factor(int n, const int* sub_ptr,
     const int Wk = (k - fk) * n;
     double* Lk = U + u_off[gk];
     // A row of gk
-    const int lo = nbr_ptr[gk], deg = nbr_ptr[gk + 1] - lo, WA = deg * n;
+    const int lo = nbr_ptr[gk], deg = nbr_ptr[gk + 1] - lo;
     const double* Ak = A + a_off[gk];
     for (int j = fk; j < k; ++j) {
       const int gj = s0 + j, fj = first[gj];
-      const int Wj = (j - fj) * n;
       const double* Lj = U + u_off[gj];
       int sl = -1;
       for (int t = 0; t < deg; ++t) if (nbr[lo + t] == gj) sl = t;
       const int l0 = max(fk, fj);
       for (int e = threadIdx.x; e < nn; e += blockDim.x) {
         int a = e / n, b = e % n;
-        double v = sl >= 0 ? Ak[(size_t)a * WA + sl * n + b] : 0.0;
+        double v = sl >= 0 ? Ak[((size_t)sl * n + b) * n + a] : 0.0;
         for (int l = l0; l < j; ++l) {
-          const double* x = Lk + (size_t)a * Wk + (l - fk) * n;
-          const double* y = Lj + (size_t)b * Wj + (l - fj) * n;
-          for (int c = 0; c < n; ++c) v -= x[c] * y[c];
+          const double* x = Lk + (size_t)(l - fk) * n * n + a;   // L_kl[a][c] at x[c * n]
+          const double* y = Lj + (size_t)(l - fj) * n * n + b;
+          for (int c = 0; c < n; ++c) v -= x[c * n] * y[c * n];
         }
         S[e] = v;
       }
@@ -325,7 +324,7 @@ __global__ void __launch_bounds__(256) k_local_factor(int n, const int* sub_ptr,
         int a = e / n, b = e % n;
         double v = 0;
         for (int c = 0; c <= b; ++c) v += S[a * n + c] * Li[b * n + c];
-        Lk[(size_t)a * Wk + (j - fk) * n + b] = v;
+        Lk[((size_t)(j - fk) * n + b) * n + a] = v;
       }
       __syncthreads();
     }
@@ -334,11 +333,11 @@ __global__ void __launch_bounds__(256) k_local_factor(int n, const int* sub_ptr,
     for (int t = 0; t < deg; ++t) if (nbr[lo + t] == gk) slk = t;
     for (int e = threadIdx.x; e < nn; e += blockDim.x) {
       int a = e / n, b = e % n;
-      double v = Ak[(size_t)a * WA + slk * n + b];
+      double v = Ak[((size_t)slk * n + b) * n + a];
       for (int l = fk; l < k; ++l) {
-        const double* x = Lk + (size_t)a * Wk + (l - fk) * n;
-        const double* y = Lk + (size_t)b * Wk + (l - fk) * n;
-        for (int c = 0; c < n; ++c) v -= x[c] * y[c];
+        const double* x = Lk + (size_t)(l - fk) * n * n + a;
+        const double* y = Lk + (size_t)(l - fk) * n * n + b;
+        for (int c = 0; c < n; ++c) v -= x[c * n] * y[c * n];
       }
       S[e] = v;
     }
@@ -358,11 +357,11 @@ __global__ void __launch_bounds__(256) k_local_factor(int n, const int* sub_ptr,
     __syncthreads();
     for (int col = threadIdx.x; col < Wk; col += blockDim.x) {
       double v[DGAS_MAXNP];
-      for (int a = 0; a < n; ++a) v[a] = Lk[(size_t)a * Wk + col];
+      for (int a = 0; a < n; ++a) v[a] = Lk[(size_t)col * n + a];
       for (int a = n - 1; a >= 0; --a) {
         double t = 0;
         for (int c = 0; c <= a; ++c) t += Li[a * n + c] * v[c];
-        Lk[(size_t)a * Wk + col] = t;
+        Lk[(size_t)col * n + a] = t;
       }
     }
     __syncthreads();
