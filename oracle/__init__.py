@@ -50,6 +50,8 @@ def lib():
         L.or_apply.argtypes = [_P, _P, _P]
         L.or_apply_ld.argtypes = [_P, _P, _P]
         L.or_apply_sampled.argtypes = [_P, ctypes.c_int, _P, _P, _P]
+        L.or_set_refine.argtypes = [_P, ctypes.c_int]
+        L.or_set_perturb.argtypes = [_P, ctypes.c_double, ctypes.c_uint64]
         L.or_get_G.argtypes = [_P, _P]
         L.or_get_A0.argtypes = [_P, _P]
         L.or_coarse_basis.argtypes = [_P, ctypes.c_int, _P, _P]
@@ -186,6 +188,14 @@ class Oracle:
         if st:
             raise OracleError(st, "apply failed (missing factors?)")
         return z
+
+    def set_refine(self, steps):
+        """Iterative-refinement steps of the banded coarse solve (R30)."""
+        lib().or_set_refine(self.h, steps)
+
+    def set_perturb(self, eps, seed=1):
+        """Relative perturbation of G before A0 is formed (sensitivity probe, R30)."""
+        lib().or_set_perturb(self.h, eps, seed)
 
     def apply_sampled(self, r, sample):
         r = np.ascontiguousarray(r, dtype=np.float64)

@@ -269,6 +269,9 @@ struct Ctx {
   Factors<double> F;
   Factors<long double> FL;
   bool use_coarse = true, use_local = true, have_schwarz = false;
+  int refine = 0;  // iterative-refinement steps of the band coarse solve (R30)
+  double perturb = 0;  // relative last-bit perturbation of G (sensitivity measurement, R30)
+  uint64_t perturb_seed = 1;
   int status = 0;
   char msg[256] = {0};
 };
@@ -673,6 +676,15 @@ int or_setup_schwarz(void* h, int ncoarse, int q, int n_ov, const int* ov_fine, 
       }
     }
   }
+  if (c->perturb != 0) {  // sensitivity probe: G *= (1 + perturb * u), u uniform in [-1, 1]
+    uint64_t x = c->perturb_seed;
+    for (auto& g : c->G)
+      for (auto& v : g) {
+        x = x * 6364136223846793005ULL + 1442695040888963407ULL;
+        double u = (double)(x >> 11) * (1.0 / 9007199254740992.0) * 2 - 1;
+        v *= 1 + c->perturb * u;
+      }
+  }
   // --- A0 = Q^T A Q (eq:A0)
   int64_t N0 = (int64_t)ncoarse * nq;
   int bw = 0;
@@ -812,8 +824,25 @@ int apply_t(Ctx* c, const Factors<T>& F, const double* r, double* z, const std::
       }
     if (F.band < 0) chol_solve((int)N0, F.L0, r0);
     else {
-      if constexpr (std::is_same<T, double>::value) band_solve(N0, F.band, F.L0, r0);
-      else return -2;
+      if constexpr (std::is_same<T, double>::value) {
+        std::vector<double> b0(r0.begin(), r0.end());
+        band_solve(N0, F.band, F.L0, r0);
+        for (int it = 0; it < c->refine; ++it) {  // DESIGN.md R30: residual in long double, one more solve
+          const int bw = F.band;
+          const int64_t ld = bw + 1;
+          std::vector<double> res(N0);
+          for (int64_t i = 0; i < N0; ++i) {
+            long double s = b0[i];
+            for (int64_t j = std::max<int64_t>(0, i - bw); j <= std::min<int64_t>(N0 - 1, i + bw); ++j) {
+              double a = j <= i ? c->A0band[i * ld + (j - i + bw)] : c->A0band[j * ld + (i - j + bw)];
+              s -= (long double)a * r0[j];
+            }
+            res[i] = (double)s;
+          }
+          band_solve(N0, F.band, F.L0, res);
+          for (int64_t i = 0; i < N0; ++i) r0[i] += res[i];
+        }
+      } else return -2;
     }
     for (size_t o = 0; o < c->G.size(); ++o) {  // z += Q z0
       int f = c->ov_fine[o];
@@ -835,6 +864,8 @@ extern "C" {
 int or_apply(void* h, const double* r, double* z) { return apply_t(((Ctx*)h), ((Ctx*)h)->F, r, z, nullptr); }
 int or_apply_ld(void* h, const double* r, double* z) { return apply_t(((Ctx*)h), ((Ctx*)h)->FL, r, z, nullptr); }
 // apply restricted to the dofs of the listed subdomains (others left 0): sampled full-size parity
+void or_set_refine(void* h, int steps) { ((Ctx*)h)->refine = steps; }
+void or_set_perturb(void* h, double eps, uint64_t seed) { ((Ctx*)h)->perturb = eps; ((Ctx*)h)->perturb_seed = seed; }
 int or_apply_sampled(void* h, int n_sample, const int* sample, const double* r, double* z) {
   Ctx* c = (Ctx*)h;
   std::vector<char> only(c->nsub, 0);

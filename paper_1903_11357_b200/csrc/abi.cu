@@ -25,6 +25,10 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     DGAS_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork[i], cudaEventDisableTiming));
     DGAS_CUDA(cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming));
   }
+  if (ctx->coarse_mode == 2) {
+    int st2 = nd_set_smem(ctx);
+    if (st2) return st2;
+  }
   ctx->n_coarse_ctas = ctx->coarse_dense ? (int)std::min<int64_t>(592, std::max<int64_t>(1, ctx->N0 / 32)) : 1;
   {
     // TMA ring of the local-solve CTAs: unit = CC columns of a row-block (about the average row-block
@@ -33,33 +37,26 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     // S - 1 units, because the slots of a block are refilled only after that block's barrier.
     ctx->ring_slots = 0;
     {
-      // budget per CTA from the expected residency: all subdomains resident at once when possible
+      // Ring of the warp-specialised local solve: fixed slots of CC columns; S from the per-CTA budget.
+      // The budget targets enough resident CTAs for all subdomains at once when possible.
       int dev = 0, nsm = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       const int T = local_threads(ctx->p);
       const int per_sm = (ctx->nsub + nsm - 1) / nsm;
-      size_t b0 = per_sm <= 1 ? 200 * 1024 : per_sm <= 2 ? 105 * 1024 : per_sm <= 3 ? 70 * 1024 : 55 * 1024;
-      if (T == 256) b0 = std::max<size_t>(b0, 105 * 1024);
-      size_t budgets[2] = {b0, (size_t)200 * 1024};
-      size_t target = T == 128 ? 12 * 1024 : 24 * 1024;
-      if (const char* e = std::getenv("DGAS_APPLY_BUDGET_KB")) budgets[0] = budgets[1] = (size_t)std::atoi(e) * 1024;
+      size_t budget = per_sm <= 1 ? 200 * 1024 : per_sm <= 2 ? 105 * 1024 : per_sm <= 3 ? 70 * 1024
+                      : per_sm <= 4 ? 55 * 1024 : per_sm <= 5 ? 44 * 1024 : per_sm <= 6 ? 36 * 1024 : 31 * 1024;
+      if (T == 256) budget = std::max<size_t>(budget, 100 * 1024);
+      size_t target = T == 128 ? 6 * 1024 : 12 * 1024;
+      if (const char* e = std::getenv("DGAS_APPLY_BUDGET_KB")) budget = (size_t)std::atoi(e) * 1024;
       if (const char* e = std::getenv("DGAS_APPLY_SLOT_KB")) target = (size_t)std::atoi(e) * 1024;
       const int maxW = std::max(2, (ctx->max_urow + 1) / 2 * 2);
       const size_t base = apply_smem_bytes(ctx);
-      const int CC0 = std::min(maxW, std::max(2, (int)(target / (8 * ctx->np)) / 2 * 2));
-      auto try_cc = [&](int CC, size_t budget) {
+      int CC = std::min(maxW, std::max(2, (int)(target / (8 * ctx->np)) / 2 * 2));
+      for (; CC >= 2; CC -= 2) {
         uint32_t sb = (uint32_t)(((((int64_t)CC * ctx->np + 1) / 2 * 2) * 8 + 127) / 128 * 128);
         int S = (int)std::min<size_t>(64, (budget - std::min(budget, base)) / sb);
-        int units = (maxW + CC - 1) / CC;
-        if (S >= 3 && S >= units + 1) { ctx->ring_slots = S; ctx->slot_bytes = sb; ctx->ring_rows = CC; return true; }
-        return false;
-      };
-      for (size_t budget : budgets) {
-        bool ok = false;
-        for (int CC = CC0; CC >= 2 && !ok; CC -= 2) ok = try_cc(CC, budget);
-        for (int CC = CC0 + 2; CC <= maxW && !ok; CC += 2) ok = try_cc(CC, budget);
-        if (ok) break;
+        if (S >= 2) { ctx->ring_slots = S; ctx->slot_bytes = sb; ctx->ring_rows = CC; break; }
       }
     }
     if (ctx->ring_slots < 2) { ctx->detail = "subdomain row-block too large for shared memory"; return DGAS_E_INVALID_ARG; }
@@ -321,7 +318,7 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->bytes_U = ctx->u_total * 8;
   info->bytes_Dinv = (int64_t)ctx->nc * np * np * 8;
   info->bytes_G = (int64_t)ctx->nov * np * nq * 8;
-  info->bytes_coarse = ctx->coarse_dense ? ctx->N0 * ctx->ldX * 8
+  info->bytes_coarse = ctx->coarse_mode == 2 ? ctx->nd.bytes : ctx->coarse_dense ? ctx->N0 * ctx->ldX * 8
                                          : (int64_t)ctx->nT * (ctx->bt + 1) * CT * CT * 8 + (int64_t)ctx->nT * CT * CT * 8;
   // algorithmic bytes: every operator entry read once, vectors once each
   info->alg_bytes_spmv = info->bytes_A + (2 * N) * 8 + (int64_t)ctx->nnzb * 4;
@@ -360,7 +357,7 @@ extern "C" int dgas_debug_basis(dgas_ctx ctx, int32_t i, double* out) {
 
 extern "C" int dgas_debug_A0(dgas_ctx ctx, double* out) {
   if (!ctx || !out) return DGAS_E_INVALID_ARG;
-  if (!ctx->coarse_dense) return DGAS_E_INVALID_ARG;
+  if (!ctx->coarse_dense && ctx->coarse_mode != 1) return DGAS_E_INVALID_ARG;
   // the tile storage holds the Cholesky factor after setup: return L L^T (lower tiles) densely
   const int nT = ctx->nT, bt = ctx->bt;
   std::vector<double> t((size_t)nT * (bt + 1) * CT * CT);

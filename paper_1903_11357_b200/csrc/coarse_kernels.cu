@@ -134,7 +134,7 @@ __device__ inline double* tile_ptr(double* T, int bt, int I, int K) {
 
 __global__ void __launch_bounds__(128) k_A0(int n, int nqq, int bt, const int* pair, const int* cptr,
                                             const int4* contrib, const int* nbr_ptr, const int64_t* a_off,
-                                            const double* A, const double* G, double* A0t) {
+                                            const double* A, const double* G, double* A0t, double* A0b) {
   const int pr = blockIdx.x;
   const int J1 = pair[2 * pr], J2 = pair[2 * pr + 1];
   __shared__ double T[DGAS_MAXNP * DGAS_MAXNP];
@@ -164,6 +164,8 @@ __global__ void __launch_bounds__(128) k_A0(int n, int nqq, int bt, const int* p
   }
   for (int e = threadIdx.x, s = 0; e < nqq * nqq; e += blockDim.x, ++s) {
     int a = e / nqq, b = e % nqq;
+    if (A0b) A0b[(size_t)pr * nqq * nqq + e] = acc[s];
+    if (!A0t) continue;
     int r = J1 * nqq + a, c = J2 * nqq + b;
     int I = r / CT, K = c / CT;
     if (K > I || I - K > bt) continue;
@@ -304,8 +306,19 @@ int coarse_setup_run(dgas_ctx ctx) {
   DGAS_CUDA(cudaGetLastError());
   if (ctx->n_pairs > 0)
     k_A0<<<(unsigned)ctx->n_pairs, 128, 0, s>>>(n, nqq, ctx->bt, ctx->d_pair, ctx->d_contrib_ptr, ctx->d_contrib,
-                                                 ctx->d_nbr_ptr, ctx->d_a_off, ctx->d_A, ctx->d_G, ctx->d_A0t);
+                                                 ctx->d_nbr_ptr, ctx->d_a_off, ctx->d_A, ctx->d_G,
+                                                 ctx->coarse_mode == 2 ? nullptr : ctx->d_A0t, ctx->d_A0b);
   DGAS_CUDA(cudaGetLastError());
+  if (ctx->coarse_mode == 2) {
+    int st = nd_setup_run(ctx);
+    if (st) return st;
+    int herr[8];
+    DGAS_CUDA(cudaMemcpyAsync(herr, ctx->d_err, sizeof herr, cudaMemcpyDeviceToHost, s));
+    DGAS_CUDA(cudaStreamSynchronize(s));
+    if (herr[3]) { ctx->detail = "coarse basis Gram not SPD"; return DGAS_E_MESH; }
+    if (herr[4]) { ctx->detail = "coarse operator A0 not SPD (nested-dissection front)"; return DGAS_E_NOT_SPD; }
+    return 0;
+  }
   k_pad<<<1, CT, 0, s>>>(ctx->N0, ctx->nT, ctx->bt, ctx->d_A0t);
   const int nT = ctx->nT, bt = ctx->bt;
   for (int K = 0; K < nT; ++K) {

@@ -35,12 +35,36 @@ struct Reduce {
   int cap;
 };
 
+// Nested-dissection plan of the coarse solve (nd_host.cu / nd_kernels.cu)
+struct NdPlan {
+  int nf = 0, nlev = 0, maxF = 0, maxU = 0, maxN = 0;
+  int64_t bytes = 0;
+  std::vector<int> h_lev_ptr, h_lev_fronts, h_nF, h_nU, h_offT, h_offu, h_offFe, h_offUe, h_Fe, h_Ue, h_childptr,
+      h_childs, h_cmap_ptr, h_cmap, h_asm_ptr, h_wf_ptr, h_wb_ptr;
+  std::vector<int64_t> h_offX, h_offM, h_offUpd, h_offS;
+  std::vector<int4> h_asm;
+  int *d_nF = nullptr, *d_nU = nullptr, *d_offT = nullptr, *d_offu = nullptr, *d_offFe = nullptr, *d_offUe = nullptr;
+  int *d_Fe = nullptr, *d_Ue = nullptr, *d_childptr = nullptr, *d_childs = nullptr, *d_cmap_ptr = nullptr, *d_cmap = nullptr;
+  int *d_asm_ptr = nullptr, *d_lev_fronts = nullptr;
+  int4* d_asm = nullptr;
+  int2 *d_wf = nullptr, *d_wb = nullptr;
+  int64_t *d_offX = nullptr, *d_offM = nullptr, *d_offUpd = nullptr, *d_offS = nullptr;
+  double *d_X = nullptr, *d_M = nullptr, *d_MT = nullptr, *d_T = nullptr, *d_u = nullptr;
+  int refine = 0;                      // iterative-refinement steps of the coarse solve (R30, off)
+  std::vector<int> h_prow;             // coarse pair rows (pairs sorted by (J1, J2))
+  int* d_prow = nullptr;
+  double *d_rb = nullptr, *d_zb = nullptr;
+};
+
 struct dgas_ctx_s {
   // sizes
   int p = 0, q = 0, np = 0, nq = 0, nc = 0, nsub = 0, ncoarse = 0, nface = 0, nov = 0;
   int64_t N = 0, N0 = 0;
   double penalty = 10;
   int coarse_dense = 1, coarse_bw = 0, nT = 0, bt = 0;  // coarse tiles
+  int coarse_mode = 0;       // 0 dense explicit inverse, 1 band Cholesky (tile sweeps), 2 nested dissection
+  NdPlan nd;
+  double* d_A0b = nullptr;   // A0 blocks per coarse pair (n_pairs x nq x nq)
   int max_sub_cells = 0, max_urow = 0, max_deg = 0;
   int64_t nnzb = 0, u_total = 0;
   std::string detail;
@@ -215,6 +239,11 @@ void launch_init_state(dgas_ctx ctx, PcgState* st, int maxit, double rtol, cudaS
 void launch_pcg_init(dgas_ctx ctx, cudaStream_t s);
 void launch_lanczos(dgas_ctx ctx, cudaStream_t s);
 int dgas_post_setup(dgas_ctx ctx);
+int nd_build(dgas_ctx ctx, const std::vector<int>& pair_h, const std::vector<double>& centroid, int leaf);
+int nd_setup_run(dgas_ctx ctx);
+void nd_solve_launch(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s);
+int nd_set_smem(dgas_ctx ctx);
+void nd_free(dgas_ctx ctx);
 int apply_set_smem(dgas_ctx ctx, size_t smem);
 size_t apply_smem_bytes(dgas_ctx ctx);
 size_t spmv_smem_bytes(dgas_ctx ctx);

@@ -474,26 +474,31 @@ __global__ void __launch_bounds__(CO_T) k_coarse(int mode, int dense, int64_t N0
 
 // ------------------------------------------------------------------ local solves z_i = A_i^-1 r_i
 // One CTA per subdomain: s = D^-1 r, U y = s (forward), U^T u = y (backward), z = D^-T u, with
-// A_i = L L^T, L = D_b^-1-scaled block envelope factor (setup_kernels.cu). Row-block U_k
-// (n x W_k, column-major) streams through a ring of S shared-memory slots by cp.async.bulk, in
-// units of CC columns; unit u lives in slot u % S. Forward consumes units in order and refills
-// slot u%S with unit u+S after the row-block's barrier; the last S units stay resident for the
-// backward sweep, which consumes units in reverse order and refills with unit u-S. One barrier per
-// row-block; the copies are issued by the CTA's last thread, idle in the forward step.
+// A_i = L L^T and U = D_b^-1-scaled block-envelope rows (setup_kernels.cu). Warp-specialised:
+//   * a producer warp streams the column-major row-blocks U_k through S shared-memory slots with
+//     cp.async.bulk, in units of CC columns (unit u in slot u % S). Forward order u = 0..U-1; the
+//     last S units stay resident for the backward sweep, which consumes u = U-1..0 and refills the
+//     slot of unit v with unit v - S. A slot is refilled as soon as every consumer warp has released
+//     it (per-slot "empty" mbarrier), so prefetch depth does not depend on row-block sizes;
+//   * consumer warps run the two sweeps; the only CTA-level dependency per row-block (y_k complete
+//     before step k+1) is a named barrier among the consumers.
 template <int NP>
 struct LocalCfg {
-  static constexpr int T = NP <= 15 ? 128 : 256;
+  static constexpr int T = NP <= 15 ? 128 : 256;   // consumer threads
+  static constexpr int W = T / 32;                 // consumer warps
 };
 
+__device__ __forceinline__ int nd_slot_events(int U, int S, int s) { return s < U ? (U - 1 - s) / S + 1 : 0; }
+
 template <int NP>
-__global__ void __launch_bounds__(LocalCfg<NP>::T) k_local(int mode, const int* __restrict__ sub_ptr,
-                                                           const int* __restrict__ first,
-                                                           const int64_t* __restrict__ u_off,
-                                                           const double* __restrict__ U,
-                                                           const double* __restrict__ Dinv, const double* r_in,
-                                                           double* const* rbuf, double* z, const PcgState* st,
-                                                           int S, uint32_t slot_bytes, int ymax_cells, int CC) {
-  constexpr int T = LocalCfg<NP>::T;
+__global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const int* __restrict__ sub_ptr,
+                                                                const int* __restrict__ first,
+                                                                const int64_t* __restrict__ u_off,
+                                                                const double* __restrict__ U,
+                                                                const double* __restrict__ Dinv, const double* r_in,
+                                                                double* const* rbuf, double* z, const PcgState* st,
+                                                                int S, uint32_t slot_bytes, int ymax_cells, int CC) {
+  constexpr int T = LocalCfg<NP>::T, NW = LocalCfg<NP>::W;
   extern __shared__ __align__(128) double sm[];
   const double* r = r_in;
   if (mode >= 1) {
@@ -502,59 +507,69 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T) k_local(int mode, const int* 
   }
   const int s = blockIdx.x;
   const int s0 = sub_ptr[s], m = sub_ptr[s + 1] - s0;
-  // layout (must match local_smem_offsets on the host): all offsets 8/128-byte aligned
-  const size_t off_us = 512 + (((size_t)(ymax_cells + 1) * 4 + 7) & ~(size_t)7);
+  // layout (must match apply_smem_bytes): full[64] | empty[64] | fk | us | uo | y | ring
+  const size_t off_fk = 1024;
+  const size_t off_us = off_fk + (((size_t)(ymax_cells + 1) * 4 + 7) & ~(size_t)7);
   const size_t off_uo = off_us + (((size_t)(ymax_cells + 2) * 4 + 7) & ~(size_t)7);
   const size_t off_y = (off_uo + (size_t)ymax_cells * 8 + 127) & ~(size_t)127;
   unsigned char* smb = reinterpret_cast<unsigned char*>(sm);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smb);
-  int* fk_s = reinterpret_cast<int*>(smb + 512);
-  int* us_s = reinterpret_cast<int*>(smb + off_us);                      // first unit of block k
+  uint64_t* full = reinterpret_cast<uint64_t*>(smb);
+  uint64_t* empty = full + 64;
+  int* fk_s = reinterpret_cast<int*>(smb + off_fk);
+  int* us_s = reinterpret_cast<int*>(smb + off_us);
   int64_t* uo_s = reinterpret_cast<int64_t*>(smb + off_uo);
   double* y = reinterpret_cast<double*>(smb + off_y);
   unsigned char* ring = reinterpret_cast<unsigned char*>(y) + (((size_t)ymax_cells * NP * 8 + 127) & ~(size_t)127);
-  for (int k = threadIdx.x; k < m; k += T) { fk_s[k] = first[s0 + k]; uo_s[k] = u_off[s0 + k]; }
+  for (int k = threadIdx.x; k < m; k += T + 32) { fk_s[k] = first[s0 + k]; uo_s[k] = u_off[s0 + k]; }
   if (threadIdx.x == 0) {
-    for (int t = 0; t < S; ++t) mbar_init(&bars[t], 1);
+    for (int t = 0; t < S; ++t) { mbar_init(&full[t], 1); mbar_init(&empty[t], NW); }
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // unit prefix: block k owns units [us_s[k], us_s[k+1])
     int acc = 0;
-    us_s[0] = 0;
     for (int k = 0; k < m; ++k) {
       us_s[k] = acc;
-      acc += k == 0 ? 0 : ((k - fk_s[k]) * NP + CC - 1) / CC;
+      acc += k == 0 ? 0 : ((k - first[s0 + k]) * NP + CC - 1) / CC;
     }
     us_s[m] = acc;
   }
   __syncthreads();
   const int nunits = us_s[m];
-  const int prod = T - 1;
-  if (threadIdx.x == 0)
-    for (int k = 1; k < m; ++k)
-      if (us_s[k + 1] - us_s[k] > S - 1) __trap();  // host guarantees it; never hang instead
-  auto unit_blk = [&](int u, int k, int& cA, int& cB) {
+  auto unit_cols = [&](int u, int k, int& cA, int& cB) {
     cA = (u - us_s[k]) * CC;
     cB = min((k - fk_s[k]) * NP, cA + CC);
   };
-  auto issue = [&](int u, int k) {
-    int cA, cB;
-    unit_blk(u, k, cA, cB);
-    const uint32_t nbytes = (uint32_t)((((int64_t)(cB - cA) * NP + 1) & ~1LL) * 8);
-    bulk_load(ring + (size_t)(u % S) * slot_bytes, U + uo_s[k] + (int64_t)cA * NP, nbytes, &bars[u % S]);
-  };
-  // block of unit u (units are few per block: walk from a hint)
-  auto blk_of = [&](int u, int hint) {
-    int k = hint;
-    while (us_s[k + 1] <= u) ++k;
-    while (us_s[k] > u) --k;
-    return k;
-  };
-  if (threadIdx.x == prod) {
+  if (threadIdx.x >= T) {
+    // ---------------- producer warp (lane 0 issues every copy)
+    if (threadIdx.x != T) return;
+    auto issue = [&](int u, int k) {
+      int cA, cB;
+      unit_cols(u, k, cA, cB);
+      const uint32_t nbytes = (uint32_t)((((int64_t)(cB - cA) * NP + 1) & ~1LL) * 8);
+      bulk_load(ring + (size_t)(u % S) * slot_bytes, U + uo_s[k] + (int64_t)cA * NP, nbytes, &full[u % S]);
+    };
     int k = 1;
-    for (int u = 0; u < nunits && u < S; ++u) { k = blk_of(u, k); issue(u, k); }
+    for (int u = 0; u < nunits; ++u) {  // forward stream
+      while (us_s[k + 1] <= u) ++k;
+      if (u >= S) {  // wait for the forward release of unit u - S (event (u - S) / S of its slot)
+        mbar_wait(&empty[u % S], (uint32_t)(((u - S) / S) & 1));
+      }
+      issue(u, k);
+    }
+    int kv = m - 1, kw = m - 1;
+    for (int v = nunits - 1; v >= S; --v) {  // backward refills: after releasing v, load v - S
+      const int sl = v % S;
+      const int vmax = sl + S * (nd_slot_events(nunits, S, sl) - 1);  // largest unit of the slot
+      const int Fs = nd_slot_events(nunits - S, S, sl);               // forward releases of the slot
+      const int ev = Fs + (vmax - v) / S;  // index of v's backward release event in its slot
+      mbar_wait(&empty[sl], (uint32_t)(ev & 1));
+      const int w = v - S;
+      while (us_s[kw] > w) --kw;
+      (void)kv;
+      issue(w, kw);
+    }
+    return;
   }
+  // ---------------- consumers
+  const int lane = threadIdx.x & 31;
   uint64_t ph = 0;
   const double* rs = r + (size_t)s0 * NP;
   for (int e = threadIdx.x; e < m * NP; e += T) {
@@ -564,62 +579,71 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T) k_local(int mode, const int* 
     for (int c = 0; c <= a; ++c) v += __ldg(D + c) * rs[k * NP + c];
     y[e] = v;
   }
-  __syncthreads();
+  named_sync(1, T);
   // forward: thread (a, q) accumulates row a over columns col = q (mod 8) of every unit of U_k
   const int fa = threadIdx.x >> 3, fq = threadIdx.x & 7;
-  int pk_hint = 1;
   for (int k = 1; k < m; ++k) {
     const int u0 = us_s[k], u1 = us_s[k + 1];
     if (u1 > u0) {
       const double* yw = y + fk_s[k] * NP;
       double v = 0;
       for (int u = u0; u < u1; ++u) {
-        mbar_wait(&bars[u % S], (uint32_t)((ph >> (u % S)) & 1u));
-        ph ^= 1ull << (u % S);
+        const int sl = u % S;
+        mbar_wait(&full[sl], (uint32_t)((ph >> sl) & 1u));
+        ph ^= 1ull << sl;
         int cA, cB;
-        unit_blk(u, k, cA, cB);
-        const double* Uc = reinterpret_cast<const double*>(ring + (size_t)(u % S) * slot_bytes);
-        if (fa < NP)
-          for (int col = cA + fq; col < cB; col += 8) v += Uc[(col - cA) * NP + fa] * yw[col];
+        unit_cols(u, k, cA, cB);
+        const double* Uc = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+        if (fa < NP) {
+          double v1 = 0;
+          int col = cA + fq;
+          for (; col + 8 < cB; col += 16) {
+            v += Uc[(col - cA) * NP + fa] * yw[col];
+            v1 += Uc[(col + 8 - cA) * NP + fa] * yw[col + 8];
+          }
+          if (col < cB) v += Uc[(col - cA) * NP + fa] * yw[col];
+          v += v1;
+        }
+        __syncwarp();
+        // resident units (u >= U - S) are released only once, in the backward sweep: every slot's
+        // release events then alternate with producer refills (no mbarrier phase aliasing)
+        if (lane == 0 && u < nunits - S) mbar_arrive(&empty[sl]);
       }
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       v += __shfl_xor_sync(0xffffffffu, v, 4);
       if (fa < NP && fq == 0) y[k * NP + fa] -= v;
     }
-    __syncthreads();
-    if (threadIdx.x == prod)
-      for (int u = u0; u < u1; ++u)
-        if (u + S < nunits) { pk_hint = blk_of(u + S, pk_hint); issue(u + S, pk_hint); }
+    named_sync(1, T);
   }
   // backward: u_k is final; y[f_k .. k) -= U_k^T u_k (thread per column)
-  pk_hint = m - 1;
   for (int k = m - 1; k > 0; --k) {
     const int u0 = us_s[k], u1 = us_s[k + 1];
     if (u1 > u0) {
       const double* uk = y + k * NP;
       double* yw = y + fk_s[k] * NP;
       for (int u = u1 - 1; u >= u0; --u) {
+        const int sl = u % S;
         if (u < nunits - S) {
-          mbar_wait(&bars[u % S], (uint32_t)((ph >> (u % S)) & 1u));
-          ph ^= 1ull << (u % S);
+          mbar_wait(&full[sl], (uint32_t)((ph >> sl) & 1u));
+          ph ^= 1ull << sl;
         }
         int cA, cB;
-        unit_blk(u, k, cA, cB);
-        const double* Uc = reinterpret_cast<const double*>(ring + (size_t)(u % S) * slot_bytes);
+        unit_cols(u, k, cA, cB);
+        const double* Uc = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
         for (int col = cA + threadIdx.x; col < cB; col += T) {
           const double* uc = Uc + (size_t)(col - cA) * NP;
-          double v = 0;
+          double v0 = 0, v1 = 0;
 #pragma unroll
-          for (int a = 0; a < NP; ++a) v += uc[a] * uk[a];
-          yw[col] -= v;
+          for (int a = 0; a + 1 < NP; a += 2) { v0 += uc[a] * uk[a]; v1 += uc[a + 1] * uk[a + 1]; }
+          if (NP & 1) v0 += uc[NP - 1] * uk[NP - 1];
+          yw[col] -= v0 + v1;
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sl]);
       }
     }
-    __syncthreads();
-    if (threadIdx.x == prod)
-      for (int u = u1 - 1; u >= u0; --u)
-        if (u - S >= 0) { pk_hint = blk_of(u - S, pk_hint); issue(u - S, pk_hint); }
+    named_sync(1, T);
   }
   double* zs = z + (size_t)s0 * NP;
   for (int e = threadIdx.x; e < m * NP; e += T) {
@@ -847,7 +871,7 @@ void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cuda
 
 size_t apply_smem_bytes(dgas_ctx ctx) {
   const size_t mc = ctx->max_sub_cells, n = ctx->np;
-  const size_t off_us = 512 + ((mc + 1) * 4 + 7) / 8 * 8;
+  const size_t off_us = 1024 + ((mc + 1) * 4 + 7) / 8 * 8;
   const size_t off_uo = off_us + ((mc + 2) * 4 + 7) / 8 * 8;
   const size_t off_y = (off_uo + mc * 8 + 127) / 128 * 128;
   const size_t ybytes = (mc * n * 8 + 127) / 128 * 128;
@@ -862,14 +886,28 @@ int local_threads(int p) {
 
 // z = P^-1 r minus the prolongation: coarse solve on the side stream || local solves on s
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
+  static const bool no_fork = std::getenv("DGAS_NO_FORK") != nullptr;
+  if (no_fork) {
+    if (ctx->coarse_mode == 2) nd_solve_launch(ctx, mode, st, s);
+    else
+      k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt,
+                                                    ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
+    const size_t smem = apply_smem_bytes(ctx);
+    DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
+                           mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
+                           st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+    return;
+  }
   cudaStream_t side = ctx->side[ctx->side_sel];
   cudaEvent_t ef = ctx->ev_fork[ctx->side_sel], ej = ctx->ev_join[ctx->side_sel];
   cudaEventRecord(ef, s);
   cudaStreamWaitEvent(side, ef, 0);
-  k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, side>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt,
-                                                   ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
+  if (ctx->coarse_mode == 2) nd_solve_launch(ctx, mode, st, side);
+  else
+    k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, side>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt,
+                                                     ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
   const size_t smem = apply_smem_bytes(ctx);
-  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T, smem, s>>>(
+  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
                          mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
                          st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
   cudaEventRecord(ej, side);
@@ -878,12 +916,13 @@ void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double*
 
 void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s) {
   const size_t smem = apply_smem_bytes(ctx);
-  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T, smem, s>>>(
+  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
                          0, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
                          nullptr, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
 }
 
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s) {
+  if (ctx->coarse_mode == 2) { nd_solve_launch(ctx, 0, nullptr, s); return; }
   k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(0, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt, ctx->d_X,
                                                 ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, nullptr);
 }

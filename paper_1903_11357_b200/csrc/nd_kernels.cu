@@ -1,0 +1,333 @@
+// nd_kernels.cu — multifrontal nested-dissection factorisation and solve of the coarse operator
+// A0 = Q^T A Q (eq:A0) for large N0 (see nd_host.cu for the plan).
+//   setup, per tree level (deepest first), one CTA per front:
+//     S = [S_FF S_FU; S_UF S_UU] = A0 restricted to (F, F u U) + extend-add of the children's updates
+//     X_F = S_FF^-1 (Cholesky, triangular inverse, L^-T L^-1),  M_F = S_UF X_F,
+//     update_F = S_UU - M_F S_UF^T  (passed to the parent)
+//   solve, per level: forward u_F = t_U - M_F t_F (t = r0|_F + children's u), backward
+//     x_F = X_F t_F - M_F^T x_U. Every level is one launch of GEMV rows (row chunks per CTA).
+#include "internal.h"
+
+#define ND_T 256
+#define ND_ROWS 32  // rows of a front per CTA in the solve
+
+// ------------------------------------------------------------------ setup: assemble front matrices
+__global__ void __launch_bounds__(ND_T) k_nd_assemble(int nq, const int* __restrict__ fronts, const int* nF, const int* nU,
+                                                      const int64_t* offS, const int64_t* offUpd, const int* asm_ptr,
+                                                      const int4* asmv, const int* childptr, const int* childs,
+                                                      const int* cmap_ptr, const int* cmap, const double* A0b,
+                                                      const double* Upd, double* Sg) {
+  const int f = fronts[blockIdx.x];
+  const int n = nF[f] + nU[f], nFe = nF[f] / nq;
+  double* S = Sg + offS[f];
+  for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += ND_T) S[e] = 0.0;
+  __syncthreads();
+  const int nq2 = nq * nq;
+  for (int e = threadIdx.x; e < (asm_ptr[f + 1] - asm_ptr[f]) * nq2; e += ND_T) {
+    const int4 a4 = asmv[asm_ptr[f] + e / nq2];
+    const int ab = e % nq2, a = ab / nq, b = ab % nq;
+    const double v = A0b[(size_t)a4.x * nq2 + ab];
+    S[(size_t)(a4.y * nq + a) * n + a4.z * nq + b] = v;
+    if (a4.z >= nFe) S[(size_t)(a4.z * nq + b) * n + a4.y * nq + a] = v;
+  }
+  __syncthreads();
+  for (int ci = childptr[f]; ci < childptr[f + 1]; ++ci) {
+    const int c = childs[ci];
+    const int nuc = nU[c];
+    const double* Uc = Upd + offUpd[c];
+    const int* mp = cmap + cmap_ptr[ci];
+    for (int64_t e = threadIdx.x; e < (int64_t)nuc * nuc; e += ND_T) {
+      const int a = (int)(e / nuc), b = (int)(e % nuc);
+      const int la = mp[a / nq] * nq + a % nq, lb = mp[b / nq] * nq + b % nq;
+      S[(size_t)la * n + lb] += Uc[e];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ setup: partial factorisation
+__global__ void __launch_bounds__(ND_T) k_nd_factor(const int* __restrict__ fronts, const int* nF, const int* nU,
+                                                    const int64_t* offS, const int64_t* offX, const int64_t* offM,
+                                                    const int64_t* offUpd, double* Sg, double* Xg, double* Mg,
+                                                    double* MTg, double* Upd, int* err) {
+  const int f = fronts[blockIdx.x];
+  const int nf = nF[f], nu = nU[f], n = nf + nu;
+  double* S = Sg + offS[f];
+  double* L = Xg + offX[f];  // Cholesky factor, later overwritten by X
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int64_t e = threadIdx.x; e < (int64_t)nf * nf; e += ND_T) L[e] = S[(e / nf) * n + e % nf];
+  __syncthreads();
+  // right-looking Cholesky of S_FF (lower, in L)
+  for (int j = 0; j < nf; ++j) {
+    if (threadIdx.x == 0) {
+      double d = L[(size_t)j * nf + j];
+      if (!(d > 0)) { bad = 1; d = 1.0; }
+      L[(size_t)j * nf + j] = sqrt(d);
+    }
+    __syncthreads();
+    const double d = L[(size_t)j * nf + j];
+    for (int i = j + 1 + threadIdx.x; i < nf; i += ND_T) L[(size_t)i * nf + j] /= d;
+    __syncthreads();
+    const int m = nf - j - 1;
+    for (int64_t e = threadIdx.x; e < (int64_t)m * m; e += ND_T) {
+      const int i = j + 1 + (int)(e / m), k = j + 1 + (int)(e % m);
+      if (k <= i) L[(size_t)i * nf + k] -= L[(size_t)i * nf + j] * L[(size_t)k * nf + j];
+    }
+    __syncthreads();
+  }
+  if (bad && threadIdx.x == 0) atomicExch(&err[4], 1);
+  // W = L^-1 into the S_FF block of S (no longer needed), column per thread
+  for (int c = threadIdx.x; c < nf; c += ND_T) {
+    for (int i = 0; i < c; ++i) S[(size_t)i * n + c] = 0.0;
+    for (int i = c; i < nf; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) s -= L[(size_t)i * nf + k] * S[(size_t)k * n + c];
+      S[(size_t)i * n + c] = s / L[(size_t)i * nf + i];
+    }
+  }
+  __syncthreads();
+  // X = W^T W (symmetric, full)
+  double* X = L;
+  for (int64_t e = threadIdx.x; e < (int64_t)nf * nf; e += ND_T) {
+    const int i = (int)(e / nf), j = (int)(e % nf);
+    double s = 0;
+    for (int k = max(i, j); k < nf; ++k) s += S[(size_t)k * n + i] * S[(size_t)k * n + j];
+    X[e] = s;
+  }
+  __syncthreads();
+  // M = S_UF X (nu x nf) and M^T
+  double* M = Mg + offM[f];
+  double* MT = MTg + offM[f];
+  for (int64_t e = threadIdx.x; e < (int64_t)nu * nf; e += ND_T) {
+    const int r = (int)(e / nf), j = (int)(e % nf);
+    const double* srow = S + (size_t)(nf + r) * n;
+    double s = 0;
+    for (int i = 0; i < nf; ++i) s += srow[i] * X[(size_t)i * nf + j];
+    M[e] = s;
+    MT[(size_t)j * nu + r] = s;
+  }
+  __syncthreads();
+  // update = S_UU - M S_UF^T  (nu x nu)
+  double* Up = Upd + offUpd[f];
+  for (int64_t e = threadIdx.x; e < (int64_t)nu * nu; e += ND_T) {
+    const int r = (int)(e / nu), t = (int)(e % nu);
+    const double* mrow = M + (size_t)r * nf;
+    const double* srow = S + (size_t)(nf + t) * n;
+    double s = S[(size_t)(nf + r) * n + nf + t];
+    for (int j = 0; j < nf; ++j) s -= mrow[j] * srow[j];
+    Up[e] = s;
+  }
+}
+
+// ------------------------------------------------------------------ solve: forward level
+// work item (front, first row of U); t assembled in shared memory by every CTA of the front
+__global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict__ work, const int* __restrict__ nF,
+                                                 const int* __restrict__ nU, const int* __restrict__ offT,
+                                                 const int* __restrict__ offu, const int* __restrict__ offFe,
+                                                 const int* __restrict__ Fe, const int64_t* __restrict__ offM,
+                                                 const int* __restrict__ childptr, const int* __restrict__ childs,
+                                                 const int* __restrict__ cmap_ptr, const int* __restrict__ cmap,
+                                                 const double* __restrict__ Mg, const double* r0, double* Tg,
+                                                 double* ug, const PcgState* st, int mode) {
+  extern __shared__ double t[];
+  if (mode >= 1 && st->done) return;
+  const int2 wi = work[blockIdx.x];
+  const int f = wi.x, row0 = wi.y;
+  const int nf = nF[f], nu = nU[f];
+  for (int k = threadIdx.x; k < nf; k += ND_T) t[k] = r0[(size_t)Fe[offFe[f] + k / nq] * nq + k % nq];
+  for (int k = nf + threadIdx.x; k < nf + nu; k += ND_T) t[k] = 0.0;
+  __syncthreads();
+  for (int ci = childptr[f]; ci < childptr[f + 1]; ++ci) {
+    const int c = childs[ci];
+    const double* uc = ug + offu[c];
+    const int* mp = cmap + cmap_ptr[ci];
+    for (int a = threadIdx.x; a < nU[c]; a += ND_T) t[mp[a / nq] * nq + a % nq] += uc[a];
+    __syncthreads();
+  }
+  if (row0 == 0)
+    for (int k = threadIdx.x; k < nf; k += ND_T) Tg[offT[f] + k] = t[k];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* M = Mg + offM[f];
+  const int rend = min(nu, row0 + ND_ROWS);
+  for (int r = row0 + w; r < rend; r += ND_T / 32) {
+    const double* mr = M + (size_t)r * nf;
+    double v = 0;
+    for (int k = lane; k < nf; k += 32) v += mr[k] * t[k];
+    v = warp_sum(v);
+    if (lane == 0) ug[offu[f] + r] = t[nf + r] - v;
+  }
+}
+
+// ------------------------------------------------------------------ solve: backward level
+__global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict__ work, const int* __restrict__ nF,
+                                                 const int* __restrict__ nU, const int* __restrict__ offT,
+                                                 const int* __restrict__ offFe, const int* __restrict__ Fe,
+                                                 const int* __restrict__ offUe, const int* __restrict__ Ue,
+                                                 const int64_t* __restrict__ offX, const int64_t* __restrict__ offM,
+                                                 const double* __restrict__ Xg, const double* __restrict__ MTg,
+                                                 const double* Tg, double* z0, const PcgState* st, int mode) {
+  extern __shared__ double sh[];
+  if (mode >= 1 && st->done) return;
+  const int2 wi = work[blockIdx.x];
+  const int f = wi.x, row0 = wi.y;
+  const int nf = nF[f], nu = nU[f];
+  double* tF = sh;
+  double* xU = sh + nf;
+  for (int k = threadIdx.x; k < nf; k += ND_T) tF[k] = Tg[offT[f] + k];
+  for (int k = threadIdx.x; k < nu; k += ND_T) xU[k] = z0[(size_t)Ue[offUe[f] + k / nq] * nq + k % nq];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* X = Xg + offX[f];
+  const double* MT = MTg + offM[f];
+  const int rend = min(nf, row0 + ND_ROWS);
+  for (int j = row0 + w; j < rend; j += ND_T / 32) {
+    const double* xr = X + (size_t)j * nf;
+    const double* mr = MT + (size_t)j * nu;
+    double v = 0;
+    for (int k = lane; k < nf; k += 32) v += xr[k] * tF[k];
+    for (int k = lane; k < nu; k += 32) v -= mr[k] * xU[k];
+    v = warp_sum(v);
+    if (lane == 0) z0[(size_t)Fe[offFe[f] + j / nq] * nq + j % nq] = v;
+  }
+}
+
+// ------------------------------------------------------------------ host launchers
+template <typename T>
+static int up(dgas_ctx ctx, T** d, const std::vector<T>& h) {
+  DGAS_CUDA(cudaMalloc((void**)d, std::max<size_t>(1, h.size()) * sizeof(T)));
+  if (!h.empty()) DGAS_CUDA(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return 0;
+}
+
+int nd_setup_run(dgas_ctx ctx) {
+  NdPlan& P = ctx->nd;
+  cudaStream_t s = ctx->stream;
+  int st = 0;
+  if ((st = up(ctx, &P.d_nF, P.h_nF)) || (st = up(ctx, &P.d_nU, P.h_nU)) || (st = up(ctx, &P.d_offX, P.h_offX)) ||
+      (st = up(ctx, &P.d_offM, P.h_offM)) || (st = up(ctx, &P.d_offUpd, P.h_offUpd)) ||
+      (st = up(ctx, &P.d_offS, P.h_offS)) || (st = up(ctx, &P.d_offT, P.h_offT)) || (st = up(ctx, &P.d_offu, P.h_offu)) ||
+      (st = up(ctx, &P.d_offFe, P.h_offFe)) || (st = up(ctx, &P.d_offUe, P.h_offUe)) || (st = up(ctx, &P.d_Fe, P.h_Fe)) ||
+      (st = up(ctx, &P.d_Ue, P.h_Ue)) || (st = up(ctx, &P.d_childptr, P.h_childptr)) ||
+      (st = up(ctx, &P.d_childs, P.h_childs)) || (st = up(ctx, &P.d_cmap_ptr, P.h_cmap_ptr)) ||
+      (st = up(ctx, &P.d_cmap, P.h_cmap)) || (st = up(ctx, &P.d_asm_ptr, P.h_asm_ptr)) || (st = up(ctx, &P.d_asm, P.h_asm)) ||
+      (st = up(ctx, &P.d_lev_fronts, P.h_lev_fronts)))
+    return st;
+  const int nf = P.nf;
+  DGAS_CUDA(cudaMalloc((void**)&P.d_X, std::max<int64_t>(1, P.h_offX[nf]) * 8));
+  DGAS_CUDA(cudaMalloc((void**)&P.d_M, std::max<int64_t>(1, P.h_offM[nf]) * 8));
+  DGAS_CUDA(cudaMalloc((void**)&P.d_MT, std::max<int64_t>(1, P.h_offM[nf]) * 8));
+  DGAS_CUDA(cudaMalloc((void**)&P.d_T, std::max<int>(1, P.h_offT[nf]) * 8));
+  DGAS_CUDA(cudaMalloc((void**)&P.d_u, std::max<int>(1, P.h_offu[nf]) * 8));
+  double *dS = nullptr, *dUpd = nullptr;
+  DGAS_CUDA(cudaMalloc((void**)&dS, std::max<int64_t>(1, P.h_offS[nf]) * 8));
+  DGAS_CUDA(cudaMalloc((void**)&dUpd, std::max<int64_t>(1, P.h_offUpd[nf]) * 8));
+  for (int L = 0; L < P.nlev; ++L) {
+    const int n = P.h_lev_ptr[L + 1] - P.h_lev_ptr[L];
+    if (!n) continue;
+    const int* fr = P.d_lev_fronts + P.h_lev_ptr[L];
+    k_nd_assemble<<<n, ND_T, 0, s>>>(ctx->nq, fr, P.d_nF, P.d_nU, P.d_offS, P.d_offUpd, P.d_asm_ptr, P.d_asm, P.d_childptr,
+                                     P.d_childs, P.d_cmap_ptr, P.d_cmap, ctx->d_A0b, dUpd, dS);
+    k_nd_factor<<<n, ND_T, 0, s>>>(fr, P.d_nF, P.d_nU, P.d_offS, P.d_offX, P.d_offM, P.d_offUpd, dS, P.d_X, P.d_M, P.d_MT,
+                                   dUpd, ctx->d_err);
+  }
+  DGAS_CUDA(cudaGetLastError());
+  // per-level work lists (front, first row) for the solve kernels
+  std::vector<int2> wf, wb;
+  P.h_wf_ptr.assign(P.nlev + 1, 0);
+  P.h_wb_ptr.assign(P.nlev + 1, 0);
+  for (int L = 0; L < P.nlev; ++L) {
+    for (int k = P.h_lev_ptr[L]; k < P.h_lev_ptr[L + 1]; ++k) {
+      const int f = P.h_lev_fronts[k];
+      for (int r = 0; r < std::max(1, P.h_nU[f]); r += ND_ROWS) wf.push_back(make_int2(f, r));
+      for (int r = 0; r < P.h_nF[f]; r += ND_ROWS) wb.push_back(make_int2(f, r));
+    }
+    P.h_wf_ptr[L + 1] = (int)wf.size();
+    P.h_wb_ptr[L + 1] = (int)wb.size();
+  }
+  if ((st = up(ctx, &P.d_wf, wf)) || (st = up(ctx, &P.d_wb, wb)) || (st = up(ctx, &P.d_prow, P.h_prow))) return st;
+  DGAS_CUDA(cudaMalloc((void**)&P.d_rb, (ctx->N0 + 1) * 8));
+  DGAS_CUDA(cudaMalloc((void**)&P.d_zb, (ctx->N0 + 1) * 8));
+  DGAS_CUDA(cudaStreamSynchronize(s));
+  cudaFree(dS);
+  cudaFree(dUpd);
+  P.bytes = (P.h_offX[nf] + 2 * P.h_offM[nf]) * 8;
+  return 0;
+}
+
+// res = b - A0 z  (coarse block rows, warp per coarse element; A0 blocks per coupled pair)
+__global__ void __launch_bounds__(ND_T) k_a0_resid(int ncoarse, int nq, const int* __restrict__ prow,
+                                                   const int* __restrict__ pair, const double* __restrict__ A0b,
+                                                   const double* b, const double* z, double* res, const PcgState* st,
+                                                   int mode) {
+  if (mode >= 1 && st->done) return;
+  const int J = blockIdx.x * (ND_T / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (J >= ncoarse) return;
+  for (int a = 0; a < nq; ++a) {
+    double v = 0;
+    for (int e = lane; e < (prow[J + 1] - prow[J]) * nq; e += 32) {
+      const int pr = prow[J] + e / nq, bcol = e % nq;
+      v += A0b[((size_t)pr * nq + a) * nq + bcol] * z[(size_t)pair[2 * pr + 1] * nq + bcol];
+    }
+    v = warp_sum(v);
+    if (lane == 0) res[(size_t)J * nq + a] = b[(size_t)J * nq + a] - v;
+  }
+}
+
+__global__ void k_axpy_add(int64_t n, const double* a, double* y, const PcgState* st, int mode) {
+  if (mode >= 1 && st->done) return;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] += a[i];
+}
+
+static void nd_solve_once(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s, const double* rin, double* zout);
+
+void nd_solve_launch(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s) {
+  nd_solve_once(ctx, mode, st, s, ctx->d_r0, ctx->d_z0);
+  for (int it = 0; it < ctx->nd.refine; ++it) {  // iterative refinement (R30)
+    const int nb = (ctx->ncoarse + ND_T / 32 - 1) / (ND_T / 32);
+    k_a0_resid<<<nb, ND_T, 0, s>>>(ctx->ncoarse, ctx->nq, ctx->nd.d_prow, ctx->d_pair, ctx->d_A0b, ctx->d_r0,
+                                   ctx->d_z0, ctx->nd.d_rb, st, mode);
+    nd_solve_once(ctx, mode, st, s, ctx->nd.d_rb, ctx->nd.d_zb);
+    k_axpy_add<<<(unsigned)((ctx->N0 + 255) / 256), 256, 0, s>>>(ctx->N0, ctx->nd.d_zb, ctx->d_z0, st, mode);
+  }
+}
+
+static void nd_solve_once(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s, const double* rin, double* zout) {
+  NdPlan& P = ctx->nd;
+  const size_t shf = (size_t)P.maxN * 8, shb = (size_t)(P.maxF + P.maxU) * 8;
+  for (int L = 0; L < P.nlev; ++L) {
+    const int n = P.h_wf_ptr[L + 1] - P.h_wf_ptr[L];
+    if (n)
+      k_nd_fwd<<<n, ND_T, shf, s>>>(ctx->nq, P.d_wf + P.h_wf_ptr[L], P.d_nF, P.d_nU, P.d_offT, P.d_offu, P.d_offFe,
+                                    P.d_Fe, P.d_offM, P.d_childptr, P.d_childs, P.d_cmap_ptr, P.d_cmap, P.d_M, rin,
+                                    P.d_T, P.d_u, st, mode);
+  }
+  for (int L = P.nlev - 1; L >= 0; --L) {
+    const int n = P.h_wb_ptr[L + 1] - P.h_wb_ptr[L];
+    if (n)
+      k_nd_bwd<<<n, ND_T, shb, s>>>(ctx->nq, P.d_wb + P.h_wb_ptr[L], P.d_nF, P.d_nU, P.d_offT, P.d_offFe, P.d_Fe,
+                                    P.d_offUe, P.d_Ue, P.d_offX, P.d_offM, P.d_X, P.d_MT, P.d_T, zout, st, mode);
+  }
+}
+
+int nd_set_smem(dgas_ctx ctx) {
+  NdPlan& P = ctx->nd;
+  const size_t shf = (size_t)P.maxN * 8, shb = (size_t)(P.maxF + P.maxU) * 8;
+  int dev = 0, mx = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if ((int)std::max(shf, shb) > mx) { ctx->detail = "nested-dissection front too large for shared memory"; return DGAS_E_INVALID_ARG; }
+  DGAS_CUDA(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shf));
+  DGAS_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
+  return 0;
+}
+
+void nd_free(dgas_ctx ctx) {
+  NdPlan& P = ctx->nd;
+  void* ptrs[] = {P.d_nF, P.d_nU, P.d_offX, P.d_offM, P.d_offUpd, P.d_offS, P.d_offT, P.d_offu, P.d_offFe, P.d_offUe,
+                  P.d_Fe, P.d_Ue, P.d_childptr, P.d_childs, P.d_cmap_ptr, P.d_cmap, P.d_asm_ptr, P.d_asm,
+                  P.d_lev_fronts, P.d_X, P.d_M, P.d_MT, P.d_T, P.d_u, P.d_wf, P.d_wb, P.d_prow, P.d_rb, P.d_zb};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}

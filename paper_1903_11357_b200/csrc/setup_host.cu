@@ -307,10 +307,17 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
   ctx->coarse_bw = bw;
   ctx->nT = (int)((ctx->N0 + CT - 1) / CT);
   {
-    // dense explicit A0^-1 up to 8192 coarse dofs; env override for tests
+    // dense explicit A0^-1 up to 8192 coarse dofs, nested dissection above;
+    // DGAS_COARSE_MODE=dense|band|nd overrides (tests exercise every path on small problems)
     int64_t dense_max = 8192;
     if (const char* e = std::getenv("DGAS_COARSE_DENSE_MAX")) dense_max = std::atoll(e);
-    ctx->coarse_dense = ctx->N0 <= dense_max;
+    ctx->coarse_mode = ctx->N0 <= dense_max ? 0 : 2;
+    if (std::getenv("DGAS_COARSE_DENSE_MAX") && ctx->N0 > dense_max) ctx->coarse_mode = 1;  // legacy test knob
+    if (const char* e = std::getenv("DGAS_COARSE_MODE")) {
+      std::string m(e);
+      ctx->coarse_mode = m == "dense" ? 0 : m == "band" ? 1 : m == "nd" ? 2 : ctx->coarse_mode;
+    }
+    ctx->coarse_dense = ctx->coarse_mode == 0;
   }
   ctx->bt = ctx->coarse_dense ? ctx->nT - 1 : std::min(ctx->nT - 1, (bw + CT - 1) / CT);
   std::vector<int> pair_h, cptr_h(1, 0);
@@ -322,6 +329,26 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
   }
   ctx->n_pairs = (int64_t)pairs.size();
   pairs.clear();
+  if (ctx->coarse_mode == 2) {
+    // coarse-element centroids (area-weighted over the overlap pieces): ordering heuristic only
+    std::vector<double> cen(2 * ctx->ncoarse, 0.0), ar(ctx->ncoarse, 0.0);
+    for (int o = 0; o < nov; ++o) {
+      const double* v = &ov_xy[2 * ov_pptr[o]];
+      const int n = ov_pptr[o + 1] - ov_pptr[o];
+      double a = 0, cx = 0, cy = 0;
+      for (int k = 0; k < n; ++k) {
+        const int l = (k + 1) % n;
+        const double cr = v[2 * k] * v[2 * l + 1] - v[2 * l] * v[2 * k + 1];
+        a += cr; cx += (v[2 * k] + v[2 * l]) * cr; cy += (v[2 * k + 1] + v[2 * l + 1]) * cr;
+      }
+      const int J = ov_coarse[o];
+      ar[J] += 0.5 * a; cen[2 * J] += cx / 6; cen[2 * J + 1] += cy / 6;
+    }
+    for (int J = 0; J < ctx->ncoarse; ++J) { cen[2 * J] /= ar[J]; cen[2 * J + 1] /= ar[J]; }
+    int leaf = 32;
+    if (const char* e = std::getenv("DGAS_ND_LEAF")) leaf = std::max(2, std::atoi(e));
+    if ((st = nd_build(ctx, pair_h, cen, leaf))) return bail(st, ctx->detail);
+  }
   // ------------------------------------------------ device buffers
   if ((st = dev_upload(ctx, &ctx->d_xy, cxy))) return bail(st, ctx->detail);
   if ((st = dev_upload(ctx, &ctx->d_cptr, cptr))) return bail(st, ctx->detail);
@@ -362,7 +389,8 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
   if ((st = dev_upload(ctx, &ctx->d_pair, pair_h))) return bail(st, ctx->detail);
   if ((st = dev_upload(ctx, &ctx->d_contrib_ptr, cptr_h))) return bail(st, ctx->detail);
   if ((st = dev_upload(ctx, &ctx->d_contrib, contrib))) return bail(st, ctx->detail);
-  {
+  if ((st = dev_alloc(ctx, &ctx->d_A0b, (size_t)std::max<int64_t>(1, ctx->n_pairs) * nq * nq))) return bail(st, ctx->detail);
+  if (ctx->coarse_mode != 2) {
     size_t tiles = (size_t)ctx->nT * (ctx->bt + 1);
     if ((st = dev_alloc(ctx, &ctx->d_A0t, tiles * CT * CT))) return bail(st, ctx->detail);
     if ((st = dev_alloc(ctx, &ctx->d_Dinv0, (size_t)ctx->nT * CT * CT))) return bail(st, ctx->detail);
@@ -419,6 +447,8 @@ static void free_ctx(dgas_ctx ctx) {
                   ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (ctx->d_A0b) cudaFree(ctx->d_A0b);
+  nd_free(ctx);
   for (int i = 0; i < 3; ++i) {
     if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
     if (ctx->ev_fork[i]) cudaEventDestroy(ctx->ev_fork[i]);

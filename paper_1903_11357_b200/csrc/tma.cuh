@@ -42,3 +42,12 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
     bulk_g2s((char*)dst + o, (const char*)src + o, n, bar);
   }
 }
+
+// plain arrive (count 1) on an mbarrier
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// named barrier among `count` threads (multiple of 32) with id `id` (1..15)
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
