@@ -47,7 +47,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
       size_t budget = per_sm <= 1 ? 200 * 1024 : per_sm <= 2 ? 105 * 1024 : per_sm <= 3 ? 70 * 1024
                       : per_sm <= 4 ? 55 * 1024 : per_sm <= 5 ? 44 * 1024 : per_sm <= 6 ? 36 * 1024 : 31 * 1024;
       if (T == 256) budget = std::max<size_t>(budget, 100 * 1024);
-      size_t target = T == 128 ? 6 * 1024 : 12 * 1024;
+      size_t target = T == 128 ? 12 * 1024 : 24 * 1024;  // measured best on B200 (tools/ab.sh)
       if (const char* e = std::getenv("DGAS_APPLY_BUDGET_KB")) budget = (size_t)std::atoi(e) * 1024;
       if (const char* e = std::getenv("DGAS_APPLY_SLOT_KB")) target = (size_t)std::atoi(e) * 1024;
       const int maxW = std::max(2, (ctx->max_urow + 1) / 2 * 2);
