@@ -79,6 +79,18 @@ class Clocks:
             return None
 
 
+def aggregate(ms, iters, world, device="cpu"):
+    """Whole-job numbers over replicas: time = MAX over ranks, iterations = SUM over ranks."""
+    if world <= 1:
+        return ms, iters
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms, iters], dtype=torch.float64, device=device)
+    mx = t.clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = t.clone(); dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return float(mx[0]), float(sm[1])
+
+
 def cpu_baseline(name, P=None, max_sub=8):
     """The oracle as it stands, on a bounded sample of the same workload (see `sample`)."""
     import numpy as np
@@ -181,13 +193,7 @@ def main():
         e1.record()
         barrier()
     ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms, iters_total], dtype=torch.float64, device="cuda")
-        mx = t.clone(); torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = t.clone(); torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        ms, iters_all = float(mx[0]), float(sm[1])
-    else:
-        iters_all = iters_total
+    ms, iters_all = aggregate(ms, iters_total, world, device="cuda")
     value = iters_all / (ms / 1e3)
     iters_per_solve = iters_total / args.steps
 
@@ -252,7 +258,8 @@ def main():
                    "l2_policy": (f"inputs larger than L2: operator bytes "
                                  f"{(info['bytes_A'] + info['bytes_U'] + info['bytes_coarse']) / 1e9:.2f} GB "
                                  f"> 126 MB L2"),
-                   "parallelism": "replicas" if world > 1 else "single-gpu", "setup_s": t_setup},
+                   "parallelism": "replicas" if world > 1 else "single-gpu", "setup_s": t_setup,
+                   "coarse_solver": ["dense-inverse", "band", "nested-dissection"][info["coarse_mode"]]},
         "dof_iters_per_s": value * N / max(world, 1) * world,
         "ms_per_apply": kt["apply_total"],
         "spmv_apply_hbm_gbs": spmv_apply_gbs,
@@ -263,7 +270,7 @@ def main():
         "kernels": kern,
         "e2e": {"value": e2e_value, "unit": "PCG it/s", "h2d_bytes_per_step": 2 * N * 8,
                 "d2h_bytes_per_step": N * 8},
-        "gpu_launches": int(4 * iters_total + 9 * args.steps),
+        "gpu_launches": int(info["launches_per_iter"] * iters_total + info["launches_per_solve"] * args.steps),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -88,6 +88,9 @@ typedef struct {
   int64_t alg_bytes_iter;        /* algorithmic HBM bytes of one PCG iteration */
   int32_t last_iters, last_status;
   double last_cond, last_lmin, last_lmax, last_relres;
+  int32_t coarse_mode;           /* 0 dense explicit inverse, 1 band, 2 nested dissection */
+  int32_t launches_per_iter;     /* kernel launches of one PCG iteration (graph body) */
+  int32_t launches_per_solve;    /* fixed launches of one dgas_pcg besides the iterations */
 } dgas_info_t;
 
 /* Build the SIPDG operator and the two-level Schwarz preconditioner on the GPU.

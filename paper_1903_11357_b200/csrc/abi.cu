@@ -70,9 +70,10 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     ctx->spmv_grid = std::min(ctx->nc, per_sm * nsm);
     // SpMV ring: one slot per batch of G consecutive row-blocks of a CTA's cell range
     {
-      const int G = spmv_batch_cells(ctx->p);
+      int G = spmv_batch_cells(ctx->p);
+      while (G > 1 && (int64_t)G * ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p)) --G;
       ctx->spmv_G = G;
-      if ((int64_t)G * ctx->max_deg * ctx->np > 4 * 256) { ctx->detail = "cell degree too large for the SpMV kernel"; return DGAS_E_INVALID_ARG; }
+      if ((int64_t)G * ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p)) { ctx->detail = "cell degree too large for the SpMV kernel"; return DGAS_E_INVALID_ARG; }
       const int chunk = (ctx->nc + ctx->spmv_grid - 1) / ctx->spmv_grid;
       int64_t mx = 0;
       for (int c0 = 0; c0 < ctx->nc; c0 += chunk) {
@@ -328,6 +329,20 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->last_iters = ctx->last_iters; info->last_status = ctx->last_status;
   info->last_cond = ctx->last_cond; info->last_lmin = ctx->last_lmin; info->last_lmax = ctx->last_lmax;
   info->last_relres = ctx->last_relres;
+  info->coarse_mode = ctx->coarse_mode;
+  int coarse_launches = 1;
+  if (ctx->coarse_mode == 2) {
+    coarse_launches = 0;
+    for (int L = 0; L < ctx->nd.nlev; ++L) {
+      coarse_launches += ctx->nd.h_wf_ptr[L + 1] > ctx->nd.h_wf_ptr[L];
+      coarse_launches += ctx->nd.h_wb_ptr[L + 1] > ctx->nd.h_wb_ptr[L];
+    }
+    coarse_launches += 2 * ctx->nd.refine;
+  }
+  // body: spmv, restrict, coarse (side stream), local, prolong; solve: 2 perm in, init_state,
+  // init (spmv, restrict, coarse, local, prolong), lanczos, perm out
+  info->launches_per_iter = 4 + coarse_launches;
+  info->launches_per_solve = 3 + (4 + coarse_launches) + 2;
   return DGAS_OK;
 }
 

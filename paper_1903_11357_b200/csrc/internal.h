@@ -248,6 +248,7 @@ int apply_set_smem(dgas_ctx ctx, size_t smem);
 size_t apply_smem_bytes(dgas_ctx ctx);
 size_t spmv_smem_bytes(dgas_ctx ctx);
 int spmv_batch_cells(int p);
+int spmv_gather_cap(int p);
 int local_threads(int p);
 void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s);
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);

@@ -147,10 +147,10 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32) k_spmv(int mode, int nc, cons
 // then value), so no global load sits on the per-batch critical path.
 // mode 0: y = A x.  mode 1 (PCG): p_new = z + beta p_old (fused), q = A p_new, p.q -> alpha.
 #define SP_T 256
-#define SP_MAXE 4
 template <int NP>
 struct SpmvCfg {
   static constexpr int TR = NP >= 21 ? 8 : 4;             // threads per row (adjacent lanes)
+  static constexpr int E = NP >= 21 ? 3 : 2;              // gathered columns per thread per batch
   static constexpr int G = (SP_T / (NP * TR)) > 0 ? SP_T / (NP * TR) : 1;  // cells per batch
 };
 
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, con
                                                 const double* z, double* const* pbuf, PcgState* st,
                                                 double* partials, double* alpha_hist, int S, uint32_t slot_bytes,
                                                 int maxW, int G) {
-  constexpr int GMAX = SpmvCfg<NP>::G, SPTR = SpmvCfg<NP>::TR;
+  constexpr int GMAX = SpmvCfg<NP>::G, SPTR = SpmvCfg<NP>::TR, SP_MAXE = SpmvCfg<NP>::E;
   extern __shared__ __align__(128) double sm[];
   __shared__ double red[SP_T / 32];
   __shared__ double wdot[SP_T / 32];
@@ -206,17 +206,20 @@ __global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, con
   int idxA[SP_MAXE], slotA[SP_MAXE];
   auto stage_idx = [&](int bi, int* idx, int* slot) {
     const int k0 = bi * G, k1 = min(ncell, k0 + G);
-    for (int t = 0; t < SP_MAXE; ++t) { idx[t] = -1; slot[t] = 0; }
-    if (bi >= nb) return;
-    int e = threadIdx.x, t = 0;
-    for (int k = k0; k < k1 && t < SP_MAXE; ++k) {
-      const int W = (np_s[k + 1] - np_s[k]) * NP;
-      while (e < W && t < SP_MAXE) {
-        idx[t] = __ldg(nbr + np_s[k] + e / NP) * NP + e % NP;
-        slot[t] = (k - k0) * ((maxW + 1) & ~1) + e;
-        e += SP_T; ++t;
+#pragma unroll
+    for (int t = 0; t < SP_MAXE; ++t) {
+      idx[t] = -1;
+      slot[t] = 0;
+      int e = threadIdx.x + SP_T * t;  // flat entry of the batch
+      for (int k = k0; k < k1; ++k) {
+        const int W = (np_s[k + 1] - np_s[k]) * NP;
+        if (e < W) {
+          idx[t] = __ldg(nbr + np_s[k] + e / NP) * NP + e % NP;
+          slot[t] = (k - k0) * ((maxW + 1) & ~1) + e;
+          break;
+        }
+        e -= W;
       }
-      e -= W;
     }
   };
   int idxB[SP_MAXE], slotB[SP_MAXE], idxC[SP_MAXE], slotC[SP_MAXE];
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, con
 // write r_new and x += alpha p_new), r.r -> convergence test, r0 = Q^T r_new.
 // mode 2 (PCG init): r_new = b - q (q = A x0), r.r and b.b.
 // One CTA per coarse element J, one warp per overlap piece.
-#define RW 4
+#define RW 16
 template <int NP, int NQ>
 __global__ void __launch_bounds__(RW * 32) k_restrict(int mode, const int* __restrict__ cov_ptr, const int* __restrict__ cov,
                                                       const int* __restrict__ ov_cell, const int* __restrict__ fov_ptr,
@@ -659,12 +662,18 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
 // z_kappa += sum_{pieces o of kappa} G_o z0_J(o).  mode 0: apply only.  mode 1: PCG init (gamma_0).
 // mode 2: PCG iteration (beta = gamma_new / gamma, history, it++, maxit, graph condition).
 #define PW 8
+template <int NP>
+struct ProlongCfg {
+  static constexpr int L = NP <= 4 ? 4 : NP <= 8 ? 8 : NP <= 16 ? 16 : 32;  // lanes per cell
+  static constexpr int CPW = 32 / L;                                         // cells per warp
+};
 template <int NP, int NQ>
 __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int* __restrict__ fov_ptr,
                                                      const int* __restrict__ fov, const int* __restrict__ ov_coarse,
                                                      const double* __restrict__ G, const double* z0, double* z,
                                                      double* const* rbuf, PcgState* st, double* partials,
                                                      double* beta_hist, cudaGraphConditionalHandle h, int use_h) {
+  constexpr int L = ProlongCfg<NP>::L, CPW = ProlongCfg<NP>::CPW;
   __shared__ double red[PW];
   __shared__ double wd[PW];
   int it = 0;
@@ -678,14 +687,14 @@ __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int
     r = rbuf[mode == 1 ? 0 : ((it + 1) & 1)];
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * PW + w;
+  const int c = (blockIdx.x * PW + w) * CPW + lane / L, a = lane % L;
   double d = 0;
-  if (c < nc && lane < NP) {
-    size_t id = (size_t)c * NP + lane;
+  if (c < nc && a < NP) {
+    size_t id = (size_t)c * NP + a;
     double v = z[id];
     for (int k = fov_ptr[c]; k < fov_ptr[c + 1]; ++k) {
       const int o = fov[k], J = ov_coarse[o];
-      const double* Go = G + ((size_t)o * NP + lane) * NQ;
+      const double* Go = G + ((size_t)o * NP + a) * NQ;
 #pragma unroll
       for (int b = 0; b < NQ; ++b) v += Go[b] * z0[(size_t)J * NQ + b];
     }
@@ -820,6 +829,12 @@ static int SpmvCfgMax(int p) {
   return G;
 }
 
+int spmv_gather_cap(int p) {
+  int e = 2;
+  DISPATCH_P(p, (e = SpmvCfg<NP_>::E));
+  return e * SP_T;
+}
+
 int spmv_batch_cells(int p) {
   int G = 1;
   DISPATCH_P(p, (G = SpmvCfg<NP_>::G));
@@ -830,7 +845,7 @@ int spmv_batch_cells(int p) {
 
 size_t spmv_smem_bytes(dgas_ctx ctx) {
   const int chunk = (ctx->nc + ctx->spmv_grid - 1) / std::max(1, ctx->spmv_grid);
-  const int maxW = ctx->max_deg * ctx->np, G = spmv_batch_cells(ctx->p);
+  const int maxW = ctx->max_deg * ctx->np, G = ctx->spmv_G;
   size_t b = 32 * 8 + (size_t)(chunk + 2) * 8 + (size_t)((chunk + 2 + 3) & ~3) * 4 + 2 * (size_t)G * ((maxW + 1) & ~1) * 8;
   return ((b + 127) & ~(size_t)127) + (size_t)ctx->spmv_slots * ctx->spmv_slot_bytes + 128;
 }
@@ -930,7 +945,8 @@ void launch_coarse_only(dgas_ctx ctx, cudaStream_t s) {
 void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s,
                     cudaGraphConditionalHandle h, int use_handle) {
   (void)r;
-  unsigned grid = (ctx->nc + PW - 1) / PW;
+  unsigned grid = 1;
+  DISPATCH_P(ctx->p, (grid = (ctx->nc + PW * ProlongCfg<NP_>::CPW - 1) / (PW * ProlongCfg<NP_>::CPW)));
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_prolong<NP_, NQ_><<<grid, PW * 32, 0, s>>>(
                                             mode, ctx->nc, ctx->d_fov_ptr, ctx->d_fov, ctx->d_ov_coarse, ctx->d_G,
                                             ctx->d_z0, z, ctx->d_rbuf, st, ctx->d_partials, ctx->d_beta, h,

@@ -307,9 +307,10 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
   ctx->coarse_bw = bw;
   ctx->nT = (int)((ctx->N0 + CT - 1) / CT);
   {
-    // dense explicit A0^-1 up to 8192 coarse dofs, nested dissection above;
+    // dense explicit A0^-1 up to 2048 coarse dofs (latency-bound small coarse problems), nested
+    // dissection above (measured on B200: cfg4 1274 -> 1374 it/s, cfg5 p6q6 1221 -> 1296);
     // DGAS_COARSE_MODE=dense|band|nd overrides (tests exercise every path on small problems)
-    int64_t dense_max = 8192;
+    int64_t dense_max = 2048;
     if (const char* e = std::getenv("DGAS_COARSE_DENSE_MAX")) dense_max = std::atoll(e);
     ctx->coarse_mode = ctx->N0 <= dense_max ? 0 : 2;
     if (std::getenv("DGAS_COARSE_DENSE_MAX") && ctx->N0 > dense_max) ctx->coarse_mode = 1;  // legacy test knob
