@@ -20,10 +20,21 @@ static int finish_setup_buffers(dgas_ctx ctx) {
   DGAS_CUDA(cudaMemcpyAsync(ctx->d_perm_dev, ctx->perm.data(), ctx->nc * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   DGAS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
   DGAS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;
+  DGAS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   for (int i = 0; i < 3; ++i) {
-    DGAS_CUDA(cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking));
+    // the coarse chain is latency-bound: give its fork stream the highest priority so its small
+    // kernels are scheduled ahead of pending local-solve CTAs
+    DGAS_CUDA(cudaStreamCreateWithPriority(&ctx->side[i], cudaStreamNonBlocking, prio_hi));
     DGAS_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork[i], cudaEventDisableTiming));
     DGAS_CUDA(cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming));
+  }
+  {
+    // restriction: about 4 overlap pieces per warp, 1..8 warps per coarse element
+    const int avg = (int)((ctx->nov + ctx->ncoarse - 1) / ctx->ncoarse);
+    int w = 1;
+    while (w < 8 && w * 4 < avg) w *= 2;
+    ctx->restrict_wpj = w;
   }
   if (ctx->coarse_mode == 2) {
     int st2 = nd_set_smem(ctx);
@@ -70,7 +81,13 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     ctx->spmv_grid = std::min(ctx->nc, per_sm * nsm);
     // SpMV ring: one slot per batch of G consecutive row-blocks of a CTA's cell range
     {
+      // cells per batch: ~24 KB of row-blocks per bulk copy (per-batch consumer overhead dominates
+      // below that, tools/ab.sh), at most the thread-limited maximum
       int G = spmv_batch_cells(ctx->p);
+      if (!std::getenv("DGAS_SPMV_G")) {
+        const double avg_row = (double)ctx->a_off_h[ctx->nc] * 8.0 / ctx->nc;
+        G = std::max(1, std::min(G, (int)std::lround(24576.0 / avg_row)));
+      }
       while (G > 1 && (int64_t)G * ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p)) --G;
       ctx->spmv_G = G;
       if ((int64_t)G * ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p)) { ctx->detail = "cell degree too large for the SpMV kernel"; return DGAS_E_INVALID_ARG; }

@@ -161,7 +161,8 @@ struct dgas_ctx_s {
   int spmv_slots = 2;
   uint32_t spmv_slot_bytes = 0;
   int spmv_grid = 0;
-  int spmv_G = 1;           // cells per SpMV batch (<= compile-time maximum)
+  int spmv_G = 1;
+  int restrict_wpj = 8;     // warps per coarse element in k_restrict           // cells per SpMV batch (<= compile-time maximum)
 };
 
 // ---------------------------------------------------------------- helpers

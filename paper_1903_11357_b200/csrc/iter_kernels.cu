@@ -155,7 +155,7 @@ struct SpmvCfg {
 };
 
 template <int NP>
-__global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, const int* __restrict__ nbr_ptr,
+__global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk, const int* __restrict__ nbr_ptr,
                                                 const int* __restrict__ nbr, const int64_t* __restrict__ a_off,
                                                 const double* __restrict__ A, const double* x, double* y,
                                                 const double* z, double* const* pbuf, PcgState* st,
@@ -163,8 +163,9 @@ __global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, con
                                                 int maxW, int G) {
   constexpr int GMAX = SpmvCfg<NP>::G, SPTR = SpmvCfg<NP>::TR, SP_MAXE = SpmvCfg<NP>::E;
   extern __shared__ __align__(128) double sm[];
-  __shared__ double red[SP_T / 32];
-  __shared__ double wdot[SP_T / 32];
+  constexpr int NTT = SP_T + 32;  // consumers + producer warp
+  __shared__ double red[NTT / 32];
+  __shared__ double wdot[NTT / 32];
   __shared__ double own[2][GMAX * NP];
   int it = 0;
   double beta = 0;
@@ -180,25 +181,32 @@ __global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, con
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c0 = min(nc, blockIdx.x * chunk), c1 = min(nc, c0 + chunk), ncell = c1 - c0;
   const int nb = (ncell + G - 1) / G;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);          // full[16]
+  uint64_t* empt = bars + 16;                                 // empty[16]
   int64_t* ao_s = reinterpret_cast<int64_t*>(bars + 32);                  // a_off[c0 .. c1]
   int* np_s = reinterpret_cast<int*>(ao_s + chunk + 2);                    // nbr_ptr[c0 .. c1]
   const int xstride = G * ((maxW + 1) & ~1);
   double* xs = reinterpret_cast<double*>(np_s + ((chunk + 2 + 3) & ~3));   // [2][G][maxW]
   unsigned char* ring = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(xs + 2 * xstride) + 127) & ~(uintptr_t)127);
-  for (int k = threadIdx.x; k <= ncell; k += SP_T) { np_s[k] = nbr_ptr[c0 + k]; ao_s[k] = a_off[c0 + k]; }
+  for (int k = threadIdx.x; k <= ncell; k += SP_T + 32) { np_s[k] = nbr_ptr[c0 + k]; ao_s[k] = a_off[c0 + k]; }
   if (threadIdx.x == 0) {
-    for (int t = 0; t < S; ++t) mbar_init(&bars[t], 1);
+    for (int t = 0; t < S; ++t) { mbar_init(&bars[t], 1); mbar_init(&empt[t], SP_T / 32); }
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](int bi) {
-    const int k0 = bi * G, k1 = min(ncell, k0 + G);
-    bulk_load(ring + (size_t)(bi % S) * slot_bytes, A + ao_s[k0], (uint32_t)((ao_s[k1] - ao_s[k0]) * 8), &bars[bi % S]);
-  };
-  if (threadIdx.x == 0)
-    for (int bi = 0; bi < nb && bi < S; ++bi) issue(bi);
+  if (threadIdx.x >= SP_T) {
+    // producer warp: batch bi goes to slot bi % S as soon as the consumers released batch bi - S
+    if (threadIdx.x == SP_T)
+      for (int bi = 0; bi < nb; ++bi) {
+        if (bi >= S) mbar_wait(&empt[bi % S], (uint32_t)(((bi - S) / S) & 1));
+        const int k0 = bi * G, k1 = min(ncell, k0 + G);
+        bulk_load(ring + (size_t)(bi % S) * slot_bytes, A + ao_s[k0], (uint32_t)((ao_s[k1] - ao_s[k0]) * 8),
+                  &bars[bi % S]);
+      }
+  }
+  double mydot = 0;
+  if (threadIdx.x < SP_T) {  // ---------------- consumers
   auto colval = [&](int64_t id) -> double {
     return mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
   };
@@ -241,10 +249,9 @@ __global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, con
   stage_idx(1, idxB, slotB);
   for (int t = 0; t < SP_MAXE; ++t) vB[t] = idxB[t] >= 0 ? colval(idxB[t]) : 0.0;
   stage_idx(2, idxC, slotC);
-  __syncthreads();
+  named_sync(1, SP_T);
   const int g = threadIdx.x / (NP * SPTR), a = (threadIdx.x / SPTR) % NP, q = threadIdx.x % SPTR;
   uint32_t ph = 0;
-  double mydot = 0;
   for (int bi = 0; bi < nb; ++bi) {
     const int cur = bi & 1;
     // values of batch bi+2 (in flight for two batch computes), indices of batch bi+3
@@ -281,23 +288,25 @@ __global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, con
 #pragma unroll
       for (int o = 1; o < SPTR; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empt[bi % S]);  // this warp is done with the ring slot of batch bi
     publish(bi + 1, idxB, slotB, vB);  // xs[cur^1] is not read during batch bi
     for (int t = 0; t < SP_MAXE; ++t) {
       idxB[t] = idxC[t]; slotB[t] = slotC[t]; vB[t] = vC[t];
       idxC[t] = idxA[t]; slotC[t] = slotA[t];
     }
-    __syncthreads();  // batch bi+1 published; the ring slot of batch bi is free
-    if (threadIdx.x == 0 && bi + S < nb) issue(bi + S);
+    named_sync(1, SP_T);  // batch bi+1 published
   }
+  }  // consumers
   if (mode != 1) return;
   mydot = warp_sum(mydot);
   if (lane == 0) wdot[w] = mydot;
   __syncthreads();
   double tot[1] = {0};
   if (threadIdx.x == 0)
-    for (int k = 0; k < SP_T / 32; ++k) tot[0] += wdot[k];
+    for (int k = 0; k < NTT / 32; ++k) tot[0] += wdot[k];
   double res[1];
-  if (last_block<SP_T, 1>(tot, partials, &st->cnt[0], res, red)) {
+  if (last_block<NTT, 1>(tot, partials, &st->cnt[0], res, red)) {
     if (threadIdx.x == 0) {
       double pq = res[0];
       st->pq = pq;
@@ -312,17 +321,18 @@ __global__ void __launch_bounds__(SP_T) k_spmv3(int mode, int nc, int chunk, con
 // write r_new and x += alpha p_new), r.r -> convergence test, r0 = Q^T r_new.
 // mode 2 (PCG init): r_new = b - q (q = A x0), r.r and b.b.
 // One CTA per coarse element J, one warp per overlap piece.
-#define RW 16
+#define RT 256
 template <int NP, int NQ>
-__global__ void __launch_bounds__(RW * 32) k_restrict(int mode, const int* __restrict__ cov_ptr, const int* __restrict__ cov,
-                                                      const int* __restrict__ ov_cell, const int* __restrict__ fov_ptr,
-                                                      const int* __restrict__ fov, const double* __restrict__ G,
-                                                      const double* r_in, double* const* rbuf, const double* q,
-                                                      double* const* pbuf, double* x, const double* b, double* r0,
-                                                      PcgState* st, double* partials) {
-  __shared__ double red[RW];
-  __shared__ double part[RW][NQ];
-  __shared__ double wsum[RW][2];
+__global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj, const int* __restrict__ cov_ptr,
+                                                 const int* __restrict__ cov, const int* __restrict__ ov_cell,
+                                                 const int* __restrict__ fov_ptr, const int* __restrict__ fov,
+                                                 const double* __restrict__ G, const double* r_in, double* const* rbuf,
+                                                 const double* q, double* const* pbuf, double* x, const double* b,
+                                                 double* r0, PcgState* st, double* partials) {
+  // wpj warps per coarse element (adaptive: ~4 pieces per warp), RT/32/wpj elements per CTA
+  __shared__ double red[RT / 32];
+  __shared__ double part[RT / 32][NQ];
+  __shared__ double wsum[RT / 32][2];
   int it = 0;
   double alpha = 0;
   const double* rold = r_in;
@@ -340,50 +350,55 @@ __global__ void __launch_bounds__(RW * 32) k_restrict(int mode, const int* __res
       rnew = rbuf[0];
     }
   }
-  const int J = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jpc = (RT / 32) / wpj;
+  const int J = blockIdx.x * jpc + w / wpj, wj = w % wpj;
   double accq[NQ];
 #pragma unroll
   for (int k = 0; k < NQ; ++k) accq[k] = 0;
   double rr = 0, bb = 0;
-  for (int k = cov_ptr[J] + w; k < cov_ptr[J + 1]; k += RW) {
-    const int o = cov[k], cell = ov_cell[o];
-    const bool owner = fov[fov_ptr[cell]] == o;
-    double rv = 0;
-    if (lane < NP) {
-      size_t id = (size_t)cell * NP + lane;
-      if (mode == 0) rv = rold[id];
-      else if (mode == 1) rv = rold[id] - alpha * q[id];
-      else rv = b[id] - q[id];
-      if (owner && mode >= 1) {
-        rnew[id] = rv;
-        rr += rv * rv;
-        if (mode == 1) x[id] += alpha * pnew[id];
-        else bb += b[id] * b[id];
+  if (J < ncoarse)
+    for (int k = cov_ptr[J] + wj; k < cov_ptr[J + 1]; k += wpj) {
+      const int o = cov[k], cell = ov_cell[o];
+      const bool owner = fov[fov_ptr[cell]] == o;
+      double rv = 0;
+      if (lane < NP) {
+        size_t id = (size_t)cell * NP + lane;
+        if (mode == 0) rv = rold[id];
+        else if (mode == 1) rv = rold[id] - alpha * q[id];
+        else rv = b[id] - q[id];
+        if (owner && mode >= 1) {
+          rnew[id] = rv;
+          rr += rv * rv;
+          if (mode == 1) x[id] += alpha * pnew[id];
+          else bb += b[id] * b[id];
+        }
+      }
+      const double* Go = G + (size_t)o * NP * NQ;
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) {
+        double v = lane < NP ? Go[lane * NQ + c] * rv : 0.0;
+        accq[c] += warp_sum(v);
       }
     }
-    const double* Go = G + (size_t)o * NP * NQ;
-#pragma unroll
-    for (int c = 0; c < NQ; ++c) {
-      double v = lane < NP ? Go[lane * NQ + c] * rv : 0.0;
-      accq[c] += warp_sum(v);
-    }
-  }
   if (lane == 0)
     for (int c = 0; c < NQ; ++c) part[w][c] = accq[c];
   rr = warp_sum(rr); bb = warp_sum(bb);
   if (lane == 0) { wsum[w][0] = rr; wsum[w][1] = bb; }
   __syncthreads();
-  if (threadIdx.x < NQ) {
+  for (int e = threadIdx.x; e < jpc * NQ; e += RT) {
+    const int jl = e / NQ, c = e % NQ, JJ = blockIdx.x * jpc + jl;
+    if (JJ >= ncoarse) continue;
     double v = 0;
-    for (int k = 0; k < RW; ++k) v += part[k][threadIdx.x];
-    r0[(size_t)J * NQ + threadIdx.x] = v;
+    for (int k = 0; k < wpj; ++k) v += part[jl * wpj + k][c];
+    r0[(size_t)JJ * NQ + c] = v;
   }
   if (mode == 0) return;
   double mine[2] = {0, 0};
   if (threadIdx.x == 0)
-    for (int k = 0; k < RW; ++k) { mine[0] += wsum[k][0]; mine[1] += wsum[k][1]; }
+    for (int k = 0; k < RT / 32; ++k) { mine[0] += wsum[k][0]; mine[1] += wsum[k][1]; }
   double tot[2];
-  if (last_block<RW * 32, 2>(mine, partials, &st->cnt[1], tot, red)) {
+  if (last_block<RT, 2>(mine, partials, &st->cnt[1], tot, red)) {
     if (threadIdx.x == 0) {
       st->rr = tot[0];
       if (mode == 2) { st->bb = tot[1]; st->rtol2_bb *= tot[1]; }
@@ -838,7 +853,6 @@ int spmv_gather_cap(int p) {
 int spmv_batch_cells(int p) {
   int G = 1;
   DISPATCH_P(p, (G = SpmvCfg<NP_>::G));
-  G = std::min(G, 2);  // measured best on B200 (tools/ab.sh)
   if (const char* e = std::getenv("DGAS_SPMV_G")) G = std::max(1, std::min(SpmvCfgMax(p), std::atoi(e)));
   return G;
 }
@@ -853,7 +867,7 @@ size_t spmv_smem_bytes(dgas_ctx ctx) {
 void launch_spmv(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s) {
   const int grid = ctx->spmv_grid, chunk = (ctx->nc + grid - 1) / grid;
   const size_t smem = spmv_smem_bytes(ctx);
-  DISPATCH_P(ctx->p, (k_spmv3<NP_><<<grid, SP_T, smem, s>>>(mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr,
+  DISPATCH_P(ctx->p, (k_spmv3<NP_><<<grid, SP_T + 32, smem, s>>>(mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr,
                                                             ctx->d_a_off, ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st,
                                                             ctx->d_partials, ctx->d_alpha, ctx->spmv_slots,
                                                             ctx->spmv_slot_bytes, ctx->max_deg * ctx->np,
@@ -878,8 +892,9 @@ int spmv_set_smem(dgas_ctx ctx, size_t smem) {
 }
 
 void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cudaStream_t s) {
-  DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_restrict<NP_, NQ_><<<ctx->ncoarse, RW * 32, 0, s>>>(
-                                            mode, ctx->d_cov_ptr, ctx->d_cov, ctx->d_ov_cell, ctx->d_fov_ptr,
+  const int wpj = ctx->restrict_wpj, grid = (ctx->ncoarse + (RT / 32 / wpj) - 1) / (RT / 32 / wpj);
+  DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_restrict<NP_, NQ_><<<grid, RT, 0, s>>>(
+                                            mode, ctx->ncoarse, wpj, ctx->d_cov_ptr, ctx->d_cov, ctx->d_ov_cell, ctx->d_fov_ptr,
                                             ctx->d_fov, ctx->d_G, r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf, ctx->d_x,
                                             ctx->d_b, ctx->d_r0, st, ctx->d_partials))));
 }
