@@ -168,3 +168,82 @@ def config(k: int, p: int | None = None, q: int | None = None, scale: str = "ful
         return generate(1, nc, seed=5, lloyd=5, sub_mode=1, n_sub=ns, coarse_mode=0,
                         name=f"cfg5{'s' if small else ''}_p{p}q{q}", p=p, q=q, f_kind=F_SINSIN)
     raise ValueError(k)
+
+
+# ---------------------------------------------------------------- paper regime
+PAPER_EX2 = {  # Table tab:ASPCG_P1_poly / _P3_poly: K (iters), rows H, cols N_h
+    1: {16: {64: (20.70, 45), 256: (72.31, 86), 1024: (269.70, 163), 4096: (818.09, 289)},
+        8: {256: (21.89, 46), 1024: (73.42, 86), 4096: (261.36, 163)},
+        4: {1024: (20.91, 46), 4096: (83.77, 91)},
+        2: {4096: (23.08, 48)}},
+    3: {16: {64: (88.63, 80), 256: (291.77, 145), 1024: (1137.55, 276), 4096: (3241.64, 513)},
+        8: {256: (102.96, 82), 1024: (278.15, 140), 4096: (949.21, 271)},
+        4: {1024: (90.30, 79), 4096: (343.19, 148)},
+        2: {4096: (104.24, 82)}},
+}
+PAPER_EX4 = {  # Table tab:ASPCG_Cond_Nest0_hHfine_HHcoarse_P1 / _P3: rows N_H, cols N_h
+    1: {16: {64: (23.29, 38), 256: (92.13, 77), 1024: (387.61, 159), 4096: (1624.26, 324), 16384: (6370.86, 657)},
+        64: {256: (25.91, 39), 1024: (106.42, 84), 4096: (411.02, 167), 16384: (1774.19, 342)},
+        256: {1024: (26.73, 41), 4096: (100.89, 82), 16384: (425.97, 169)},
+        1024: {4096: (31.81, 44), 16384: (118.61, 86)},
+        4096: {16384: (30.56, 43)}},
+    3: {16: {64: (148.36, 83), 256: (429.84, 143), 1024: (1602.53, 275), 4096: (5405.40, 529), 16384: (21263.66, 1058)},
+        64: {256: (142.42, 76), 1024: (405.44, 135), 4096: (1525.94, 263), 16384: (5170.13, 498)},
+        256: {1024: (157.47, 80), 4096: (452.41, 137), 16384: (1469.08, 249)},
+        1024: {4096: (147.97, 77), 16384: (402.98, 124)},
+        4096: {16384: (135.77, 70)}},
+}
+
+
+def paper_case(example: int, n_fine: int, coarse: int, p: int, seed: int = 17) -> Problem:
+    """The paper's experimental regime: T_HH = T_h (every cell its own subdomain),
+    Voronoi fine mesh of n_fine cells on (0,1)^2, rho = 1, q = p, C_sigma = 10.
+    example 2: nested agglomerates with H = coarse * h_bar (h_bar = h of the 4096-cell mesh, so the
+               coarse mesh has 4096 / coarse^2 RCB agglomerates; PAPER.md:851-853);
+    example 4: an independently generated Voronoi coarse mesh of `coarse` cells.
+    The paper never states f; BASELINE's f = 2 pi^2 sin sin is used (R21)."""
+    if example == 2:
+        n_coarse = max(1, 4096 // (coarse * coarse))
+        return generate(1, n_fine, seed=seed, lloyd=5, sub_mode=1, n_sub=n_fine, coarse_mode=1, n_coarse=n_coarse,
+                        name=f"ex2_h{n_fine}_H{coarse}_p{p}", p=p, q=p, f_kind=F_SINSIN)
+    if example == 4:
+        return generate(1, n_fine, seed=seed, lloyd=5, sub_mode=1, n_sub=n_fine, coarse_mode=4, n_coarse=coarse,
+                        name=f"ex4_h{n_fine}_H{coarse}_p{p}", p=p, q=p, f_kind=F_SINSIN)
+    raise ValueError(example)
+
+
+PAPER_EX1 = {  # Tables tab:RhoAlignedAndNotAligned / ...NonCOnvex (PAPER.md:786-816): K vs rho_e = 10..1e6
+    "convex": {("aligned", 1): [231, 233, 234, 234, 234, 234], ("aligned", 2): [612, 614, 614, 612, 611, 610],
+               ("not_aligned", 1): [292, 1.04e3, 7.73e3, 7.42e4, 7.39e5, 7.38e6],
+               ("not_aligned", 2): [654, 2.26e3, 1.71e4, 1.65e5, 1.64e6, 1.64e7]},
+    "nonconvex": {("aligned", 1): [965, 1.15e3, 1.20e3, 1.21e3, 1.21e3, 1.21e3],
+                  ("aligned", 2): [2.47e3, 2.86e3, 3.18e3, 3.25e3, 3.26e3, 3.26e3],
+                  ("not_aligned", 1): [802, 2.09e3, 1.68e4, 1.65e5, 1.64e6, 1.64e7],
+                  ("not_aligned", 2): [2.36e3, 6.10e3, 4.74e4, 4.62e5, 4.61e6, 4.61e7]},
+}
+
+
+def paper_case_ex1(variant: str, aligned: bool, rho_e: float, p: int, levels: int = 3, n_fine: int = 2000,
+                   n_coarse: int = 16, seed: int = 11) -> Problem:
+    """Ex.1: L-shaped domain, T_HH = T_h, q = p, rho_o = 1 and rho_e on even-indexed
+    elements. variant "convex": a Voronoi coarse mesh of 16 convex cells on the L, fine mesh by `levels`
+    centroid-midpoint refinements (nested); variant "nonconvex": a Voronoi fine mesh of n_fine cells on the
+    L with RCB agglomerates (METIS is out of scope; R33). aligned: rho_e on coarse elements D_j
+    with even 1-based index j; not aligned: rho_e on fine elements with even 1-based index."""
+    if variant == "convex":
+        # the cell around the re-entrant corner splits into two convex cells (gen.cpp clip_L), so fewer
+        # seeds may be needed for exactly n_coarse coarse cells
+        for ns in (n_coarse, n_coarse - 1, n_coarse - 2):
+            P = generate(2, levels, seed=seed, lloyd=5, sub_mode=2, coarse_mode=5, n_coarse=ns,
+                         name=f"ex1c_l{levels}_{'al' if aligned else 'na'}_p{p}", p=p, q=p, f_kind=F_SINSIN)
+            if P.n_coarse == n_coarse:
+                break
+    elif variant == "nonconvex":
+        P = generate(3, n_fine, seed=seed, lloyd=5, sub_mode=2, coarse_mode=1, n_coarse=n_coarse,
+                     name=f"ex1n_{n_fine}_{'al' if aligned else 'na'}_p{p}", p=p, q=p, f_kind=F_SINSIN)
+    else:
+        raise ValueError(variant)
+    idx = P.parent if aligned else np.arange(P.n_cells)
+    P.kappa = np.where(idx % 2 == 1, float(rho_e), 1.0)
+    P.meta.update(rho_e=rho_e, aligned=aligned, variant=variant)
+    return P

@@ -223,6 +223,111 @@ void make_cartesian(int n, Mesh& m) {
     }
 }
 
+// ------------------------------------------------------------------ L-shaped domain (paper Ex.1)
+// L = [0,1]^2 minus the quadrant (1/2,1] x [0,1/2) (re-entrant corner at (1/2,1/2); the paper's
+// (-1,1)^2-type L scaled by 1/2, which leaves K unchanged). A Voronoi cell of the unit square is cut to
+// the L as A = cell ∩ {x <= 1/2} and B = cell ∩ {x >= 1/2, y >= 1/2}; when both are non-empty the cell is
+// split into the two convex polygons A and B unless cell ∩ L is already a single half-plane clip
+// (only cells around the corner split, which can add one or two cells to the requested count).
+const double LC = 0.5;
+bool in_L(P2 s) { return !(s.x > LC && s.y < LC); }
+
+void clip_L(const Poly& c, std::vector<Poly>& out) {
+  Poly a = clip_halfplane(c, {LC, 0}, {1, 0});                         // x <= 1/2
+  Poly b = clip_halfplane(clip_halfplane(c, {LC, 0}, {-1, 0}), {0, LC}, {0, -1});  // x >= 1/2, y >= 1/2
+  double ac = std::fabs(poly_area(c)), tol = 1e-12 * ac;
+  double aa = a.size() >= 3 ? std::fabs(poly_area(a)) : 0, ab = b.size() >= 3 ? std::fabs(poly_area(b)) : 0;
+  if (std::fabs(aa + ab - ac) <= tol) { out.push_back(c); return; }   // cell inside L
+  // cell ∩ L is convex when it is a single half-plane clip of the cell; only otherwise split into A, B
+  Poly up = clip_halfplane(c, {0, LC}, {0, -1});                      // y >= 1/2
+  double au = up.size() >= 3 ? std::fabs(poly_area(up)) : 0;
+  if (std::fabs(au - (aa + ab)) <= tol) { out.push_back(up); return; }
+  if (std::fabs(aa - (aa + ab)) <= tol) { out.push_back(a); return; }
+  if (aa > tol) out.push_back(a);
+  if (ab > tol) out.push_back(b);
+}
+
+// insert every mesh vertex that lies strictly inside another cell's edge into that cell's loop, so that
+// faces are conforming vertex pairs (the split above creates such hanging vertices)
+void insert_hanging(Mesh& m) {
+  const int NV = (int)m.xy.size() / 2;
+  const int G = std::max(1, (int)std::sqrt((double)NV));
+  std::vector<std::vector<int>> bk(G * G);
+  auto bi = [&](double v) { return std::min(G - 1, std::max(0, (int)(v * G))); };
+  for (int i = 0; i < NV; ++i) bk[bi(m.xy[2 * i + 1]) * G + bi(m.xy[2 * i])].push_back(i);
+  std::vector<int> nptr(1, 0), nv;
+  for (int c = 0; c < m.ncells(); ++c) {
+    const int n = m.cptr[c + 1] - m.cptr[c];
+    for (int k = 0; k < n; ++k) {
+      int ia = m.cvtx[m.cptr[c] + k], ib = m.cvtx[m.cptr[c] + (k + 1) % n];
+      nv.push_back(ia);
+      P2 a = m.v(ia), b = m.v(ib);
+      double L2 = (b.x - a.x) * (b.x - a.x) + (b.y - a.y) * (b.y - a.y);
+      std::vector<std::pair<double, int>> hits;
+      for (int yy = bi(std::min(a.y, b.y)); yy <= bi(std::max(a.y, b.y)); ++yy)
+        for (int xx = bi(std::min(a.x, b.x)); xx <= bi(std::max(a.x, b.x)); ++xx)
+          for (int j : bk[yy * G + xx]) {
+            if (j == ia || j == ib) continue;
+            P2 v = m.v(j);
+            double t = ((v.x - a.x) * (b.x - a.x) + (v.y - a.y) * (b.y - a.y)) / L2;
+            if (t <= 1e-9 || t >= 1 - 1e-9) continue;
+            double cr = (b.x - a.x) * (v.y - a.y) - (b.y - a.y) * (v.x - a.x);
+            if (cr * cr <= 1e-22 * L2 * L2) hits.push_back({t, j});
+          }
+      std::sort(hits.begin(), hits.end());
+      for (auto& h : hits) nv.push_back(h.second);
+    }
+    nptr.push_back((int)nv.size());
+  }
+  m.cptr = nptr; m.cvtx = nv;
+}
+
+bool make_voronoi_L(int N, uint64_t seed, int lloyd, Mesh& m, std::string& err) {
+  Rng rng(seed);
+  std::vector<P2> seeds;
+  while ((int)seeds.size() < N) {                                       // uniform in L by rejection
+    P2 s = {rng.uniform(), rng.uniform()};
+    if (in_L(s)) seeds.push_back(s);
+  }
+  std::vector<Poly> cells, parts;
+  for (int it = 0; it < lloyd; ++it) {                                  // Lloyd on cell ∩ L
+    voronoi(seeds, cells);
+    for (int i = 0; i < N; ++i) {
+      parts.clear();
+      clip_L(cells[i], parts);
+      double A = 0, cx = 0, cy = 0;
+      for (auto& q : parts) { double a = poly_area(q); P2 c = poly_centroid(q); A += a; cx += a * c.x; cy += a * c.y; }
+      if (A > 0) seeds[i] = {cx / A, cy / A};
+    }
+  }
+  voronoi(seeds, cells);
+  std::vector<Poly> out;
+  for (auto& c : cells) clip_L(c, out);
+  if (!weld(out, m, err)) return false;
+  insert_hanging(m);
+  return true;
+}
+
+// one level of centroid-midpoint refinement ("successive refinement of elements"): an
+// n-gon v_0..v_{n-1} with centroid c becomes the n quadrilaterals (c, m_{i-1,i}, v_i, m_{i,i+1});
+// shared edges are split at the same midpoint on both sides, so the result is conforming.
+// parent[c'] = the cell c' came from; children of one cell are consecutive.
+void refine_once(const Mesh& m, Mesh& out, std::vector<int>& parent, std::string& err) {
+  std::vector<Poly> cells;
+  parent.clear();
+  for (int c = 0; c < m.ncells(); ++c) {
+    Poly p = m.poly(c);
+    P2 g = poly_centroid(p);
+    const int n = (int)p.size();
+    for (int i = 0; i < n; ++i) {
+      P2 vp = p[(i + n - 1) % n], v = p[i], vn = p[(i + 1) % n];
+      cells.push_back({g, {0.5 * (vp.x + v.x), 0.5 * (vp.y + v.y)}, v, {0.5 * (v.x + vn.x), 0.5 * (v.y + vn.y)}});
+      parent.push_back(c);
+    }
+  }
+  weld(cells, out, err);
+}
+
 // ------------------------------------------------------------------ partitions
 std::vector<P2> centroids(const Mesh& m) {
   std::vector<P2> c(m.ncells());
@@ -542,25 +647,68 @@ std::vector<int> cart_tiles(int n, int t) {
 
 extern "C" {
 
-// kind: 0 = Cartesian n x n, 1 = Voronoi with n cells
-// sub_mode: 0 = Cartesian tiles of sub_tile^2 cells, 1 = RCB into n_sub parts
+// kind: 0 = Cartesian n x n, 1 = Voronoi with n cells, 2 = L-shape Voronoi of n_coarse cells refined n
+//       times, 3 = L-shape Voronoi with n cells
+// sub_mode: 0 = Cartesian tiles of sub_tile^2 cells, 1 = RCB into n_sub parts, 2 = one cell per subdomain
 // coarse_mode: 0 = coarse = subdomains (nested), 1 = RCB into n_coarse (nested), 2 = Cartesian tiles
-//              of coarse_tile^2 (nested), 3 = RCB into n_coarse + merged edges (non-nested)
+//              of coarse_tile^2 (nested), 3 = RCB into n_coarse + merged edges (non-nested),
+//              4 = independent Voronoi mesh of n_coarse cells (non-nested, paper Ex.4),
+//              5 = the refinement parent of kind 2 (nested)
 // kappa_mode: 0 = 1 everywhere, 1 = 10^U(-4,4) per subdomain (stream seeded with seed ^ 0x6b617070)
 void* dgas_gen_problem(int kind, int n, uint64_t seed, int lloyd, int sub_mode, int sub_tile, int n_sub,
                        int coarse_mode, int coarse_tile, int n_coarse, int kappa_mode) {
   Problem* P = new Problem();
   Mesh& m = P->mesh;
+  std::vector<int> refine_parent;
   if (kind == 0) make_cartesian(n, m);
-  else if (!make_voronoi(n, seed, lloyd, m, P->err)) return P;
+  else if (kind == 1) { if (!make_voronoi(n, seed, lloyd, m, P->err)) return P; }
+  else if (kind == 2) {
+    // L-shape: Voronoi mesh of n_coarse cells refined n times (Ex.1, first variant); parent = refinement
+    Mesh cur;
+    if (!make_voronoi_L(n_coarse, seed, lloyd, cur, P->err)) return P;
+    refine_parent.resize(cur.ncells());
+    std::iota(refine_parent.begin(), refine_parent.end(), 0);
+    P->ncoarse = cur.ncells();
+    for (int l = 0; l < n; ++l) {
+      Mesh nx;
+      std::vector<int> par;
+      refine_once(cur, nx, par, P->err);
+      if (!P->err.empty()) return P;
+      for (int& v : par) v = refine_parent[v];
+      refine_parent = par;
+      cur = nx;
+    }
+    m = cur;
+  } else if (kind == 3) { if (!make_voronoi_L(n, seed, lloyd, m, P->err)) return P; }
+  else { P->err = "unknown mesh kind"; return P; }
   int NC = m.ncells();
   if (sub_mode == 0) { P->part = cart_tiles(n, sub_tile); P->nsub = (n / sub_tile) * (n / sub_tile); }
+  else if (sub_mode == 2) { P->part.resize(NC); std::iota(P->part.begin(), P->part.end(), 0); P->nsub = NC; }
   else { P->part = rcb(m, n_sub); P->nsub = n_sub; }
   P->nested = 1;
   if (coarse_mode == 0) { P->parent = P->part; P->ncoarse = P->nsub; }
   else if (coarse_mode == 1) { P->parent = rcb(m, n_coarse); P->ncoarse = n_coarse; }
+  else if (coarse_mode == 5) {
+    if (kind != 2) { P->err = "coarse_mode 5 needs kind 2 (refinement hierarchy)"; return P; }
+    P->parent = refine_parent;
+  }
   else if (coarse_mode == 2) { P->parent = cart_tiles(n, coarse_tile); P->ncoarse = (n / coarse_tile) * (n / coarse_tile); }
-  else {
+  else if (coarse_mode == 4) {
+    // independent Voronoi coarse mesh (Ex.4 "independently generated"): seeds from the
+    // stream seed ^ 0x636f61727365, same Lloyd count; pieces kappa ∩ D_J by convex clipping
+    Mesh cm;
+    if (!make_voronoi(n_coarse, seed ^ 0x636f61727365ULL, lloyd, cm, P->err)) return P;
+    std::vector<Poly> cp(cm.ncells());
+    for (int J = 0; J < cm.ncells(); ++J) cp[J] = cm.poly(J);
+    std::vector<int> bad;
+    if (!compute_overlaps(m, cp, P->ov, bad)) { P->err = "independent coarse mesh: overlap coverage failed"; return P; }
+    P->nested = 0; P->ncoarse = cm.ncells();
+    P->cpoly_ptr.assign(1, 0);
+    for (auto& poly : cp) {
+      for (auto& v : poly) { P->cpoly_xy.push_back(v.x); P->cpoly_xy.push_back(v.y); }
+      P->cpoly_ptr.push_back((int)P->cpoly_xy.size() / 2);
+    }
+  } else {
     std::vector<int> agg = rcb(m, n_coarse);
     fix_connectivity(m, agg, n_coarse);
     std::vector<Poly> cp;

@@ -112,6 +112,16 @@ int dgas_spmv(dgas_ctx ctx, const double* x, double* y, void* stream);
 /* z = P^-1 r = Q A0^-1 Q^T r + sum_i E_i A_i^-1 E_i^T r (device vectors, caller order). */
 int dgas_apply(dgas_ctx ctx, const double* r, double* z, void* stream);
 
+/* Which preconditioner dgas_apply and dgas_pcg use (default DGAS_PRECOND_TWO_LEVEL):
+ *   TWO_LEVEL  P^-1 = R0^T A0^-1 R0 + sum_i R_i^T A_i^-1 R_i        (eq:Pad)
+ *   ONE_LEVEL  P^-1 = sum_i R_i^T A_i^-1 R_i  (no coarse space)
+ *   COARSE     P^-1 = R0^T A0^-1 R0           (coarse space only; singular as a preconditioner unless
+ *                                              V_H spans V_h, test/diagnostic use)
+ *   NONE       P^-1 = I, plain CG: its Lanczos estimate is K(A_h) (Tables of Ex.3)
+ * Returns DGAS_E_INVALID_ARG for an unknown mode. Takes effect for the next call on the context. */
+enum { DGAS_PRECOND_TWO_LEVEL = 0, DGAS_PRECOND_ONE_LEVEL = 1, DGAS_PRECOND_COARSE = 2, DGAS_PRECOND_NONE = 3 };
+int dgas_set_precond(dgas_ctx ctx, int mode);
+
 /* ASPCG: solves A x = b from the initial guess in x (device vectors, caller order); stops when
  * ||b - A x_k||_2 (recursive residual) <= rtol ||b||_2 or after maxit iterations. Writes the
  * iteration count and the Lanczos estimate lambda_max/lambda_min of P^-1 A built from the same

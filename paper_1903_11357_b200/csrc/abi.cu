@@ -159,6 +159,22 @@ extern "C" int dgas_apply(dgas_ctx ctx, const double* r, double* z, void* stream
   return DGAS_OK;
 }
 
+extern "C" int dgas_set_precond(dgas_ctx ctx, int mode) {
+  if (!ctx || mode < DGAS_PRECOND_TWO_LEVEL || mode > DGAS_PRECOND_NONE) return DGAS_E_INVALID_ARG;
+  if (mode == ctx->precond) return DGAS_OK;
+  int st = finish_setup_buffers(ctx);
+  if (st) return st;
+  // the PCG graph bakes the kernel sequence in: rebuild it on the next solve
+  if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
+  if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
+  ctx->precond = mode;
+  if (mode == DGAS_PRECOND_ONE_LEVEL || mode == DGAS_PRECOND_NONE) {
+    DGAS_CUDA(cudaMemset(ctx->d_z0, 0, (size_t)ctx->N0 * sizeof(double)));
+    DGAS_CUDA(cudaDeviceSynchronize());
+  }
+  return DGAS_OK;
+}
+
 // Internal-order hooks used by bench.py's kernel timing (same kernels as inside the PCG graph).
 extern "C" int dgas_bench_kernels(dgas_ctx ctx, int which, int reps, void* stream) {
   if (!ctx || reps < 1) return DGAS_E_INVALID_ARG;

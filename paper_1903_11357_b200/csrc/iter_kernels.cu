@@ -915,8 +915,41 @@ int local_threads(int p) {
 }
 
 // z = P^-1 r minus the prolongation: coarse solve on the side stream || local solves on s
+// preconditioner variants without local solves (dgas_set_precond): z = r (NONE) or z = 0 (COARSE); the
+// coarse part is added by k_prolong as for the two-level operator
+__global__ void k_zfill(int mode, int copy, int64_t n, const double* r_in, double* const* rbuf, double* z,
+                        const PcgState* st) {
+  const double* r = r_in;
+  if (mode >= 1) {
+    if (st->done) return;
+    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = copy ? r[i] : 0.0;
+}
+
+static void launch_coarse_part(dgas_ctx ctx, int mode, PcgState* st, cudaStream_t s) {
+  if (ctx->coarse_mode == 2) nd_solve_launch(ctx, mode, st, s);
+  else
+    k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt,
+                                                  ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
+}
+
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
   static const bool no_fork = std::getenv("DGAS_NO_FORK") != nullptr;
+  if (ctx->precond != 0) {
+    // variants (z0 is zeroed by dgas_set_precond when the coarse part is off)
+    if (ctx->precond == 2) launch_coarse_part(ctx, mode, st, s);
+    if (ctx->precond == 1) {
+      const size_t smem = apply_smem_bytes(ctx);
+      DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
+                             mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf,
+                             z, st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+    } else {
+      k_zfill<<<2 * 148, 256, 0, s>>>(mode, ctx->precond == 3, ctx->N, r, ctx->d_rbuf, z, st);
+    }
+    return;
+  }
   if (no_fork) {
     if (ctx->coarse_mode == 2) nd_solve_launch(ctx, mode, st, s);
     else

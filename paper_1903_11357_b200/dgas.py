@@ -19,7 +19,8 @@ E_INVALID_ARG, E_MESH, E_NOT_SPD, E_BREAKDOWN, E_CUDA, E_NOMEM = -1, -2, -3, -4,
 
 EXPORTS = ["dgas_setup", "dgas_rhs", "dgas_spmv", "dgas_apply", "dgas_pcg", "dgas_pcg_host", "dgas_info",
            "dgas_history", "dgas_debug_block", "dgas_debug_basis", "dgas_debug_A0", "dgas_bench_kernels",
-           "dgas_destroy", "dgas_strerror", "dgas_error_detail"]
+           "dgas_destroy", "dgas_strerror", "dgas_error_detail", "dgas_set_precond"]
+PRECOND = {"two_level": 0, "one_level": 1, "coarse": 2, "none": 3}   # DGAS_PRECOND_* (include/dgas.h)
 
 
 class Mesh(ctypes.Structure):
@@ -71,6 +72,7 @@ def load():
     L.dgas_debug_basis.argtypes = [_P, ctypes.c_int32, _P]
     L.dgas_debug_A0.argtypes = [_P, _P]
     L.dgas_bench_kernels.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P]
+    L.dgas_set_precond.argtypes = [_P, ctypes.c_int]
     L.dgas_destroy.argtypes = [_P]
     L.dgas_strerror.restype = ctypes.c_char_p
     L.dgas_strerror.argtypes = [ctypes.c_int]
@@ -176,6 +178,10 @@ class Solver:
         z = torch.empty_like(r) if out is None else out
         self._check(load().dgas_apply(self.ctx, _dptr(r), _dptr(z), _stream(stream)))
         return z
+
+    def set_precond(self, mode):
+        """mode: "two_level" (default), "one_level", "coarse" or "none" (plain CG)."""
+        self._check(load().dgas_set_precond(self.ctx, PRECOND[mode] if isinstance(mode, str) else int(mode)))
 
     def pcg(self, b, x=None, rtol=1e-8, maxit=5000, stream=None):
         """Solve A x = b (device tensors). Returns (x, iters, cond, status)."""

@@ -47,6 +47,11 @@ CASES = {
     "cfg5s_p4q4": lambda: g.config(5, 4, 4, scale="small"),
     "cfg5s_p6q1": lambda: g.config(5, 6, 1, scale="small"),
     "cfg5s_p6q6": lambda: g.config(5, 6, 6, scale="small"),
+    # paper regime T_HH = T_h: nested agglomeration (Ex.2) and independent
+    # non-nested Voronoi coarse meshes (Ex.4)
+    "ex2_h256_H8_p1": lambda: g.paper_case(2, 256, 8, 1),
+    "ex4_h256_H16_p3": lambda: g.paper_case(4, 256, 16, 3),
+    "ex4_h1024_H64_p1": lambda: g.paper_case(4, 1024, 64, 1),
 }
 _cache = {}
 
@@ -304,3 +309,46 @@ def test_nested_dissection_coarse_path(monkeypatch, name, leaf):
     ref = o.pcg(b, rtol=1e-8)
     x, iters, cond, st = S.pcg(_dev(b), rtol=1e-8)
     assert st == 0 and abs(iters - ref["iters"]) <= 2
+
+
+@pytest.mark.parametrize("name", ["cfg2s", "ex4_h256_H16_p3", "cfg4s"])
+def test_precond_variants(name):
+    """dgas_set_precond: one-level (no coarse space), coarse only, and none (plain CG,
+    whose Lanczos estimate is K(A_h)) against the oracle with the same parts switched off."""
+    P = CASES[name]()
+    S = _solver(P)
+    b = None
+    for mode in ("one_level", "coarse", "none"):
+        o = O.Oracle(P)
+        o.setup_schwarz(use_coarse=mode != "one_level", use_local=mode != "coarse")
+        S.set_precond(mode)
+        r = g.normal(7, S.N)
+        z = S.apply(_dev(r)).cpu().numpy()
+        if mode == "none":
+            assert np.array_equal(z, r)
+        else:
+            zr = o.apply(r)
+            assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr), mode
+        if mode == "coarse":
+            continue  # R0^T A0^-1 R0 alone is singular on V_h: not a preconditioner for PCG
+        b = o.rhs() if b is None else b
+        ref = o.pcg(b, rtol=1e-8, maxit=20000, precond=mode != "none")
+        x, iters, cond, st = S.pcg(_dev(b), rtol=1e-8, maxit=20000)
+        assert st == 0 and ref["status"] == 0
+        # long unpreconditioned runs: the stopping iteration drifts with rounding (R22), compare x at
+        # a common iteration count and K to 1%
+        assert abs(iters - ref["iters"]) <= max(2, 0.02 * ref["iters"]), (mode, iters, ref["iters"])
+        k = min(iters, ref["iters"])
+        xk, ik, _, _ = S.pcg(_dev(b), rtol=1e-300, maxit=k)
+        rk = o.pcg(b, rtol=1e-300, maxit=k, precond=mode != "none")
+        assert np.linalg.norm(xk.cpu().numpy() - rk["x"]) <= 1e-7 * np.linalg.norm(rk["x"]), mode
+        assert abs(cond - ref["cond"]) <= 0.01 * ref["cond"], (mode, cond, ref["cond"])
+    S.set_precond("two_level")
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    r = g.normal(8, S.N)
+    zr = o.apply(r)
+    assert np.linalg.norm(S.apply(_dev(r)).cpu().numpy() - zr) <= 1e-10 * np.linalg.norm(zr)
+    with pytest.raises(Exception):
+        S.set_precond(7)
+    S.close()

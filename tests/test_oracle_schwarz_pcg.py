@@ -235,3 +235,72 @@ def test_P10_p_scaling_nested():
         Ks.append(_K(P)); ps.append(p)
     slope = np.polyfit(np.log(ps), np.log(Ks), 1)[0]
     assert 0.6 <= slope <= 1.4, (Ks, slope)
+
+
+# ---------------------------------------------------------------- paper regime
+def _paper_run(ex, nf, coarse, p):
+    P = g.paper_case(ex, nf, coarse, p)
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    return o.pcg(o.rhs(), rtol=1e-8)  # rtol 1e-8, x0 = 0
+
+
+@pytest.mark.parametrize("ex", [2, 4])
+def test_paper_tables_p1_magnitude_and_trend(ex):
+    """Tables tab:ASPCG_P1_poly and tab:ASPCG_Cond_Nest0_hHfine_HHcoarse_P1
+    (PAPER.md:998-1002). Our seeded Voronoi meshes are not the paper's, so the printed values pin
+    magnitude (K within [0.3, 1.5]x, iterations within [0.6, 1.2]x) and the stated trends: K grows like
+    (H/h)^2 along a row (fitted slope in [1.4, 2.3]) and stays nearly constant along the diagonal H/h = 2."""
+    tab = (g.PAPER_EX2 if ex == 2 else g.PAPER_EX4)[1]
+    first = next(iter(tab))                  # coarsest coarse mesh: H = 16 h_bar / N_H = 16
+    row, diag = [], []
+    for coarse, cols in tab.items():
+        for nf, (k_ref, it_ref) in cols.items():
+            if nf > 1024:
+                continue
+            r = _paper_run(ex, nf, coarse, 1)
+            assert 0.3 * k_ref <= r["cond"] <= 1.5 * k_ref, (coarse, nf, r["cond"], k_ref)
+            assert 0.6 * it_ref <= r["iters"] <= 1.2 * it_ref, (coarse, nf, r["iters"], it_ref)
+            if coarse == first:
+                row.append((nf, r["cond"]))
+            if nf == min(cols):
+                diag.append(r["cond"])
+    hh = np.sqrt([nf for nf, _ in row])      # H/h ~ sqrt(N_h) at fixed H
+    slope = np.polyfit(np.log(hh), np.log([k for _, k in row]), 1)[0]
+    assert 1.4 <= slope <= 2.3, (row, slope)
+    assert max(diag) / min(diag) < 2.0, diag
+
+
+def test_paper_table_p3_corner():
+    """tab:ASPCG_P3_poly H = 16 h_bar, h = 8 h_bar: 88.63 (80)."""
+    r = _paper_run(2, 64, 16, 3)
+    assert 0.3 * 88.63 <= r["cond"] <= 1.5 * 88.63 and 0.6 * 80 <= r["iters"] <= 1.2 * 80
+
+
+def _ex1(variant, aligned, rho_e, p, levels=3):
+    P = g.paper_case_ex1(variant, aligned, rho_e, p, levels=levels)
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    return o.pcg(o.rhs(), rtol=1e-8, maxit=20000)
+
+
+def test_paper_ex1_rho_dichotomy():
+    """Table tab:RhoAlignedAndNotAligned and Remark 6.6: aligned with T_H, K does not
+    depend on rho_e; not aligned, K grows linearly in rho_e. Values pin magnitude (p = 1, level-3
+    refinement of a 16-cell convex Voronoi coarse mesh): within [0.5, 2]x of the printed K."""
+    ref = g.PAPER_EX1["convex"]
+    al = [_ex1("convex", True, r, 1)["cond"] for r in (10.0, 1e3, 1e6)]
+    na = [_ex1("convex", False, r, 1)["cond"] for r in (10.0, 1e3, 1e6)]
+    assert max(al) / min(al) < 1.15, al
+    assert 500 <= na[2] / na[1] <= 2000, na
+    for k, r in zip(al, (ref[("aligned", 1)][0], ref[("aligned", 1)][2], ref[("aligned", 1)][5])):
+        assert 0.5 * r <= k <= 2 * r, (al, r)
+    for k, r in zip(na, (ref[("not_aligned", 1)][0], ref[("not_aligned", 1)][2], ref[("not_aligned", 1)][5])):
+        assert 0.5 * r <= k <= 2 * r, (na, r)
+
+
+def test_paper_ex1_rho_one_identical():
+    """rho_e = 1: the aligned and not-aligned problems are the same matrix (SPEC-style trivial case)."""
+    a = _ex1("convex", True, 1.0, 1, levels=1)
+    b = _ex1("convex", False, 1.0, 1, levels=1)
+    assert a["iters"] == b["iters"] and np.array_equal(a["x"], b["x"])

@@ -21,4 +21,7 @@ if [ -n "$NCU_FULL" ]; then
   timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"${NCU_KERNELS:-k_local|k_spmv3}" -s ${NCU_FSKIP:-6} -c ${NCU_FCOUNT:-2} -o gpurun_out/prof_$NCU_FULL -f python bench.py --config $NCU_FULL --steps 1 --warmup 1 --no-cpu-baseline --kernel-reps 2 > gpurun_out/ncu_full.log 2>&1
   echo "ncu full rc $?" >> $L
 fi
+if [ -n "$PAPER" ]; then
+  timeout 1500 python tools/paper_tables.py $PAPER > gpurun_out/paper.log 2>&1; echo "paper rc $?" >> $L
+fi
 cat $L
