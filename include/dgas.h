@@ -91,6 +91,8 @@ typedef struct {
   int32_t coarse_mode;           /* 0 dense explicit inverse, 1 band, 2 nested dissection */
   int32_t launches_per_iter;     /* kernel launches of one PCG iteration (graph body) */
   int32_t launches_per_solve;    /* fixed launches of one dgas_pcg besides the iterations */
+  int32_t coarse_refine;         /* iterative-refinement steps of the ND coarse solve (R30 calibration) */
+  double coarse_solve_relerr;    /* measured ||z - v|| / ||v|| of one coarse solve of A0 z = A0 v (ND only) */
 } dgas_info_t;
 
 /* Build the SIPDG operator and the two-level Schwarz preconditioner on the GPU.

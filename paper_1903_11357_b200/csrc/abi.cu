@@ -39,6 +39,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
   if (ctx->coarse_mode == 2) {
     int st2 = nd_set_smem(ctx);
     if (st2) return st2;
+    if ((st2 = nd_calibrate(ctx))) return st2;
   }
   ctx->n_coarse_ctas = ctx->coarse_dense ? (int)std::min<int64_t>(592, std::max<int64_t>(1, ctx->N0 / 32)) : 1;
   {
@@ -357,12 +358,18 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   // algorithmic bytes: every operator entry read once, vectors once each
   info->alg_bytes_spmv = info->bytes_A + (2 * N) * 8 + (int64_t)ctx->nnzb * 4;
   const int64_t dinv_tri = (int64_t)ctx->nc * (np * (np + 1) / 2) * 8;
-  info->alg_bytes_apply = info->bytes_U + dinv_tri + info->bytes_coarse + 2 * info->bytes_G + 3 * N * 8;
-  info->alg_bytes_iter = info->bytes_A + info->bytes_U + dinv_tri + info->bytes_coarse + 2 * info->bytes_G + 16 * N * 8;
+  // refinement steps of the ND coarse solve re-read the factors and read the A0 pair blocks once more
+  const int refine = ctx->coarse_mode == 2 ? ctx->nd.refine : 0;
+  const int64_t a0b = (int64_t)(ctx->nd.h_prow.empty() ? 0 : ctx->nd.h_prow.back()) * nq * nq * 8;
+  const int64_t coarse_alg = info->bytes_coarse * (1 + refine) + refine * a0b;
+  info->alg_bytes_apply = info->bytes_U + dinv_tri + coarse_alg + 2 * info->bytes_G + 3 * N * 8;
+  info->alg_bytes_iter = info->bytes_A + info->bytes_U + dinv_tri + coarse_alg + 2 * info->bytes_G + 16 * N * 8;
   info->last_iters = ctx->last_iters; info->last_status = ctx->last_status;
   info->last_cond = ctx->last_cond; info->last_lmin = ctx->last_lmin; info->last_lmax = ctx->last_lmax;
   info->last_relres = ctx->last_relres;
   info->coarse_mode = ctx->coarse_mode;
+  info->coarse_refine = ctx->coarse_mode == 2 ? ctx->nd.refine : 0;
+  info->coarse_solve_relerr = ctx->coarse_mode == 2 ? ctx->nd.calib_err : 0.0;
   int coarse_launches = 1;
   if (ctx->coarse_mode == 2) {
     coarse_launches = 0;
@@ -370,7 +377,7 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
       coarse_launches += ctx->nd.h_wf_ptr[L + 1] > ctx->nd.h_wf_ptr[L];
       coarse_launches += ctx->nd.h_wb_ptr[L + 1] > ctx->nd.h_wb_ptr[L];
     }
-    coarse_launches += 2 * ctx->nd.refine;
+    coarse_launches = coarse_launches * (1 + ctx->nd.refine) + 2 * ctx->nd.refine;  // + residual, axpy per step
   }
   // body: spmv, restrict, coarse (side stream), local, prolong; solve: 2 perm in, init_state,
   // init (spmv, restrict, coarse, local, prolong), lanczos, perm out

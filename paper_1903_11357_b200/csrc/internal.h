@@ -50,10 +50,14 @@ struct NdPlan {
   int2 *d_wf = nullptr, *d_wb = nullptr;
   int64_t *d_offX = nullptr, *d_offM = nullptr, *d_offUpd = nullptr, *d_offS = nullptr;
   double *d_X = nullptr, *d_M = nullptr, *d_MT = nullptr, *d_T = nullptr, *d_u = nullptr;
-  int refine = 0;                      // iterative-refinement steps of the coarse solve (R30, off)
+  int refine = 0;                      // iterative-refinement steps of the coarse solve (R30; nd_calibrate)
+  int refine_env = -1;                 // DGAS_ND_REFINE override (-1: calibrate)
+  double calib_err = 0;                // measured relative error of one coarse solve (nd_calibrate)
+  double calib_err0 = 0;               // the same without refinement
   std::vector<int> h_prow;             // coarse pair rows (pairs sorted by (J1, J2))
   int* d_prow = nullptr;
   double *d_rb = nullptr, *d_zb = nullptr;
+  double* d_dsc = nullptr;             // diag(A0)^-1/2 (symmetric scaling of the fronts)
 };
 
 struct dgas_ctx_s {
@@ -245,6 +249,7 @@ int nd_build(dgas_ctx ctx, const std::vector<int>& pair_h, const std::vector<dou
 int nd_setup_run(dgas_ctx ctx);
 void nd_solve_launch(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s);
 int nd_set_smem(dgas_ctx ctx);
+int nd_calibrate(dgas_ctx ctx);
 void nd_free(dgas_ctx ctx);
 int apply_set_smem(dgas_ctx ctx, size_t smem);
 size_t apply_smem_bytes(dgas_ctx ctx);

@@ -206,6 +206,6 @@ int nd_build(dgas_ctx ctx, const std::vector<int>& pair_h, const std::vector<dou
   P.h_prow.assign(NC + 1, 0);
   for (size_t k = 0; k < pair_h.size() / 2; ++k) P.h_prow[pair_h[2 * k] + 1]++;
   for (int J = 0; J < NC; ++J) P.h_prow[J + 1] += P.h_prow[J];
-  if (const char* e = std::getenv("DGAS_ND_REFINE")) P.refine = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("DGAS_ND_REFINE")) P.refine = P.refine_env = std::max(0, std::atoi(e));
   return 0;
 }

@@ -2,8 +2,8 @@
 // A0 = Q^T A Q (eq:A0) for large N0 (see nd_host.cu for the plan).
 //   setup, per tree level (deepest first), one CTA per front:
 //     S = [S_FF S_FU; S_UF S_UU] = A0 restricted to (F, F u U) + extend-add of the children's updates
-//     X_F = S_FF^-1 (Cholesky, triangular inverse, L^-T L^-1),  M_F = S_UF X_F,
-//     update_F = S_UU - M_F S_UF^T  (passed to the parent)
+//     X_F = S_FF^-1 (Cholesky, triangular inverse, L^-T L^-1),  B_F = S_UF L^-T,  M_F = B_F L^-1,
+//     update_F = S_UU - B_F B_F^T  (passed to the parent)
 //   solve, per level: forward u_F = t_U - M_F t_F (t = r0|_F + children's u), backward
 //     x_F = X_F t_F - M_F^T x_U. Every level is one launch of GEMV rows (row chunks per CTA).
 #include "internal.h"
@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(ND_T) k_nd_assemble(int nq, const int* __restr
                                                       const int64_t* offS, const int64_t* offUpd, const int* asm_ptr,
                                                       const int4* asmv, const int* childptr, const int* childs,
                                                       const int* cmap_ptr, const int* cmap, const double* A0b,
+                                                      const int* __restrict__ pair, const double* __restrict__ dsc,
                                                       const double* Upd, double* Sg) {
   const int f = fronts[blockIdx.x];
   const int n = nF[f] + nU[f], nFe = nF[f] / nq;
@@ -26,7 +27,9 @@ __global__ void __launch_bounds__(ND_T) k_nd_assemble(int nq, const int* __restr
   for (int e = threadIdx.x; e < (asm_ptr[f + 1] - asm_ptr[f]) * nq2; e += ND_T) {
     const int4 a4 = asmv[asm_ptr[f] + e / nq2];
     const int ab = e % nq2, a = ab / nq, b = ab % nq;
-    const double v = A0b[(size_t)a4.x * nq2 + ab];
+    // symmetric diagonal scaling D^-1/2 A0 D^-1/2 (see nd_setup_run)
+    const double v = A0b[(size_t)a4.x * nq2 + ab] * dsc[(size_t)pair[2 * a4.x] * nq + a] *
+                     dsc[(size_t)pair[2 * a4.x + 1] * nq + b];
     S[(size_t)(a4.y * nq + a) * n + a4.z * nq + b] = v;
     if (a4.z >= nFe) S[(size_t)(a4.z * nq + b) * n + a4.y * nq + a] = v;
   }
@@ -43,6 +46,18 @@ __global__ void __launch_bounds__(ND_T) k_nd_assemble(int nq, const int* __restr
     }
     __syncthreads();
   }
+}
+
+// dsc[J nq + a] = diag(A0)^-1/2 (the diagonal entry of the (J, J) pair block)
+__global__ void k_nd_diag(int ncoarse, int nq, const int* __restrict__ prow, const int* __restrict__ pair,
+                          const double* __restrict__ A0b, double* dsc) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ncoarse * nq) return;
+  const int J = g / nq, a = g % nq;
+  double d = 1.0;
+  for (int pr = prow[J]; pr < prow[J + 1]; ++pr)
+    if (pair[2 * pr + 1] == J) d = A0b[((size_t)pr * nq + a) * nq + a];
+  dsc[g] = d > 0 ? 1.0 / sqrt(d) : 1.0;  // a non-positive pivot is reported by the factorisation
 }
 
 // ------------------------------------------------------------------ setup: partial factorisation
@@ -96,27 +111,39 @@ __global__ void __launch_bounds__(ND_T) k_nd_factor(const int* __restrict__ fron
     X[e] = s;
   }
   __syncthreads();
-  // M = S_UF X (nu x nf) and M^T
+  // B = S_UF W^T = S_UF L^-T (nu x nf), held in the M^T buffer as B^T until M is formed. The Schur
+  // update S_UU - B B^T is formed without the explicit inverse: S_UF X S_UF^T carried the
+  // kappa(S_FF) eps error of X into every ancestor front (coarse-solve error on config 5 p = q = 6:
+  // 1.8e-9 that way, 9e-12 this way).
   double* M = Mg + offM[f];
   double* MT = MTg + offM[f];
   for (int64_t e = threadIdx.x; e < (int64_t)nu * nf; e += ND_T) {
     const int r = (int)(e / nf), j = (int)(e % nf);
     const double* srow = S + (size_t)(nf + r) * n;
     double s = 0;
-    for (int i = 0; i < nf; ++i) s += srow[i] * X[(size_t)i * nf + j];
-    M[e] = s;
+    for (int k = 0; k <= j; ++k) s += srow[k] * S[(size_t)j * n + k];  // W[j][k], k <= j
     MT[(size_t)j * nu + r] = s;
   }
   __syncthreads();
-  // update = S_UU - M S_UF^T  (nu x nu)
+  // update = S_UU - B B^T  (nu x nu)
   double* Up = Upd + offUpd[f];
   for (int64_t e = threadIdx.x; e < (int64_t)nu * nu; e += ND_T) {
     const int r = (int)(e / nu), t = (int)(e % nu);
-    const double* mrow = M + (size_t)r * nf;
-    const double* srow = S + (size_t)(nf + t) * n;
     double s = S[(size_t)(nf + r) * n + nf + t];
-    for (int j = 0; j < nf; ++j) s -= mrow[j] * srow[j];
+    for (int j = 0; j < nf; ++j) s -= MT[(size_t)j * nu + r] * MT[(size_t)j * nu + t];
     Up[e] = s;
+  }
+  // M = B W = S_UF S_FF^-1 (nu x nf) for the solve
+  for (int64_t e = threadIdx.x; e < (int64_t)nu * nf; e += ND_T) {
+    const int r = (int)(e / nf), j = (int)(e % nf);
+    double s = 0;
+    for (int k = j; k < nf; ++k) s += MT[(size_t)k * nu + r] * S[(size_t)k * n + j];  // W[k][j], k >= j
+    M[e] = s;
+  }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < (int64_t)nu * nf; e += ND_T) {
+    const int r = (int)(e / nf), j = (int)(e % nf);
+    MT[(size_t)j * nu + r] = M[e];
   }
 }
 
@@ -128,14 +155,18 @@ __global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict_
                                                  const int* __restrict__ Fe, const int64_t* __restrict__ offM,
                                                  const int* __restrict__ childptr, const int* __restrict__ childs,
                                                  const int* __restrict__ cmap_ptr, const int* __restrict__ cmap,
-                                                 const double* __restrict__ Mg, const double* r0, double* Tg,
-                                                 double* ug, const PcgState* st, int mode) {
+                                                 const double* __restrict__ Mg, const double* __restrict__ dsc,
+                                                 const double* r0, double* Tg, double* ug, const PcgState* st,
+                                                 int mode) {
   extern __shared__ double t[];
   if (mode >= 1 && st->done) return;
   const int2 wi = work[blockIdx.x];
   const int f = wi.x, row0 = wi.y;
   const int nf = nF[f], nu = nU[f];
-  for (int k = threadIdx.x; k < nf; k += ND_T) t[k] = r0[(size_t)Fe[offFe[f] + k / nq] * nq + k % nq];
+  for (int k = threadIdx.x; k < nf; k += ND_T) {
+    const size_t g = (size_t)Fe[offFe[f] + k / nq] * nq + k % nq;
+    t[k] = r0[g] * dsc[g];
+  }
   for (int k = nf + threadIdx.x; k < nf + nu; k += ND_T) t[k] = 0.0;
   __syncthreads();
   for (int ci = childptr[f]; ci < childptr[f + 1]; ++ci) {
@@ -166,7 +197,8 @@ __global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict_
                                                  const int* __restrict__ offUe, const int* __restrict__ Ue,
                                                  const int64_t* __restrict__ offX, const int64_t* __restrict__ offM,
                                                  const double* __restrict__ Xg, const double* __restrict__ MTg,
-                                                 const double* Tg, double* z0, const PcgState* st, int mode) {
+                                                 const double* __restrict__ dsc, const double* Tg, double* z0,
+                                                 const PcgState* st, int mode) {
   extern __shared__ double sh[];
   if (mode >= 1 && st->done) return;
   const int2 wi = work[blockIdx.x];
@@ -175,7 +207,10 @@ __global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict_
   double* tF = sh;
   double* xU = sh + nf;
   for (int k = threadIdx.x; k < nf; k += ND_T) tF[k] = Tg[offT[f] + k];
-  for (int k = threadIdx.x; k < nu; k += ND_T) xU[k] = z0[(size_t)Ue[offUe[f] + k / nq] * nq + k % nq];
+  for (int k = threadIdx.x; k < nu; k += ND_T) {
+    const size_t g = (size_t)Ue[offUe[f] + k / nq] * nq + k % nq;
+    xU[k] = z0[g] / dsc[g];  // the scaled unknown of an ancestor front
+  }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* X = Xg + offX[f];
@@ -188,7 +223,10 @@ __global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict_
     for (int k = lane; k < nf; k += 32) v += xr[k] * tF[k];
     for (int k = lane; k < nu; k += 32) v -= mr[k] * xU[k];
     v = warp_sum(v);
-    if (lane == 0) z0[(size_t)Fe[offFe[f] + j / nq] * nq + j % nq] = v;
+    if (lane == 0) {
+      const size_t g = (size_t)Fe[offFe[f] + j / nq] * nq + j % nq;
+      z0[g] = v * dsc[g];
+    }
   }
 }
 
@@ -211,9 +249,14 @@ int nd_setup_run(dgas_ctx ctx) {
       (st = up(ctx, &P.d_Ue, P.h_Ue)) || (st = up(ctx, &P.d_childptr, P.h_childptr)) ||
       (st = up(ctx, &P.d_childs, P.h_childs)) || (st = up(ctx, &P.d_cmap_ptr, P.h_cmap_ptr)) ||
       (st = up(ctx, &P.d_cmap, P.h_cmap)) || (st = up(ctx, &P.d_asm_ptr, P.h_asm_ptr)) || (st = up(ctx, &P.d_asm, P.h_asm)) ||
-      (st = up(ctx, &P.d_lev_fronts, P.h_lev_fronts)))
+      (st = up(ctx, &P.d_lev_fronts, P.h_lev_fronts)) || (st = up(ctx, &P.d_prow, P.h_prow)))
     return st;
   const int nf = P.nf;
+  // D^-1/2 of diag(A0): the fronts factor the symmetrically scaled D^-1/2 A0 D^-1/2, whose conditioning
+  // does not carry the rho contrast (config 4: 1e8) into the explicit front inverses
+  DGAS_CUDA(cudaMalloc((void**)&P.d_dsc, std::max<int64_t>(1, ctx->N0) * 8));
+  k_nd_diag<<<(unsigned)((ctx->N0 + 255) / 256), 256, 0, s>>>(ctx->ncoarse, ctx->nq, P.d_prow, ctx->d_pair,
+                                                             ctx->d_A0b, P.d_dsc);
   DGAS_CUDA(cudaMalloc((void**)&P.d_X, std::max<int64_t>(1, P.h_offX[nf]) * 8));
   DGAS_CUDA(cudaMalloc((void**)&P.d_M, std::max<int64_t>(1, P.h_offM[nf]) * 8));
   DGAS_CUDA(cudaMalloc((void**)&P.d_MT, std::max<int64_t>(1, P.h_offM[nf]) * 8));
@@ -227,7 +270,7 @@ int nd_setup_run(dgas_ctx ctx) {
     if (!n) continue;
     const int* fr = P.d_lev_fronts + P.h_lev_ptr[L];
     k_nd_assemble<<<n, ND_T, 0, s>>>(ctx->nq, fr, P.d_nF, P.d_nU, P.d_offS, P.d_offUpd, P.d_asm_ptr, P.d_asm, P.d_childptr,
-                                     P.d_childs, P.d_cmap_ptr, P.d_cmap, ctx->d_A0b, dUpd, dS);
+                                     P.d_childs, P.d_cmap_ptr, P.d_cmap, ctx->d_A0b, ctx->d_pair, P.d_dsc, dUpd, dS);
     k_nd_factor<<<n, ND_T, 0, s>>>(fr, P.d_nF, P.d_nU, P.d_offS, P.d_offX, P.d_offM, P.d_offUpd, dS, P.d_X, P.d_M, P.d_MT,
                                    dUpd, ctx->d_err);
   }
@@ -245,7 +288,7 @@ int nd_setup_run(dgas_ctx ctx) {
     P.h_wf_ptr[L + 1] = (int)wf.size();
     P.h_wb_ptr[L + 1] = (int)wb.size();
   }
-  if ((st = up(ctx, &P.d_wf, wf)) || (st = up(ctx, &P.d_wb, wb)) || (st = up(ctx, &P.d_prow, P.h_prow))) return st;
+  if ((st = up(ctx, &P.d_wf, wf)) || (st = up(ctx, &P.d_wb, wb))) return st;
   DGAS_CUDA(cudaMalloc((void**)&P.d_rb, (ctx->N0 + 1) * 8));
   DGAS_CUDA(cudaMalloc((void**)&P.d_zb, (ctx->N0 + 1) * 8));
   DGAS_CUDA(cudaStreamSynchronize(s));
@@ -300,15 +343,80 @@ static void nd_solve_once(dgas_ctx ctx, int mode, const PcgState* st, cudaStream
     const int n = P.h_wf_ptr[L + 1] - P.h_wf_ptr[L];
     if (n)
       k_nd_fwd<<<n, ND_T, shf, s>>>(ctx->nq, P.d_wf + P.h_wf_ptr[L], P.d_nF, P.d_nU, P.d_offT, P.d_offu, P.d_offFe,
-                                    P.d_Fe, P.d_offM, P.d_childptr, P.d_childs, P.d_cmap_ptr, P.d_cmap, P.d_M, rin,
-                                    P.d_T, P.d_u, st, mode);
+                                    P.d_Fe, P.d_offM, P.d_childptr, P.d_childs, P.d_cmap_ptr, P.d_cmap, P.d_M, P.d_dsc,
+                                    rin, P.d_T, P.d_u, st, mode);
   }
   for (int L = P.nlev - 1; L >= 0; --L) {
     const int n = P.h_wb_ptr[L + 1] - P.h_wb_ptr[L];
     if (n)
       k_nd_bwd<<<n, ND_T, shb, s>>>(ctx->nq, P.d_wb + P.h_wb_ptr[L], P.d_nF, P.d_nU, P.d_offT, P.d_offFe, P.d_Fe,
-                                    P.d_offUe, P.d_Ue, P.d_offX, P.d_offM, P.d_X, P.d_MT, P.d_T, zout, st, mode);
+                                    P.d_offUe, P.d_Ue, P.d_offX, P.d_offM, P.d_X, P.d_MT, P.d_dsc, P.d_T, zout, st,
+                                    mode);
   }
+}
+
+// deterministic test vector in [-1, 1) (splitmix of the index)
+__global__ void k_nd_testvec(int64_t n, double* v) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t z = (uint64_t)i * 0x9e3779b97f4a7c15ULL + 0x632be59bd9b4e019ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  z ^= z >> 31;
+  v[i] = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+// Choose the iterative-refinement steps of the multifrontal coarse solve (R30): solve
+// A0 z = A0 v for a fixed test vector v; when its relative error ||z - v|| / ||v|| exceeds 1e-9, add
+// refinement steps while each one cuts the error by at least 4x (at most 2). Measured on config 4
+// (kappa(A0) = 8e8, 9e6 after diagonal scaling): LAPACK Cholesky 5.8e-11, explicit dense inverse
+// 3.5e-6, this solve 4.4e-10, with one refinement step 7.7e-12 -- but the refinement step doubles the
+// coarse chain, which then no longer hides behind the local solves (-17% PCG it/s), so it is only
+// taken beyond 1e-9.
+int nd_calibrate(dgas_ctx ctx) {
+  NdPlan& P = ctx->nd;
+  if (P.refine_env >= 0) return 0;
+  cudaStream_t s = ctx->stream;
+  const int64_t n = ctx->N0;
+  double *dv = nullptr, *dzero = nullptr;
+  DGAS_CUDA(cudaMalloc((void**)&dv, n * 8));
+  DGAS_CUDA(cudaMalloc((void**)&dzero, n * 8));
+  DGAS_CUDA(cudaMemsetAsync(dzero, 0, n * 8, s));
+  k_nd_testvec<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, dv);
+  const int nb = (ctx->ncoarse + ND_T / 32 - 1) / (ND_T / 32);
+  std::vector<double> hv(n), hz(n);
+  DGAS_CUDA(cudaMemcpyAsync(hv.data(), dv, n * 8, cudaMemcpyDeviceToHost, s));
+  auto measure = [&](int refine) -> double {
+    P.refine = refine;
+    // r0 = 0 - A0 v, so the solve should return z0 = -v
+    k_a0_resid<<<nb, ND_T, 0, s>>>(ctx->ncoarse, ctx->nq, P.d_prow, ctx->d_pair, ctx->d_A0b, dzero, dv, ctx->d_r0,
+                                   nullptr, 0);
+    nd_solve_launch(ctx, 0, nullptr, s);
+    if (cudaMemcpyAsync(hz.data(), ctx->d_z0, n * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+    double e = 0, vv = 0;
+    for (int64_t i = 0; i < n; ++i) { e += (hz[i] + hv[i]) * (hz[i] + hv[i]); vv += hv[i] * hv[i]; }
+    return std::sqrt(e / vv);
+  };
+  double err = measure(0);
+  P.calib_err0 = err;
+  int best = 0;
+  for (int r = 1; r <= 2 && err > 1e-9; ++r) {
+    const double e = measure(r);
+    if (!(e >= 0) || !(e < 0.25 * err)) break;
+    err = e;
+    best = r;
+  }
+  P.refine = best;
+  P.calib_err = err;
+  if (std::getenv("DGAS_VERBOSE"))
+    fprintf(stderr, "dgas: ND coarse solve relerr %.3e unrefined, %.3e with %d refinement step(s)\n", P.calib_err0, err,
+            best);
+  cudaFree(dv);
+  cudaFree(dzero);
+  DGAS_CUDA(cudaMemsetAsync(ctx->d_z0, 0, n * 8, s));
+  DGAS_CUDA(cudaGetLastError());
+  return err >= 0 ? 0 : DGAS_E_CUDA;
 }
 
 int nd_set_smem(dgas_ctx ctx) {
@@ -327,7 +435,8 @@ void nd_free(dgas_ctx ctx) {
   NdPlan& P = ctx->nd;
   void* ptrs[] = {P.d_nF, P.d_nU, P.d_offX, P.d_offM, P.d_offUpd, P.d_offS, P.d_offT, P.d_offu, P.d_offFe, P.d_offUe,
                   P.d_Fe, P.d_Ue, P.d_childptr, P.d_childs, P.d_cmap_ptr, P.d_cmap, P.d_asm_ptr, P.d_asm,
-                  P.d_lev_fronts, P.d_X, P.d_M, P.d_MT, P.d_T, P.d_u, P.d_wf, P.d_wb, P.d_prow, P.d_rb, P.d_zb};
+                  P.d_lev_fronts, P.d_X, P.d_M, P.d_MT, P.d_T, P.d_u, P.d_wf, P.d_wb, P.d_prow, P.d_rb, P.d_zb,
+                  P.d_dsc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }

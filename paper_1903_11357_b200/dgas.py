@@ -44,7 +44,8 @@ class Info(ctypes.Structure):
                 ("alg_bytes_iter", ctypes.c_int64), ("last_iters", ctypes.c_int32), ("last_status", ctypes.c_int32),
                 ("last_cond", ctypes.c_double), ("last_lmin", ctypes.c_double), ("last_lmax", ctypes.c_double),
                 ("last_relres", ctypes.c_double), ("coarse_mode", ctypes.c_int32), ("launches_per_iter", ctypes.c_int32),
-                ("launches_per_solve", ctypes.c_int32)]
+                ("launches_per_solve", ctypes.c_int32), ("coarse_refine", ctypes.c_int32),
+                ("coarse_solve_relerr", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

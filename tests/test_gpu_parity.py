@@ -298,6 +298,10 @@ def test_nested_dissection_coarse_path(monkeypatch, name, leaf):
     monkeypatch.setenv("DGAS_ND_LEAF", leaf)
     P = CASES[name]()
     S = _solver(P)
+    info = S.get_info()
+    assert info["coarse_mode"] == 2
+    # setup-time calibration of the ND solve (R30): one solve of A0 z = A0 v within 1e-9 after refinement
+    assert 0 < info["coarse_solve_relerr"] <= 1e-9 and 0 <= info["coarse_refine"] <= 2
     o = O.Oracle(P)
     o.setup_schwarz()
     for seed in range(3):
@@ -331,6 +335,8 @@ def test_precond_variants(name):
             assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr), mode
         if mode == "coarse":
             continue  # R0^T A0^-1 R0 alone is singular on V_h: not a preconditioner for PCG
+        if mode == "none" and P.kappa.max() > 10 * P.kappa.min():
+            continue  # plain CG on the 1e8 rho-jump matrix does not converge in 20000 iterations
         b = o.rhs() if b is None else b
         ref = o.pcg(b, rtol=1e-8, maxit=20000, precond=mode != "none")
         x, iters, cond, st = S.pcg(_dev(b), rtol=1e-8, maxit=20000)
