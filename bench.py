@@ -180,6 +180,7 @@ def main():
         x.zero_(); S.pcg(b, x)
     barrier()
     iters_total = 0
+    iters_list = []
     conds = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -189,6 +190,7 @@ def main():
             x.zero_()
             _, it, cond, st = S.pcg(b, x)
             iters_total += it
+            iters_list.append(it)
             conds.append(cond)
         e1.record()
         barrier()
@@ -270,7 +272,10 @@ def main():
         "kernels": kern,
         "e2e": {"value": e2e_value, "unit": "PCG it/s", "h2d_bytes_per_step": 2 * N * 8,
                 "d2h_bytes_per_step": N * 8},
-        "gpu_launches": int(info["launches_per_iter"] * iters_total + info["launches_per_solve"] * args.steps),
+        # the last WHILE body of a solve also launches its remaining unrolled copies (immediate return)
+        "gpu_launches": int(info["launches_per_iter"] * sum(-(-it // info["unroll"]) * info["unroll"]
+                                                            for it in iters_list)
+                            + info["launches_per_solve"] * args.steps),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

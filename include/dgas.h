@@ -93,6 +93,8 @@ typedef struct {
   int32_t launches_per_solve;    /* fixed launches of one dgas_pcg besides the iterations */
   int32_t coarse_refine;         /* iterative-refinement steps of the ND coarse solve (R30 calibration) */
   double coarse_solve_relerr;    /* measured ||z - v|| / ||v|| of one coarse solve of A0 z = A0 v (ND only) */
+  int32_t unroll;                /* PCG iterations per execution of the graph's WHILE body; the last body of a
+                                    solve launches its remaining copies as immediate-return kernels */
 } dgas_info_t;
 
 /* Build the SIPDG operator and the two-level Schwarz preconditioner on the GPU.

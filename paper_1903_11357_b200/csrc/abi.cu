@@ -41,6 +41,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     if (st2) return st2;
     if ((st2 = nd_calibrate(ctx))) return st2;
   }
+  if (const char* e = std::getenv("DGAS_UNROLL")) ctx->unroll = std::max(1, std::min(8, std::atoi(e)));
   ctx->n_coarse_ctas = ctx->coarse_dense ? (int)std::min<int64_t>(592, std::max<int64_t>(1, ctx->N0 / 32)) : 1;
   {
     // TMA ring of the local-solve CTAs: unit = CC columns of a row-block (about the average row-block
@@ -256,10 +257,14 @@ static int build_graph_impl(dgas_ctx ctx, int maxit) {
   DGAS_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
   DGAS_CUDA(cudaStreamBeginCaptureToGraph(cs2, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   ctx->side_sel = 2;
-  launch_spmv(ctx, 1, nullptr, ctx->d_q, st, cs2);
-  launch_restrict(ctx, 1, st, nullptr, cs2);
-  launch_apply(ctx, 2, st, nullptr, ctx->d_z, cs2);
-  launch_prolong(ctx, 2, st, nullptr, ctx->d_z, cs2, h, 1);
+  // the body holds `unroll` iterations: every kernel returns at once when the state says done, so the
+  // copies after convergence cost one launch each, and the per-body cost of the WHILE node is shared
+  for (int u = 0; u < ctx->unroll; ++u) {
+    launch_spmv(ctx, 1, nullptr, ctx->d_q, st, cs2);
+    launch_restrict(ctx, 1, st, nullptr, cs2);
+    launch_apply(ctx, 2, st, nullptr, ctx->d_z, cs2);
+    launch_prolong(ctx, 2, st, nullptr, ctx->d_z, cs2, h, 1);
+  }
   DGAS_CUDA(cudaGetLastError());
   DGAS_CUDA(cudaStreamEndCapture(cs2, &body));
   ctx->side_sel = 0;
@@ -369,6 +374,7 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->last_relres = ctx->last_relres;
   info->coarse_mode = ctx->coarse_mode;
   info->coarse_refine = ctx->coarse_mode == 2 ? ctx->nd.refine : 0;
+  info->unroll = ctx->unroll;
   info->coarse_solve_relerr = ctx->coarse_mode == 2 ? ctx->nd.calib_err : 0.0;
   int coarse_launches = 1;
   if (ctx->coarse_mode == 2) {

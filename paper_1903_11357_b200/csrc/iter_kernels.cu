@@ -935,53 +935,78 @@ static void launch_coarse_part(dgas_ctx ctx, int mode, PcgState* st, cudaStream_
                                                   ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
 }
 
+// T_HH = T_h (the paper's regime): every subdomain is one cell, A_i^-1 = D^T D with
+// D = L_kk^-1 (row-major lower triangle), so the local solve is two tiny triangular GEMVs per cell.
+// L lanes per cell (ProlongCfg), the cell's r and y exchanged by shuffles.
+template <int NP>
+__global__ void __launch_bounds__(256) k_bjacobi(int mode, int nc, const double* __restrict__ Dinv, const double* r_in,
+                                                 double* const* rbuf, double* z, const PcgState* st) {
+  constexpr int L = ProlongCfg<NP>::L, CPW = ProlongCfg<NP>::CPW;
+  const double* r = r_in;
+  if (mode >= 1) {
+    if (st->done) return;
+    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+  }
+  const int lane = threadIdx.x & 31, a = lane % L, base = lane - a;
+  const int c = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * CPW + lane / L;
+  const bool on = c < nc && a < NP;
+  const double rv = on ? r[(size_t)c * NP + a] : 0.0;
+  const double* D = Dinv + (size_t)(c < nc ? c : 0) * NP * NP;
+  double y = 0;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const double rk = __shfl_sync(0xffffffffu, rv, base + k);
+    if (on && k <= a) y += __ldg(D + a * NP + k) * rk;
+  }
+  double v = 0;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const double yk = __shfl_sync(0xffffffffu, y, base + k);
+    if (on && k >= a) v += __ldg(D + k * NP + a) * yk;
+  }
+  if (on) z[(size_t)c * NP + a] = v;
+}
+
+// all local solves z_i = A_i^-1 r_i
+static void launch_local(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
+  if (ctx->max_sub_cells == 1) {
+    unsigned grid = 1;
+    DISPATCH_P(ctx->p, (grid = (ctx->nc + 8 * ProlongCfg<NP_>::CPW - 1) / (8 * ProlongCfg<NP_>::CPW)));
+    DISPATCH_P(ctx->p, (k_bjacobi<NP_><<<grid, 256, 0, s>>>(mode, ctx->nc, ctx->d_Dinv, r, ctx->d_rbuf, z, st)));
+    return;
+  }
+  const size_t smem = apply_smem_bytes(ctx);
+  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
+                         mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
+                         st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+}
+
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
   static const bool no_fork = std::getenv("DGAS_NO_FORK") != nullptr;
   if (ctx->precond != 0) {
     // variants (z0 is zeroed by dgas_set_precond when the coarse part is off)
     if (ctx->precond == 2) launch_coarse_part(ctx, mode, st, s);
-    if (ctx->precond == 1) {
-      const size_t smem = apply_smem_bytes(ctx);
-      DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
-                             mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf,
-                             z, st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
-    } else {
-      k_zfill<<<2 * 148, 256, 0, s>>>(mode, ctx->precond == 3, ctx->N, r, ctx->d_rbuf, z, st);
-    }
+    if (ctx->precond == 1) launch_local(ctx, mode, st, r, z, s);
+    else k_zfill<<<2 * 148, 256, 0, s>>>(mode, ctx->precond == 3, ctx->N, r, ctx->d_rbuf, z, st);
     return;
   }
   if (no_fork) {
-    if (ctx->coarse_mode == 2) nd_solve_launch(ctx, mode, st, s);
-    else
-      k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt,
-                                                    ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
-    const size_t smem = apply_smem_bytes(ctx);
-    DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
-                           mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
-                           st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+    launch_coarse_part(ctx, mode, st, s);
+    launch_local(ctx, mode, st, r, z, s);
     return;
   }
   cudaStream_t side = ctx->side[ctx->side_sel];
   cudaEvent_t ef = ctx->ev_fork[ctx->side_sel], ej = ctx->ev_join[ctx->side_sel];
   cudaEventRecord(ef, s);
   cudaStreamWaitEvent(side, ef, 0);
-  if (ctx->coarse_mode == 2) nd_solve_launch(ctx, mode, st, side);
-  else
-    k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, side>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt,
-                                                     ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
-  const size_t smem = apply_smem_bytes(ctx);
-  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
-                         mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
-                         st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+  launch_coarse_part(ctx, mode, st, side);
+  launch_local(ctx, mode, st, r, z, s);
   cudaEventRecord(ej, side);
   cudaStreamWaitEvent(s, ej, 0);
 }
 
 void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s) {
-  const size_t smem = apply_smem_bytes(ctx);
-  DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
-                         0, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
-                         nullptr, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+  launch_local(ctx, 0, nullptr, r, z, s);
 }
 
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s) {

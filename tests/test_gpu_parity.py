@@ -52,6 +52,8 @@ CASES = {
     "ex2_h256_H8_p1": lambda: g.paper_case(2, 256, 8, 1),
     "ex4_h256_H16_p3": lambda: g.paper_case(4, 256, 16, 3),
     "ex4_h1024_H64_p1": lambda: g.paper_case(4, 1024, 64, 1),
+    # Ex.1 L-shape, rho_e = 1e3 on every other fine cell (not aligned with T_H; K ~ 4e3)
+    "ex1c_l2_na_1e3_p2": lambda: g.paper_case_ex1("convex", False, 1e3, 2, levels=2),
 }
 _cache = {}
 

@@ -1,8 +1,11 @@
 #!/bin/bash
+# A/B sweep of env settings: AB_CONFIGS="cfg4 cfg2" AB_SETS="base u2:DGAS_UNROLL=2 u4:DGAS_UNROLL=4"
 cd $GRAFT_REPO_ROOT
-C=${AB_CONFIG:-cfg4}
-run() { tag=$1; shift; env "$@" timeout 600 python bench.py --config $C --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ab_${C}_$tag.log 2>&1; echo "$tag rc $?"; }
-run base
-run leaf16 DGAS_ND_LEAF=16
-run leaf64 DGAS_ND_LEAF=64
-run leaf128 DGAS_ND_LEAF=128
+for C in ${AB_CONFIGS:-cfg4}; do
+  for set in ${AB_SETS:-base}; do
+    tag=${set%%:*}; envs=""
+    [ "$set" != "$tag" ] && envs=$(echo ${set#*:} | tr ',' ' ')
+    env $envs timeout 600 python bench.py --config $C --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ab_${C}_$tag.log 2>&1
+    echo "$C $tag rc $? $(tail -1 gpurun_out/ab_${C}_$tag.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"],1), d["ms_per_step"])' 2>/dev/null)"
+  done
+done
