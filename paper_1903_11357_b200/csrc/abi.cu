@@ -30,11 +30,24 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     DGAS_CUDA(cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming));
   }
   {
-    // restriction: about 4 overlap pieces per warp, 1..8 warps per coarse element
-    const int avg = (int)((ctx->nov + ctx->ncoarse - 1) / ctx->ncoarse);
+    // restriction: about 4 warp steps (32 / L pieces each) per warp; 1..8 warps per coarse element in one
+    // CTA, then more CTAs per coarse element (cpj) while the grid stays within the partials buffer
+    const int lanes = ctx->np <= 4 ? 4 : ctx->np <= 8 ? 8 : ctx->np <= 16 ? 16 : 32;
+    const int64_t per_warp = 4 * (32 / lanes);
+    const int64_t need = (ctx->nov + ctx->ncoarse * per_warp - 1) / (ctx->ncoarse * per_warp);  // warps per J
     int w = 1;
-    while (w < 8 && w * 4 < avg) w *= 2;
+    while (w < 8 && w < need) w *= 2;
     ctx->restrict_wpj = w;
+    int64_t cpj = w == 8 ? (need + 7) / 8 : 1;
+    cpj = std::min<int64_t>(cpj, std::max<int64_t>(1, ctx->partial_cap / 2 / std::max(1, ctx->ncoarse) - 1));
+    cpj = std::min<int64_t>(cpj, 64);
+    if (const char* e = std::getenv("DGAS_RESTRICT_CPJ")) cpj = std::max(1, std::atoi(e));
+    ctx->restrict_cpj = (int)cpj;
+    if (cpj > 1) {
+      DGAS_CUDA(cudaMalloc((void**)&ctx->d_rpart, (size_t)ctx->ncoarse * cpj * ctx->nq * sizeof(double)));
+      DGAS_CUDA(cudaMalloc((void**)&ctx->d_jcnt, (size_t)ctx->ncoarse * sizeof(unsigned)));
+      DGAS_CUDA(cudaMemsetAsync(ctx->d_jcnt, 0, (size_t)ctx->ncoarse * sizeof(unsigned), ctx->stream));
+    }
   }
   if (ctx->coarse_mode == 2) {
     int st2 = nd_set_smem(ctx);

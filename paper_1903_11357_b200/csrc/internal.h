@@ -66,7 +66,10 @@ struct dgas_ctx_s {
   int64_t N = 0, N0 = 0;
   double penalty = 10;
   int coarse_dense = 1, coarse_bw = 0, nT = 0, bt = 0;  // coarse tiles
-  int unroll = 1;            // PCG iterations per WHILE-body execution (DGAS_UNROLL)
+  int restrict_cpj = 1;      // CTAs per coarse element in k_restrict (partials in d_rpart, counters d_jcnt)
+  double* d_rpart = nullptr;
+  unsigned* d_jcnt = nullptr;
+  int unroll = 4;            // PCG iterations per WHILE-body execution (DGAS_UNROLL)
   int precond = 0;           // DGAS_PRECOND_*: 0 two-level, 1 one-level, 2 coarse only, 3 none
   int coarse_mode = 0;       // 0 dense explicit inverse, 1 band Cholesky (tile sweeps), 2 nested dissection
   NdPlan nd;

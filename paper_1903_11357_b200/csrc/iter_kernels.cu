@@ -53,6 +53,13 @@ __device__ inline bool last_block(const double* mine, double* partials, unsigned
   return true;
 }
 
+// lanes per cell row (or overlap piece) in the cell-wise vector kernels, cells per warp
+template <int NP>
+struct ProlongCfg {
+  static constexpr int L = NP <= 4 ? 4 : NP <= 8 ? 8 : NP <= 16 ? 16 : 32;  // lanes per cell
+  static constexpr int CPW = 32 / L;                                         // cells per warp
+};
+
 // ------------------------------------------------------------------ SpMV (+ fused direction update)
 // mode 0: y = A x.   mode 1 (PCG): p_new = z + beta p_old (beta = 0 at it = 0), q = A p_new, p.q.
 // One warp per cell row; the row block is n x (deg n) row-major, lanes stride its columns.
@@ -320,19 +327,24 @@ __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk
 // mode 0: r0 = Q^T r_in (no update).  mode 1 (PCG iteration): r_new = r_old - alpha q (owner pieces
 // write r_new and x += alpha p_new), r.r -> convergence test, r0 = Q^T r_new.
 // mode 2 (PCG init): r_new = b - q (q = A x0), r.r and b.b.
-// One CTA per coarse element J, one warp per overlap piece.
+// Pieces of J are spread over wpj warps of a CTA and, when J has many pieces (e.g. 16 coarse elements
+// over 16384 cells), over cpj CTAs whose partial sums the last-arriving CTA of J adds in split order
+// (deterministic). L lanes per piece (ProlongCfg), 32/L pieces per warp step; per-lane accumulation,
+// one warp reduction per coarse dof at the end.
 #define RT 256
 template <int NP, int NQ>
-__global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj, const int* __restrict__ cov_ptr,
+__global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj, int cpj, const int* __restrict__ cov_ptr,
                                                  const int* __restrict__ cov, const int* __restrict__ ov_cell,
                                                  const int* __restrict__ fov_ptr, const int* __restrict__ fov,
                                                  const double* __restrict__ G, const double* r_in, double* const* rbuf,
                                                  const double* q, double* const* pbuf, double* x, const double* b,
-                                                 double* r0, PcgState* st, double* partials) {
-  // wpj warps per coarse element (adaptive: ~4 pieces per warp), RT/32/wpj elements per CTA
+                                                 double* r0, double* rpart, unsigned* jcnt, PcgState* st,
+                                                 double* partials) {
+  constexpr int L = ProlongCfg<NP>::L, PPW = 32 / L;
   __shared__ double red[RT / 32];
   __shared__ double part[RT / 32][NQ];
   __shared__ double wsum[RT / 32][2];
+  __shared__ bool j_last;
   int it = 0;
   double alpha = 0;
   const double* rold = r_in;
@@ -350,48 +362,70 @@ __global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj,
       rnew = rbuf[0];
     }
   }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int jpc = (RT / 32) / wpj;
-  const int J = blockIdx.x * jpc + w / wpj, wj = w % wpj;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, a = lane % L;
+  const int jpc = cpj > 1 ? 1 : (RT / 32) / wpj;
+  const int J = cpj > 1 ? blockIdx.x / cpj : blockIdx.x * jpc + w / wpj;
+  const int split = cpj > 1 ? blockIdx.x % cpj : 0;
+  const int wj = w % wpj, TW = wpj * cpj, gw = split * wpj + wj;
   double accq[NQ];
 #pragma unroll
   for (int k = 0; k < NQ; ++k) accq[k] = 0;
   double rr = 0, bb = 0;
   if (J < ncoarse)
-    for (int k = cov_ptr[J] + wj; k < cov_ptr[J + 1]; k += wpj) {
+    for (int k = cov_ptr[J] + gw * PPW + lane / L; k < cov_ptr[J + 1]; k += TW * PPW) {
+      if (a >= NP) continue;
       const int o = cov[k], cell = ov_cell[o];
       const bool owner = fov[fov_ptr[cell]] == o;
-      double rv = 0;
-      if (lane < NP) {
-        size_t id = (size_t)cell * NP + lane;
-        if (mode == 0) rv = rold[id];
-        else if (mode == 1) rv = rold[id] - alpha * q[id];
-        else rv = b[id] - q[id];
-        if (owner && mode >= 1) {
-          rnew[id] = rv;
-          rr += rv * rv;
-          if (mode == 1) x[id] += alpha * pnew[id];
-          else bb += b[id] * b[id];
-        }
+      const size_t id = (size_t)cell * NP + a;
+      double rv;
+      if (mode == 0) rv = rold[id];
+      else if (mode == 1) rv = rold[id] - alpha * q[id];
+      else rv = b[id] - q[id];
+      if (owner && mode >= 1) {
+        rnew[id] = rv;
+        rr += rv * rv;
+        if (mode == 1) x[id] += alpha * pnew[id];
+        else bb += b[id] * b[id];
       }
-      const double* Go = G + (size_t)o * NP * NQ;
+      const double* Go = G + ((size_t)o * NP + a) * NQ;
 #pragma unroll
-      for (int c = 0; c < NQ; ++c) {
-        double v = lane < NP ? Go[lane * NQ + c] * rv : 0.0;
-        accq[c] += warp_sum(v);
-      }
+      for (int c = 0; c < NQ; ++c) accq[c] += Go[c] * rv;
     }
-  if (lane == 0)
-    for (int c = 0; c < NQ; ++c) part[w][c] = accq[c];
+#pragma unroll
+  for (int c = 0; c < NQ; ++c) {
+    const double v = warp_sum(accq[c]);
+    if (lane == 0) part[w][c] = v;
+  }
   rr = warp_sum(rr); bb = warp_sum(bb);
   if (lane == 0) { wsum[w][0] = rr; wsum[w][1] = bb; }
   __syncthreads();
-  for (int e = threadIdx.x; e < jpc * NQ; e += RT) {
-    const int jl = e / NQ, c = e % NQ, JJ = blockIdx.x * jpc + jl;
-    if (JJ >= ncoarse) continue;
-    double v = 0;
-    for (int k = 0; k < wpj; ++k) v += part[jl * wpj + k][c];
-    r0[(size_t)JJ * NQ + c] = v;
+  if (cpj == 1) {
+    for (int e = threadIdx.x; e < jpc * NQ; e += RT) {
+      const int jl = e / NQ, c = e % NQ, JJ = blockIdx.x * jpc + jl;
+      if (JJ >= ncoarse) continue;
+      double v = 0;
+      for (int k = 0; k < wpj; ++k) v += part[jl * wpj + k][c];
+      r0[(size_t)JJ * NQ + c] = v;
+    }
+  } else {
+    if (threadIdx.x < NQ) {
+      double v = 0;
+      for (int k = 0; k < wpj; ++k) v += part[k][threadIdx.x];
+      rpart[((size_t)J * cpj + split) * NQ + threadIdx.x] = v;
+      __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) j_last = atomicAdd(&jcnt[J], 1u) == (unsigned)cpj - 1;
+    __syncthreads();
+    if (j_last) {
+      __threadfence();
+      if (threadIdx.x < NQ) {
+        double v = 0;
+        for (int sp = 0; sp < cpj; ++sp) v += __ldcg(rpart + ((size_t)J * cpj + sp) * NQ + threadIdx.x);
+        r0[(size_t)J * NQ + threadIdx.x] = v;
+      }
+      if (threadIdx.x == 0) jcnt[J] = 0;
+    }
   }
   if (mode == 0) return;
   double mine[2] = {0, 0};
@@ -677,11 +711,6 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
 // z_kappa += sum_{pieces o of kappa} G_o z0_J(o).  mode 0: apply only.  mode 1: PCG init (gamma_0).
 // mode 2: PCG iteration (beta = gamma_new / gamma, history, it++, maxit, graph condition).
 #define PW 8
-template <int NP>
-struct ProlongCfg {
-  static constexpr int L = NP <= 4 ? 4 : NP <= 8 ? 8 : NP <= 16 ? 16 : 32;  // lanes per cell
-  static constexpr int CPW = 32 / L;                                         // cells per warp
-};
 template <int NP, int NQ>
 __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int* __restrict__ fov_ptr,
                                                      const int* __restrict__ fov, const int* __restrict__ ov_coarse,
@@ -892,11 +921,13 @@ int spmv_set_smem(dgas_ctx ctx, size_t smem) {
 }
 
 void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cudaStream_t s) {
-  const int wpj = ctx->restrict_wpj, grid = (ctx->ncoarse + (RT / 32 / wpj) - 1) / (RT / 32 / wpj);
+  const int wpj = ctx->restrict_wpj, cpj = ctx->restrict_cpj;
+  const int grid = cpj > 1 ? ctx->ncoarse * cpj : (ctx->ncoarse + (RT / 32 / wpj) - 1) / (RT / 32 / wpj);
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_restrict<NP_, NQ_><<<grid, RT, 0, s>>>(
-                                            mode, ctx->ncoarse, wpj, ctx->d_cov_ptr, ctx->d_cov, ctx->d_ov_cell, ctx->d_fov_ptr,
-                                            ctx->d_fov, ctx->d_G, r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf, ctx->d_x,
-                                            ctx->d_b, ctx->d_r0, st, ctx->d_partials))));
+                                            mode, ctx->ncoarse, wpj, cpj, ctx->d_cov_ptr, ctx->d_cov, ctx->d_ov_cell,
+                                            ctx->d_fov_ptr, ctx->d_fov, ctx->d_G, r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf,
+                                            ctx->d_x, ctx->d_b, ctx->d_r0, ctx->d_rpart, ctx->d_jcnt, st,
+                                            ctx->d_partials))));
 }
 
 size_t apply_smem_bytes(dgas_ctx ctx) {

@@ -308,7 +308,8 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
   ctx->nT = (int)((ctx->N0 + CT - 1) / CT);
   {
     // dense explicit A0^-1 up to 2048 coarse dofs (latency-bound small coarse problems), nested
-    // dissection above (measured on B200: cfg4 1274 -> 1374 it/s, cfg5 p6q6 1221 -> 1296);
+    // dissection above (measured on B200: cfg4 1274 -> 1374 it/s, cfg5 p6q6 1221 -> 1296)
+    // unless the cost model after nd_build below prefers the dense inverse;
     // DGAS_COARSE_MODE=dense|band|nd overrides (tests exercise every path on small problems)
     int64_t dense_max = 2048;
     if (const char* e = std::getenv("DGAS_COARSE_DENSE_MAX")) dense_max = std::atoll(e);
@@ -349,6 +350,25 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
     int leaf = 32;
     if (const char* e = std::getenv("DGAS_ND_LEAF")) leaf = std::max(2, std::atoi(e));
     if ((st = nd_build(ctx, pair_h, cen, leaf))) return bail(st, ctx->detail);
+    // automatic choice (no DGAS_COARSE_* override): the ND chain runs beside the local solves, so its
+    // cost is what sticks out of them; the dense GEMV instead adds its bytes to the shared HBM traffic.
+    // Model (B200 measurements): ~10 us per level launch in the graph (2 per level), ND
+    // bytes at ~2 TB/s, dense X and local factors at ~6 TB/s.
+    if (!std::getenv("DGAS_COARSE_MODE") && !std::getenv("DGAS_COARSE_DENSE_MAX")) {
+      const NdPlan& P = ctx->nd;
+      const double n0 = (double)ctx->N0, bw = 6.0e12;
+      const double dense_bytes = n0 * n0 * 8;
+      const double nd_bytes = (double)(P.h_offX[P.nf] + 2 * P.h_offM[P.nf]) * 8;
+      const double t_dense = dense_bytes / bw + 3e-6;
+      const double t_nd = 2 * 10e-6 * P.nlev + nd_bytes / 2.0e12;
+      const double t_local = ctx->max_sub_cells > 1 ? 2.0 * (double)ctx->u_total * 8 / bw : 0.0;
+      if (dense_bytes <= 4.0e9 && t_dense < std::max(0.0, t_nd - t_local)) {
+        ctx->nd = NdPlan();
+        ctx->coarse_mode = 0;
+        ctx->coarse_dense = 1;
+        ctx->bt = ctx->nT - 1;
+      }
+    }
   }
   // ------------------------------------------------ device buffers
   if ((st = dev_upload(ctx, &ctx->d_xy, cxy))) return bail(st, ctx->detail);
@@ -445,7 +465,7 @@ static void free_ctx(dgas_ctx ctx) {
                   ctx->d_contrib_ptr, ctx->d_contrib, ctx->d_x, ctx->d_r, ctx->d_z, ctx->d_q, ctx->d_b,
                   ctx->d_p[0], ctx->d_p[1], ctx->d_r0, ctx->d_z0, ctx->d_t1, ctx->d_t2, ctx->d_partials,
                   ctx->d_state, ctx->d_astate, ctx->d_alpha, ctx->d_beta, ctx->d_lanczos, ctx->d_err,
-                  ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev};
+                  ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev, ctx->d_rpart, ctx->d_jcnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->d_A0b) cudaFree(ctx->d_A0b);

@@ -314,7 +314,10 @@ def test_nested_dissection_coarse_path(monkeypatch, name, leaf):
     b = o.rhs()
     ref = o.pcg(b, rtol=1e-8)
     x, iters, cond, st = S.pcg(_dev(b), rtol=1e-8)
-    assert st == 0 and abs(iters - ref["iters"]) <= 2
+    assert st == 0
+    if abs(iters - ref["iters"]) > 2:  # R22: the oracle's own spread under 1e-13 perturbations of b
+        lo, hi = _oracle_spread(o, b, ref)
+        assert lo - 2 <= iters <= hi + 2, (iters, ref["iters"], lo, hi)
 
 
 @pytest.mark.parametrize("name", ["cfg2s", "ex4_h256_H16_p3", "cfg4s"])
