@@ -86,6 +86,13 @@ static int finish_setup_buffers(dgas_ctx ctx) {
       }
     }
     if (ctx->ring_slots < 2) { ctx->detail = "subdomain row-block too large for shared memory"; return DGAS_E_INVALID_ARG; }
+    {
+      // L2 reuse across the forward/backward turnaround: the units just below each subdomain's ring-
+      // resident tail are streamed evict-last (budget shared by all subdomains; vectors keep the rest)
+      double mb = 48;
+      if (const char* e = std::getenv("DGAS_LOCAL_REUSE_MB")) mb = std::atof(e);
+      ctx->local_reuse = (int)std::min<double>(1 << 20, mb * 1048576.0 / ((double)ctx->nsub * ctx->slot_bytes));
+    }
     int st = apply_set_smem(ctx, apply_smem_bytes(ctx));
     if (st) return st;
     int dev = 0, nsm = 148;

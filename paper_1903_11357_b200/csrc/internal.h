@@ -69,6 +69,7 @@ struct dgas_ctx_s {
   int restrict_cpj = 1;      // CTAs per coarse element in k_restrict (partials in d_rpart, counters d_jcnt)
   double* d_rpart = nullptr;
   unsigned* d_jcnt = nullptr;
+  int local_reuse = 0;       // units per subdomain kept in L2 (evict-last) for the backward sweep
   int unroll = 4;            // PCG iterations per WHILE-body execution (DGAS_UNROLL)
   int precond = 0;           // DGAS_PRECOND_*: 0 two-level, 1 one-level, 2 coarse only, 3 none
   int coarse_mode = 0;       // 0 dense explicit inverse, 1 band Cholesky (tile sweeps), 2 nested dissection

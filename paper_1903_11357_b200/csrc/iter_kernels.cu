@@ -549,7 +549,8 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
                                                                 const double* __restrict__ U,
                                                                 const double* __restrict__ Dinv, const double* r_in,
                                                                 double* const* rbuf, double* z, const PcgState* st,
-                                                                int S, uint32_t slot_bytes, int ymax_cells, int CC) {
+                                                                int S, uint32_t slot_bytes, int ymax_cells, int CC,
+                                                                int reuse) {
   constexpr int T = LocalCfg<NP>::T, NW = LocalCfg<NP>::W;
   extern __shared__ __align__(128) double sm[];
   const double* r = r_in;
@@ -592,11 +593,17 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
   if (threadIdx.x >= T) {
     // ---------------- producer warp (lane 0 issues every copy)
     if (threadIdx.x != T) return;
-    auto issue = [&](int u, int k) {
+    // the `reuse` units the backward sweep re-reads first (just below the ring-resident tail) are
+    // streamed evict-last in the forward sweep, everything else evict-first
+    const uint64_t pol_first = l2_evict_first(), pol_last = l2_evict_last();
+    const int keep_lo = nunits - S - reuse, keep_hi = nunits - S;
+    auto issue = [&](int u, int k, bool fwd) {
       int cA, cB;
       unit_cols(u, k, cA, cB);
       const uint32_t nbytes = (uint32_t)((((int64_t)(cB - cA) * NP + 1) & ~1LL) * 8);
-      bulk_load(ring + (size_t)(u % S) * slot_bytes, U + uo_s[k] + (int64_t)cA * NP, nbytes, &full[u % S]);
+      const bool keep = fwd && u >= keep_lo && u < keep_hi;
+      bulk_load(ring + (size_t)(u % S) * slot_bytes, U + uo_s[k] + (int64_t)cA * NP, nbytes, &full[u % S],
+                keep ? pol_last : pol_first);
     };
     int k = 1;
     for (int u = 0; u < nunits; ++u) {  // forward stream
@@ -604,7 +611,7 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
       if (u >= S) {  // wait for the forward release of unit u - S (event (u - S) / S of its slot)
         mbar_wait(&empty[u % S], (uint32_t)(((u - S) / S) & 1));
       }
-      issue(u, k);
+      issue(u, k, true);
     }
     int kv = m - 1, kw = m - 1;
     for (int v = nunits - 1; v >= S; --v) {  // backward refills: after releasing v, load v - S
@@ -616,7 +623,7 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
       const int w = v - S;
       while (us_s[kw] > w) --kw;
       (void)kv;
-      issue(w, kw);
+      issue(w, kw, false);
     }
     return;
   }
@@ -1009,7 +1016,7 @@ static void launch_local(dgas_ctx ctx, int mode, PcgState* st, const double* r, 
   const size_t smem = apply_smem_bytes(ctx);
   DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
                          mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
-                         st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows)));
+                         st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows, ctx->local_reuse)));
 }
 
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {

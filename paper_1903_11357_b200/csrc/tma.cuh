@@ -24,10 +24,19 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// evict last: operator data that is read again soon (the local solve's forward/backward turnaround)
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 // one bulk copy (size multiple of 16, both addresses 16-byte aligned); completion counted on bar
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first()) : "memory");
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  bulk_g2s(dst, src, bytes, bar, l2_evict_first());
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -41,13 +50,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 // load `bytes` (multiple of 16) possibly larger than the 1 MB bulk limit: chunks of 64 KB
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   mbar_expect_tx(bar, bytes);
   const uint32_t CH = 65536;
   for (uint32_t o = 0; o < bytes; o += CH) {
     uint32_t n = bytes - o < CH ? bytes - o : CH;
-    bulk_g2s((char*)dst + o, (const char*)src + o, n, bar);
+    bulk_g2s((char*)dst + o, (const char*)src + o, n, bar, pol);
   }
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  bulk_load(dst, src, bytes, bar, l2_evict_first());
 }
 
 // plain arrive (count 1) on an mbarrier
