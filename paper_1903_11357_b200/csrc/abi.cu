@@ -89,7 +89,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     {
       // L2 reuse across the forward/backward turnaround: the units just below each subdomain's ring-
       // resident tail are streamed evict-last (budget shared by all subdomains; vectors keep the rest)
-      double mb = 48;
+      double mb = 0;  // measured: no gain at 24-96 MB on cfg3/4/5 (tools/ab.sh), kept as a knob
       if (const char* e = std::getenv("DGAS_LOCAL_REUSE_MB")) mb = std::atof(e);
       ctx->local_reuse = (int)std::min<double>(1 << 20, mb * 1048576.0 / ((double)ctx->nsub * ctx->slot_bytes));
     }
@@ -98,21 +98,28 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int per_sm = 3;  // measured best on B200 (tools/ab.sh): 3 CTAs/SM, 2-cell batches, ~64 KB rings
+    // consumer groups: two independent 128-thread groups for n_p = 15 (cfg4: SpMV 0.220 -> 0.185 ms;
+    // 95 registers, so 2 CTAs/SM); one 256-thread group elsewhere (n_p = 10: 12 KB batches lose)
+    int ng = ctx->np == 15 ? 2 : 1;
+    if (const char* e = std::getenv("DGAS_SPMV_GROUPS")) ng = std::atoi(e) == 2 ? 2 : 1;
+    if (spmv_groups_ok(ctx->p) < ng) ng = 1;
+    if (ng == 2 && (int64_t)ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p, 2)) ng = 1;
+    ctx->spmv_groups = ng;
+    int per_sm = ng == 2 ? 2 : 3;  // measured best on B200 (tools/ab.sh): 3 CTAs/SM, 2-cell batches, ~64 KB rings
     if (const char* e = std::getenv("DGAS_SPMV_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
     ctx->spmv_grid = std::min(ctx->nc, per_sm * nsm);
     // SpMV ring: one slot per batch of G consecutive row-blocks of a CTA's cell range
     {
       // cells per batch: ~24 KB of row-blocks per bulk copy (per-batch consumer overhead dominates
       // below that, tools/ab.sh), at most the thread-limited maximum
-      int G = spmv_batch_cells(ctx->p);
+      int G = spmv_batch_cells(ctx->p, ng);
       if (!std::getenv("DGAS_SPMV_G")) {
         const double avg_row = (double)ctx->a_off_h[ctx->nc] * 8.0 / ctx->nc;
         G = std::max(1, std::min(G, (int)std::lround(24576.0 / avg_row)));
       }
-      while (G > 1 && (int64_t)G * ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p)) --G;
+      while (G > 1 && (int64_t)G * ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p, ng)) --G;
       ctx->spmv_G = G;
-      if ((int64_t)G * ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p)) { ctx->detail = "cell degree too large for the SpMV kernel"; return DGAS_E_INVALID_ARG; }
+      if ((int64_t)G * ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p, ng)) { ctx->detail = "cell degree too large for the SpMV kernel"; return DGAS_E_INVALID_ARG; }
       const int chunk = (ctx->nc + ctx->spmv_grid - 1) / ctx->spmv_grid;
       int64_t mx = 0;
       for (int c0 = 0; c0 < ctx->nc; c0 += chunk) {
@@ -295,7 +302,52 @@ static int build_graph_impl(dgas_ctx ctx, int maxit) {
   return 0;
 }
 
+// Profiling path (DGAS_EAGER=1): the same kernels launched from the host, 8 iterations between host
+// checks of the state (kernels return at once after convergence). ncu then sees every iteration kernel
+// as its own launch, which it does not inside the graph's conditional WHILE node.
+static int pcg_eager(dgas_ctx ctx, double rtol, int maxit, cudaStream_t s) {
+  if (maxit > ctx->hist_cap) {
+    if (ctx->d_alpha) cudaFree(ctx->d_alpha);
+    if (ctx->d_beta) cudaFree(ctx->d_beta);
+    int cap = std::max(maxit, 8192);
+    DGAS_CUDA(cudaMalloc((void**)&ctx->d_alpha, cap * sizeof(double)));
+    DGAS_CUDA(cudaMalloc((void**)&ctx->d_beta, cap * sizeof(double)));
+    ctx->hist_cap = cap;
+    if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
+    if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
+  }
+  PcgState* st = ctx->d_state;
+  launch_init_state(ctx, st, maxit, rtol, s);
+  ctx->side_sel = 0;
+  launch_spmv(ctx, 0, ctx->d_x, ctx->d_q, nullptr, s);
+  launch_restrict(ctx, 2, st, nullptr, s);
+  launch_apply(ctx, 1, st, nullptr, ctx->d_z, s);
+  launch_prolong(ctx, 1, st, nullptr, ctx->d_z, s, 0, 0);
+  for (;;) {
+    for (int u = 0; u < 8; ++u) {
+      launch_spmv(ctx, 1, nullptr, ctx->d_q, st, s);
+      launch_restrict(ctx, 1, st, nullptr, s);
+      launch_apply(ctx, 2, st, nullptr, ctx->d_z, s);
+      launch_prolong(ctx, 2, st, nullptr, ctx->d_z, s, 0, 0);
+    }
+    DGAS_CUDA(cudaMemcpyAsync(ctx->h_state, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    DGAS_CUDA(cudaStreamSynchronize(s));
+    if (ctx->h_state->done) break;
+  }
+  launch_lanczos(ctx, s);
+  DGAS_CUDA(cudaGetLastError());
+  return 0;
+}
+
 static int pcg_device(dgas_ctx ctx, double rtol, int maxit, int* iters, double* cond, cudaStream_t s) {
+  const bool eager = std::getenv("DGAS_EAGER") != nullptr;  // per call (tests switch it)
+  if (eager) {
+    int st = pcg_eager(ctx, rtol, maxit, s);
+    if (st) return st;
+    DGAS_CUDA(cudaMemcpyAsync(ctx->h_state, ctx->d_state, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    DGAS_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->d_lanczos, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    return 0;
+  }
   int st = build_graph(ctx, maxit);
   if (st) return st;
   launch_init_state(ctx, ctx->d_state, maxit, rtol, s);

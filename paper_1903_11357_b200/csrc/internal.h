@@ -66,6 +66,7 @@ struct dgas_ctx_s {
   int64_t N = 0, N0 = 0;
   double penalty = 10;
   int coarse_dense = 1, coarse_bw = 0, nT = 0, bt = 0;  // coarse tiles
+  int spmv_groups = 1;       // independent consumer groups in k_spmv3 (DGAS_SPMV_GROUPS)
   int restrict_cpj = 1;      // CTAs per coarse element in k_restrict (partials in d_rpart, counters d_jcnt)
   double* d_rpart = nullptr;
   unsigned* d_jcnt = nullptr;
@@ -259,8 +260,9 @@ void nd_free(dgas_ctx ctx);
 int apply_set_smem(dgas_ctx ctx, size_t smem);
 size_t apply_smem_bytes(dgas_ctx ctx);
 size_t spmv_smem_bytes(dgas_ctx ctx);
-int spmv_batch_cells(int p);
-int spmv_gather_cap(int p);
+int spmv_batch_cells(int p, int ng);
+int spmv_gather_cap(int p, int ng);
+int spmv_groups_ok(int p);
 int local_threads(int p);
 void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s);
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);

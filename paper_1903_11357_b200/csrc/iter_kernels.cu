@@ -160,20 +160,31 @@ struct SpmvCfg {
   static constexpr int E = NP >= 21 ? 3 : 2;              // gathered columns per thread per batch
   static constexpr int G = (SP_T / (NP * TR)) > 0 ? SP_T / (NP * TR) : 1;  // cells per batch
 };
+// NG independent consumer groups (SP_T / NG threads each, own named barrier, every NG-th batch): the
+// per-batch barrier then spans half the threads and no group waits for the other's cells
+template <int NP, int NG>
+struct SpmvGrp {
+  static constexpr int GT = SP_T / NG;
+  static constexpr int TR = SpmvCfg<NP>::TR;
+  static constexpr int E = NG == 1 ? SpmvCfg<NP>::E : SpmvCfg<NP>::E + 1;
+  static constexpr int G = (GT / (NP * TR)) > 0 ? GT / (NP * TR) : 1;
+  static constexpr bool ok = NP * TR <= GT;
+};
 
-template <int NP>
+template <int NP, int NG>
 __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk, const int* __restrict__ nbr_ptr,
                                                 const int* __restrict__ nbr, const int64_t* __restrict__ a_off,
                                                 const double* __restrict__ A, const double* x, double* y,
                                                 const double* z, double* const* pbuf, PcgState* st,
                                                 double* partials, double* alpha_hist, int S, uint32_t slot_bytes,
                                                 int maxW, int G) {
-  constexpr int GMAX = SpmvCfg<NP>::G, SPTR = SpmvCfg<NP>::TR, SP_MAXE = SpmvCfg<NP>::E;
+  constexpr int GMAX = SpmvGrp<NP, NG>::G, SPTR = SpmvGrp<NP, NG>::TR, SP_MAXE = SpmvGrp<NP, NG>::E;
+  constexpr int GT = SpmvGrp<NP, NG>::GT;  // threads of one consumer group
   extern __shared__ __align__(128) double sm[];
   constexpr int NTT = SP_T + 32;  // consumers + producer warp
   __shared__ double red[NTT / 32];
   __shared__ double wdot[NTT / 32];
-  __shared__ double own[2][GMAX * NP];
+  __shared__ double own_all[NG][2][GMAX * NP];
   int it = 0;
   double beta = 0;
   const double* pold = nullptr;
@@ -193,12 +204,12 @@ __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk
   int64_t* ao_s = reinterpret_cast<int64_t*>(bars + 32);                  // a_off[c0 .. c1]
   int* np_s = reinterpret_cast<int*>(ao_s + chunk + 2);                    // nbr_ptr[c0 .. c1]
   const int xstride = G * ((maxW + 1) & ~1);
-  double* xs = reinterpret_cast<double*>(np_s + ((chunk + 2 + 3) & ~3));   // [2][G][maxW]
+  double* xs_all = reinterpret_cast<double*>(np_s + ((chunk + 2 + 3) & ~3));   // [NG][2][G][maxW]
   unsigned char* ring = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(xs + 2 * xstride) + 127) & ~(uintptr_t)127);
+      (reinterpret_cast<uintptr_t>(xs_all + NG * 2 * xstride) + 127) & ~(uintptr_t)127);
   for (int k = threadIdx.x; k <= ncell; k += SP_T + 32) { np_s[k] = nbr_ptr[c0 + k]; ao_s[k] = a_off[c0 + k]; }
   if (threadIdx.x == 0) {
-    for (int t = 0; t < S; ++t) { mbar_init(&bars[t], 1); mbar_init(&empt[t], SP_T / 32); }
+    for (int t = 0; t < S; ++t) { mbar_init(&bars[t], 1); mbar_init(&empt[t], GT / 32); }
     fence_mbar_init();
   }
   __syncthreads();
@@ -213,7 +224,10 @@ __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk
       }
   }
   double mydot = 0;
-  if (threadIdx.x < SP_T) {  // ---------------- consumers
+  if (threadIdx.x < SP_T) {  // ---------------- consumers (group gid takes batches gid, gid + NG, ...)
+  const int gid = threadIdx.x / GT, tl = threadIdx.x % GT;
+  double* xs = xs_all + gid * 2 * xstride;
+  double (*own)[GMAX * NP] = own_all[gid];
   auto colval = [&](int64_t id) -> double {
     return mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
   };
@@ -225,7 +239,7 @@ __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk
     for (int t = 0; t < SP_MAXE; ++t) {
       idx[t] = -1;
       slot[t] = 0;
-      int e = threadIdx.x + SP_T * t;  // flat entry of the batch
+      int e = tl + GT * t;  // flat entry of the batch
       for (int k = k0; k < k1; ++k) {
         const int W = (np_s[k + 1] - np_s[k]) * NP;
         if (e < W) {
@@ -240,33 +254,31 @@ __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk
   int idxB[SP_MAXE], slotB[SP_MAXE], idxC[SP_MAXE], slotC[SP_MAXE];
   double vB[SP_MAXE], vC[SP_MAXE];
   auto publish = [&](int bi, const int* idx, const int* slot, const double* v) {  // values of batch bi -> xs
-    double* xn = xs + (bi & 1) * xstride;
+    double* xn = xs + ((bi / NG) & 1) * xstride;
     const int nk0 = bi * G;
     for (int t = 0; t < SP_MAXE; ++t)
       if (idx[t] >= 0) {
         xn[slot[t]] = v[t];
         const int gg = slot[t] / ((maxW + 1) & ~1);
-        if (idx[t] / NP == c0 + nk0 + gg) own[bi & 1][gg * NP + idx[t] % NP] = v[t];
+        if (idx[t] / NP == c0 + nk0 + gg) own[(bi / NG) & 1][gg * NP + idx[t] % NP] = v[t];
       }
   };
-  // prologue: batch 0 published, batch 1 values in registers (vB), batch 2 indices (idxC)
-  stage_idx(0, idxA, slotA);
+  // prologue: the group's batch 0 published, batch 1 values in registers (vB), batch 2 indices (idxC)
+  stage_idx(gid, idxA, slotA);
   for (int t = 0; t < SP_MAXE; ++t) vC[t] = idxA[t] >= 0 ? colval(idxA[t]) : 0.0;
-  publish(0, idxA, slotA, vC);
-  stage_idx(1, idxB, slotB);
+  publish(gid, idxA, slotA, vC);
+  stage_idx(gid + NG, idxB, slotB);
   for (int t = 0; t < SP_MAXE; ++t) vB[t] = idxB[t] >= 0 ? colval(idxB[t]) : 0.0;
-  stage_idx(2, idxC, slotC);
-  named_sync(1, SP_T);
-  const int g = threadIdx.x / (NP * SPTR), a = (threadIdx.x / SPTR) % NP, q = threadIdx.x % SPTR;
-  uint32_t ph = 0;
-  for (int bi = 0; bi < nb; ++bi) {
-    const int cur = bi & 1;
-    // values of batch bi+2 (in flight for two batch computes), indices of batch bi+3
+  stage_idx(gid + 2 * NG, idxC, slotC);
+  named_sync(1 + gid, GT);
+  const int g = tl / (NP * SPTR), a = (tl / SPTR) % NP, q = tl % SPTR;
+  for (int bi = gid; bi < nb; bi += NG) {
+    const int cur = (bi / NG) & 1;
+    // values of the group's next-but-one batch (in flight for two batch computes), indices of the one after
     for (int t = 0; t < SP_MAXE; ++t) vC[t] = idxC[t] >= 0 ? colval(idxC[t]) : 0.0;
-    stage_idx(bi + 3, idxA, slotA);
+    stage_idx(bi + 3 * NG, idxA, slotA);
     const int k0 = bi * G, kg = k0 + g;
-    mbar_wait(&bars[bi % S], (ph >> (bi % S)) & 1u);
-    ph ^= 1u << (bi % S);
+    mbar_wait(&bars[bi % S], (uint32_t)((bi / S) & 1));
     if (g < G && kg < ncell) {
       const int W = (np_s[kg + 1] - np_s[kg]) * NP;
       const double* Ak = reinterpret_cast<const double*>(ring + (size_t)(bi % S) * slot_bytes) + (ao_s[kg] - ao_s[k0]) + a;
@@ -297,12 +309,12 @@ __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empt[bi % S]);  // this warp is done with the ring slot of batch bi
-    publish(bi + 1, idxB, slotB, vB);  // xs[cur^1] is not read during batch bi
+    publish(bi + NG, idxB, slotB, vB);  // xs[cur^1] is not read during batch bi
     for (int t = 0; t < SP_MAXE; ++t) {
       idxB[t] = idxC[t]; slotB[t] = slotC[t]; vB[t] = vC[t];
       idxC[t] = idxA[t]; slotC[t] = slotA[t];
     }
-    named_sync(1, SP_T);  // batch bi+1 published
+    named_sync(1 + gid, GT);  // the group's next batch published
   }
   }  // consumers
   if (mode != 1) return;
@@ -874,40 +886,60 @@ void launch_perm(dgas_ctx ctx, const double* in, double* out, int to_internal, c
   k_perm<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ctx->nc, ctx->np, ctx->d_perm_dev, in, out, to_internal);
 }
 
-static int SpmvCfgMax(int p) {
+static int SpmvCfgMax(int p, int ng) {
   int G = 1;
-  DISPATCH_P(p, (G = SpmvCfg<NP_>::G));
+  if (ng == 2) {
+    DISPATCH_P(p, (G = SpmvGrp<NP_, 2>::G));
+  } else {
+    DISPATCH_P(p, (G = SpmvGrp<NP_, 1>::G));
+  }
   return G;
 }
 
-int spmv_gather_cap(int p) {
-  int e = 2;
-  DISPATCH_P(p, (e = SpmvCfg<NP_>::E));
-  return e * SP_T;
+int spmv_groups_ok(int p) {
+  bool ok = false;
+  DISPATCH_P(p, (ok = SpmvGrp<NP_, 2>::ok));
+  return ok ? 2 : 1;
 }
 
-int spmv_batch_cells(int p) {
-  int G = 1;
-  DISPATCH_P(p, (G = SpmvCfg<NP_>::G));
-  if (const char* e = std::getenv("DGAS_SPMV_G")) G = std::max(1, std::min(SpmvCfgMax(p), std::atoi(e)));
+int spmv_gather_cap(int p, int ng) {
+  int e = 2;
+  if (ng == 2) {
+    DISPATCH_P(p, (e = SpmvGrp<NP_, 2>::E));
+  } else {
+    DISPATCH_P(p, (e = SpmvGrp<NP_, 1>::E));
+  }
+  return e * (SP_T / ng);
+}
+
+int spmv_batch_cells(int p, int ng) {
+  int G = SpmvCfgMax(p, ng);
+  if (const char* e = std::getenv("DGAS_SPMV_G")) G = std::max(1, std::min(SpmvCfgMax(p, ng), std::atoi(e)));
   return G;
 }
 
 size_t spmv_smem_bytes(dgas_ctx ctx) {
   const int chunk = (ctx->nc + ctx->spmv_grid - 1) / std::max(1, ctx->spmv_grid);
   const int maxW = ctx->max_deg * ctx->np, G = ctx->spmv_G;
-  size_t b = 32 * 8 + (size_t)(chunk + 2) * 8 + (size_t)((chunk + 2 + 3) & ~3) * 4 + 2 * (size_t)G * ((maxW + 1) & ~1) * 8;
+  size_t b = 32 * 8 + (size_t)(chunk + 2) * 8 + (size_t)((chunk + 2 + 3) & ~3) * 4 +
+             (size_t)ctx->spmv_groups * 2 * (size_t)G * ((maxW + 1) & ~1) * 8;
   return ((b + 127) & ~(size_t)127) + (size_t)ctx->spmv_slots * ctx->spmv_slot_bytes + 128;
 }
 
 void launch_spmv(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s) {
   const int grid = ctx->spmv_grid, chunk = (ctx->nc + grid - 1) / grid;
   const size_t smem = spmv_smem_bytes(ctx);
-  DISPATCH_P(ctx->p, (k_spmv3<NP_><<<grid, SP_T + 32, smem, s>>>(mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr,
-                                                            ctx->d_a_off, ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st,
-                                                            ctx->d_partials, ctx->d_alpha, ctx->spmv_slots,
-                                                            ctx->spmv_slot_bytes, ctx->max_deg * ctx->np,
-                                                            ctx->spmv_G)));
+#define SPMV_LAUNCH(NG_)                                                                                       \
+  DISPATCH_P(ctx->p, (k_spmv3<NP_, NG_><<<grid, SP_T + 32, smem, s>>>(                                          \
+                         mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr, ctx->d_a_off, ctx->d_A, x, y, ctx->d_z, \
+                         ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha, ctx->spmv_slots, ctx->spmv_slot_bytes,   \
+                         ctx->max_deg * ctx->np, ctx->spmv_G)))
+  if (ctx->spmv_groups == 2) {
+    SPMV_LAUNCH(2);
+  } else {
+    SPMV_LAUNCH(1);
+  }
+#undef SPMV_LAUNCH
 }
 
 int spmv_set_smem(dgas_ctx ctx, size_t smem) {
@@ -916,13 +948,21 @@ int spmv_set_smem(dgas_ctx ctx, size_t smem) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if ((int)smem > mx) { ctx->detail = "SpMV kernel needs more shared memory than available"; return DGAS_E_INVALID_ARG; }
-  DISPATCH_P(ctx->p, ({
-    cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, k_spmv3<NP_>);
-    if (e == cudaSuccess && (size_t)mx < smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_spmv3<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
-  }));
+#define SPMV_ATTR(NG_)                                                                                        \
+  DISPATCH_P(ctx->p, ({                                                                                        \
+    cudaFuncAttributes fa;                                                                                     \
+    e = cudaFuncGetAttributes(&fa, k_spmv3<NP_, NG_>);                                                         \
+    if (e == cudaSuccess && (size_t)mx < smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;                 \
+    if (e == cudaSuccess)                                                                                      \
+      e = cudaFuncSetAttribute(k_spmv3<NP_, NG_>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
+                               mx - (int)fa.sharedSizeBytes);                                                  \
+  }))
+  if (ctx->spmv_groups == 2) {
+    SPMV_ATTR(2);
+  } else {
+    SPMV_ATTR(1);
+  }
+#undef SPMV_ATTR
   if (e != cudaSuccess) { ctx->detail = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
   return 0;
 }

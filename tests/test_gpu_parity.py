@@ -363,3 +363,18 @@ def test_precond_variants(name):
     with pytest.raises(Exception):
         S.set_precond(7)
     S.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2s", "cfg4s"])
+def test_eager_path_matches_graph(monkeypatch, name):
+    """The profiling path (DGAS_EAGER: host-launched iterations, what ncu sees kernel by kernel) computes
+    bit-for-bit the same solve as the CUDA-graph path."""
+    P = CASES[name]()
+    S = _solver(P)
+    b = _dev(g.normal(11, S.N))
+    x1, it1, c1, s1 = S.pcg(b, rtol=1e-8)
+    monkeypatch.setenv("DGAS_EAGER", "1")
+    x2, it2, c2, s2 = S.pcg(b, rtol=1e-8)
+    assert s1 == s2 == 0 and it1 == it2 and c1 == c2
+    assert torch.equal(x1, x2)
+    S.close()

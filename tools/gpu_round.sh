@@ -12,8 +12,10 @@ for c in ${BENCH_CONFIGS:-cfg4}; do
   timeout 900 python bench.py --config $c --steps 3 --warmup 3 ${BENCH_ARGS:---no-cpu-baseline} > gpurun_out/bench_$c.log 2>&1; echo "bench $c rc $?" >> $L
 done
 if [ -n "$NCU_CONFIG" ]; then
-  timeout 600 python bench.py --config $NCU_CONFIG --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_plain.log 2>&1 && \
-  timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_spmv3|k_restrict|k_local|k_coarse|k_prolong|k_nd_" -s ${NCU_SKIP:-40} -c ${NCU_COUNT:-40} --csv --log-file gpurun_out/launches_$NCU_CONFIG.csv python bench.py --config $NCU_CONFIG --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu.log 2>&1
+  # launch list of the same command; DGAS_EAGER=1 makes every PCG iteration kernel its own launch (ncu
+  # does not profile inside the graph's conditional WHILE node); window inside the first solve
+  DGAS_EAGER=1 timeout 600 python bench.py --config $NCU_CONFIG --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_plain.log 2>&1 && \
+  DGAS_EAGER=1 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s ${NCU_SKIP:-500} -c ${NCU_COUNT:-80} --csv --log-file gpurun_out/launches_$NCU_CONFIG.csv python bench.py --config $NCU_CONFIG --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu.log 2>&1
   echo "ncu launches rc $?" >> $L
 fi
 if [ -n "$NCU_FULL" ]; then
