@@ -98,9 +98,10 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    // consumer groups: two independent 128-thread groups for n_p = 15 (cfg4: SpMV 0.220 -> 0.185 ms;
-    // 95 registers, so 2 CTAs/SM); one 256-thread group elsewhere (n_p = 10: 12 KB batches lose)
-    int ng = ctx->np == 15 ? 2 : 1;
+    // consumer groups: two independent 128-thread groups for n_p >= 10 (95 registers, so 2 CTAs/SM;
+    // measured: cfg3 765 -> 812 it/s, cfg4 1444 -> 1530, cfg5 p5q5 1848 -> 2335, p6q6 1315 -> 1470);
+    // one 256-thread group below (no gain at n_p <= 6)
+    int ng = ctx->np >= 10 ? 2 : 1;
     if (const char* e = std::getenv("DGAS_SPMV_GROUPS")) ng = std::atoi(e) == 2 ? 2 : 1;
     if (spmv_groups_ok(ctx->p) < ng) ng = 1;
     if (ng == 2 && (int64_t)ctx->max_deg * ctx->np > spmv_gather_cap(ctx->p, 2)) ng = 1;

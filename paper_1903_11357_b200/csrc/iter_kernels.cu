@@ -165,8 +165,10 @@ struct SpmvCfg {
 template <int NP, int NG>
 struct SpmvGrp {
   static constexpr int GT = SP_T / NG;
-  static constexpr int TR = SpmvCfg<NP>::TR;
-  static constexpr int E = NG == 1 ? SpmvCfg<NP>::E : SpmvCfg<NP>::E + 1;
+  // two groups: 4 lanes per row from n_p = 15 up (n_p = 28: 112 threads per cell), 2 below (n_p = 10:
+  // 20 threads per cell, 6 cells = ~24 KB per batch)
+  static constexpr int TR = NG == 1 ? SpmvCfg<NP>::TR : (NP >= 15 ? 4 : 2);
+  static constexpr int E = NG == 1 ? SpmvCfg<NP>::E : 3;
   static constexpr int G = (GT / (NP * TR)) > 0 ? GT / (NP * TR) : 1;
   static constexpr bool ok = NP * TR <= GT;
 };
