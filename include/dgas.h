@@ -95,6 +95,9 @@ typedef struct {
   double coarse_solve_relerr;    /* measured ||z - v|| / ||v|| of one coarse solve of A0 z = A0 v (ND only) */
   int32_t unroll;                /* PCG iterations per execution of the graph's WHILE body; the last body of a
                                     solve launches its remaining copies as immediate-return kernels */
+  int32_t local_kernel;          /* 1: envelope kernel (all subdomains resident); 2: panel kernel (few CTAs
+                                    per SM so the factor is re-read from L2 by the backward sweep) */
+  int32_t local_ctas_per_sm;     /* resident local-solve CTAs per SM the panel kernel is sized for */
 } dgas_info_t;
 
 /* Build the SIPDG operator and the two-level Schwarz preconditioner on the GPU.

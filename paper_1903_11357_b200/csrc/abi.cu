@@ -1,10 +1,61 @@
 // abi.cu — the remaining C-ABI entry points (include/dgas.h): rhs, spmv, apply, pcg (device-resident
 // loop: one CUDA graph whose WHILE conditional node runs PCG iterations until the device-side
 // convergence test clears the condition), info, history, diagnostics.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
+
+// Local-solve kernel choice and the panel kernel's launch geometry (local_panel.cu). Shared memory
+// per CTA leaves room for one coarse-solve CTA per SM (the coarse chain runs concurrently on a side
+// stream).
+static int panel_configure(dgas_ctx ctx) {
+  const bool ok = panel_supported(ctx->p) && ctx->max_sub_cells > 1;
+  ctx->local_kernel = ok ? 2 : 1;
+  if (const char* e = std::getenv("DGAS_LOCAL_KERNEL")) {
+    const int v = std::atoi(e);
+    if (v == 1 || (v == 2 && ok)) ctx->local_kernel = v;
+  }
+  if (ctx->local_kernel != 2) return 0;
+  int dev = 0, nsm = 148, smem_sm = 233472, optin = 232448;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // CTAs per SM: the fewest that hold every subdomain in one wave, with 256 consumer threads per
+  // subdomain (short chain steps) up to 3 per SM; beyond that the kernel is HBM-bound and runs 7
+  // 128-thread CTAs per SM (measured on B200, tools/ab.sh: cfg4 local 0.361 -> 0.336 ms, cfg3
+  // 0.562 -> 0.462 ms against the envelope kernel; 1-3 CTAs/SM with L2 reuse of the backward sweep
+  // are latency-bound, 0.78-0.90 ms)
+  int cps = (ctx->nsub + nsm - 1) / nsm;
+  if (cps > 3) cps = 7;
+  ctx->panel_cps = cps;
+  size_t reserve = 8 * 1024;
+  if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;
+  size_t per_cta = ((size_t)smem_sm - std::min((size_t)smem_sm / 2, reserve)) / cps - 1024;
+  per_cta = std::min(per_cta, (size_t)optin);
+  const size_t base = panel_base_bytes(ctx->max_sub_cells, ctx->np) + 128;
+  size_t target = 12 * 1024;
+  if (const char* e = std::getenv("DGAS_PANEL_SLOT_KB")) target = (size_t)std::atoi(e) * 1024;
+  const int maxW = ctx->max_urow + ctx->np;
+  int CC = std::min((maxW + 1) / 2 * 2, std::max(2, (int)(target / (8 * ctx->np)) / 2 * 2));
+  ctx->panel_slots = 0;
+  for (; CC >= 2; CC -= 2) {
+    const uint32_t sb = (uint32_t)(((((int64_t)CC * ctx->np + 1) / 2 * 2) * 8 + 127) / 128 * 128);
+    if (per_cta <= base) break;
+    int S = (int)std::min<size_t>(64, (per_cta - base) / sb);
+    int S2 = 1;
+    while (S2 * 2 <= S) S2 *= 2;
+    if (S2 >= 2) { ctx->panel_slots = S2; ctx->panel_slot_bytes = sb; ctx->panel_cc = CC; break; }
+  }
+  if (ctx->panel_slots < 2) { ctx->local_kernel = 1; return 0; }  // subdomain too large: envelope kernel
+  ctx->panel_keep = 1;
+  if (const char* e = std::getenv("DGAS_PANEL_KEEP")) ctx->panel_keep = std::atoi(e) != 0;
+  int st = panel_setup(ctx, ctx->sub_ptr_h, ctx->first_h);
+  if (st) return st;
+  return panel_set_smem(ctx);
+}
 
 static int finish_setup_buffers(dgas_ctx ctx) {
   if (ctx->d_pbuf) return 0;
@@ -95,6 +146,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     }
     int st = apply_set_smem(ctx, apply_smem_bytes(ctx));
     if (st) return st;
+    if ((st = panel_configure(ctx))) return st;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -448,6 +500,8 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->coarse_mode = ctx->coarse_mode;
   info->coarse_refine = ctx->coarse_mode == 2 ? ctx->nd.refine : 0;
   info->unroll = ctx->unroll;
+  info->local_kernel = ctx->local_kernel;
+  info->local_ctas_per_sm = ctx->local_kernel == 2 ? ctx->panel_cps : 0;
   info->coarse_solve_relerr = ctx->coarse_mode == 2 ? ctx->nd.calib_err : 0.0;
   int coarse_launches = 1;
   if (ctx->coarse_mode == 2) {

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -173,7 +174,18 @@ struct dgas_ctx_s {
   uint32_t spmv_slot_bytes = 0;
   int spmv_grid = 0;
   int spmv_G = 1;
-  int restrict_wpj = 8;     // warps per coarse element in k_restrict           // cells per SpMV batch (<= compile-time maximum)
+  int restrict_wpj = 8;     // warps per coarse element in k_restrict
+  // local-solve kernel: 1 = k_local (envelope U + D, all subdomains resident), 2 = k_local_panel
+  // (merged panels [D_k | -U_k], few CTAs per SM for L2 reuse across the forward/backward turnaround)
+  int local_kernel = 1;
+  std::vector<int> first_h, sub_ptr_h;   // host copies: f_k (local index), subdomain cell ranges
+  double* d_P = nullptr;                 // panels [D_k | -U_k], column-major, 16-byte aligned
+  int64_t* d_p_off = nullptr;            // [nc+1] panel offsets (doubles)
+  int* d_pus = nullptr;                  // [nc] first stream unit of cell k within its subdomain
+  int* d_sub_units = nullptr;            // [nsub] stream units per subdomain
+  int64_t p_total = 0;
+  int panel_cc = 2, panel_slots = 2, panel_keep = 1, panel_cps = 1;
+  uint32_t panel_slot_bytes = 0;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -267,3 +279,24 @@ int local_threads(int p);
 void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s);
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);
 int spmv_set_smem(dgas_ctx ctx, size_t smem);
+int panel_supported(int p);
+size_t panel_base_bytes(int max_cells, int np);
+int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first);
+size_t panel_smem_bytes(dgas_ctx ctx);
+int panel_set_smem(dgas_ctx ctx);
+void launch_local_panel(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s);
+
+template <typename T>
+inline int dev_upload(dgas_ctx ctx, T** d, const std::vector<T>& h) {
+  size_t n = std::max<size_t>(h.size(), 1);
+  DGAS_CUDA(cudaMalloc((void**)d, n * sizeof(T)));
+  if (!h.empty()) DGAS_CUDA(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return 0;
+}
+template <typename T>
+inline int dev_alloc(dgas_ctx ctx, T** d, size_t n, bool zero = true) {
+  n = std::max<size_t>(n, 1);
+  DGAS_CUDA(cudaMalloc((void**)d, n * sizeof(T)));
+  if (zero) DGAS_CUDA(cudaMemsetAsync(*d, 0, n * sizeof(T), ctx->stream));
+  return 0;
+}

@@ -1055,6 +1055,10 @@ static void launch_local(dgas_ctx ctx, int mode, PcgState* st, const double* r, 
     DISPATCH_P(ctx->p, (k_bjacobi<NP_><<<grid, 256, 0, s>>>(mode, ctx->nc, ctx->d_Dinv, r, ctx->d_rbuf, z, st)));
     return;
   }
+  if (ctx->local_kernel == 2) {
+    launch_local_panel(ctx, mode, st, r, z, s);
+    return;
+  }
   const size_t smem = apply_smem_bytes(ctx);
   DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
                          mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,

@@ -1,0 +1,303 @@
+// local_panel.cu — the local solves z_i = A_i^-1 r_i of the additive Schwarz preconditioner
+// (exact solves with the subdomain blocks A_i), built for L2 reuse.
+//
+// Why a second local-solve kernel. A direct solve with A_i = L L^T reads every factor entry twice
+// (forward sweep, then backward sweep in reverse order). k_local runs every subdomain at once
+// (7 CTAs/SM on config 4) and so reads the factor twice from HBM: the 1024 concurrent factors
+// (0.93 GB) cannot stay in the 126 MB L2 across the turnaround. This kernel runs few subdomains per
+// SM (1-2 CTAs/SM) so that the part of each factor that is live between its forward and backward
+// use (on average half a factor per running CTA) fits in L2, and it makes each step of the
+// sweep chain short enough that this low concurrency still streams at HBM speed:
+//   * merged panels P_k = [D_k | -U_k] (column-major, NP rows; D_k = L_kk^-1, U_k = D_k L_{k,f_k..k-1}),
+//     so a forward step is ONE dot product y_k = P_k [r_k ; y_{f_k..k-1}] and a backward step is ONE
+//     transposed product v = P_k^T u_k whose first NP entries are z_k = D_k^T u_k and the rest the
+//     update y_{f_k..k-1} -= U_k^T u_k. No separate D^-1 prologue/epilogue sweeps.
+//   * per-cell tables (unit ranges, f_k, panel offsets) precomputed on the host; no integer division
+//     on the chain; power-of-two ring.
+//   * 256 consumer threads per subdomain (16 lanes per row in the forward step, 2 per column in the
+//     backward step); one producer warp streams CC-column units of the panels by cp.async.bulk into S
+//     ring slots. Forward loads are evict-last (they are read again by the backward sweep), the
+//     ring-resident tail and the backward loads are evict-first.
+// Derivation (block rows of A_i = L L^T, D_k = L_kk^-1, U_k = D_k L_{k,old}):
+//   forward  L y = r   : y_k = D_k r_k - U_k y_old
+//   backward L^T z = y : u_k = y_k - sum_{j>k} U_j[:,k]^T u_j,  z_k = D_k^T u_k
+#include "internal.h"
+#include "tma.cuh"
+
+template <int NP, bool NARROW = false>
+struct PanelCfg {
+  static constexpr int T = (NP > 4 && !NARROW) ? 256 : 128;       // consumer threads
+  static constexpr int ROWS = NP > 8 ? 16 : (NP > 4 ? 8 : 4);     // row slots in the forward step
+  static constexpr int LPR = T / ROWS;                            // lanes per row (16 or 32)
+  static constexpr int NW = T / 32;
+  static constexpr int H = (NP + 1) / 2;                          // rows per half in the backward step
+};
+
+// smem layout (must match panel_smem_bytes): full[64] | empty[64] | us[mc+1] | fk[mc] | po[mc] | R | Y | ring
+struct PanelLayout {
+  size_t off_us, off_fk, off_po, off_R, off_Y, off_ring;
+  __host__ __device__ PanelLayout(int mc, int np) {
+    off_us = 1024;
+    off_fk = off_us + (((size_t)(mc + 1) * 4 + 15) & ~(size_t)15);
+    off_po = off_fk + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_R = off_po + (size_t)mc * 8;
+    off_Y = off_R + (((size_t)mc * np * 8 + 15) & ~(size_t)15);
+    off_ring = (off_Y + (size_t)mc * np * 8 + 127) & ~(size_t)127;
+  }
+};
+
+// NARROW (7 CTAs/SM): at most 48 registers so a 256-thread coarse-solve CTA still fits beside them
+template <int NP, bool NARROW>
+__global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 1) k_local_panel(
+    int mode, const int* __restrict__ sub_ptr, const int* __restrict__ first, const int* __restrict__ pus,
+    const int* __restrict__ sub_units, const int64_t* __restrict__ p_off, const double* __restrict__ P,
+    const double* r_in, double* const* rbuf, double* z, const PcgState* st, int S, uint32_t slot_bytes, int CC,
+    int max_cells, int keep_fwd) {
+  using C = PanelCfg<NP, NARROW>;
+  constexpr int T = C::T, LPR = C::LPR, NW = C::NW, H = C::H;
+  extern __shared__ __align__(128) double sm[];
+  const double* r = r_in;
+  if (mode >= 1) {
+    if (st->done) return;
+    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+  }
+  const int s = blockIdx.x, s0 = sub_ptr[s], m = sub_ptr[s + 1] - s0;
+  const PanelLayout L(max_cells, NP);
+  unsigned char* smb = reinterpret_cast<unsigned char*>(sm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smb);
+  uint64_t* empty = full + 64;
+  int* us_s = reinterpret_cast<int*>(smb + L.off_us);
+  int* fk_s = reinterpret_cast<int*>(smb + L.off_fk);
+  int64_t* po_s = reinterpret_cast<int64_t*>(smb + L.off_po);
+  double* R = reinterpret_cast<double*>(smb + L.off_R);
+  double* Y = reinterpret_cast<double*>(smb + L.off_Y);
+  unsigned char* ring = smb + L.off_ring;
+  const int tid = threadIdx.x;
+  for (int k = tid; k < m; k += T + 32) {
+    us_s[k] = pus[s0 + k];
+    fk_s[k] = first[s0 + k];
+    po_s[k] = p_off[s0 + k];
+  }
+  if (tid == 0) {
+    us_s[m] = sub_units[s];
+    for (int t = 0; t < S; ++t) { mbar_init(&full[t], 1); mbar_init(&empty[t], NW); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int U = us_s[m], SM1 = S - 1;
+  if (tid >= T) {
+    // ---------------- producer warp (one lane issues every copy)
+    if (tid != T) return;
+    const uint64_t pol_first = l2_evict_first(), pol_last = keep_fwd ? l2_evict_last() : pol_first;
+    uint64_t epar = 0;  // parity of the next empty-barrier phase per slot
+    auto issue = [&](int u, int k, uint64_t pol) {
+      const int W = (k - fk_s[k] + 1) * NP;
+      const int cA = (u - us_s[k]) * CC, cB = min(W, cA + CC);
+      const uint32_t nbytes = (uint32_t)((((int64_t)(cB - cA) * NP + 1) & ~1LL) * 8);
+      bulk_load(ring + (size_t)(u & SM1) * slot_bytes, P + po_s[k] + (int64_t)cA * NP, nbytes, &full[u & SM1], pol);
+    };
+    int k = 0;
+    for (int u = 0; u < U; ++u) {  // forward stream: slot u & SM1 after the release of unit u - S
+      while (us_s[k + 1] <= u) ++k;
+      const int sl = u & SM1;
+      if (u >= S) { mbar_wait(&empty[sl], (uint32_t)((epar >> sl) & 1)); epar ^= 1ull << sl; }
+      issue(u, k, u < U - S ? pol_last : pol_first);
+    }
+    int kw = m - 1;
+    for (int v = U - 1; v >= S; --v) {  // backward refills: after the release of unit v, load unit v - S
+      const int sl = v & SM1;
+      mbar_wait(&empty[sl], (uint32_t)((epar >> sl) & 1));
+      epar ^= 1ull << sl;
+      const int w = v - S;
+      while (us_s[kw] > w) --kw;
+      issue(w, kw, pol_first);
+    }
+    return;
+  }
+  // ---------------- consumers
+  const int lane = tid & 31;
+  uint64_t fph = 0;  // parity of the next full-barrier phase per slot
+  const double* rs = r + (size_t)s0 * NP;
+  for (int e = tid; e < m * NP; e += T) R[e] = rs[e];
+  named_sync(1, T);
+  // forward: thread (a, q) accumulates row a of P_k over columns c = q (mod LPR)
+  {
+    const int a = tid / LPR, q = tid % LPR;
+    for (int k = 0; k < m; ++k) {
+      const int u0 = us_s[k], u1 = us_s[k + 1], fk = fk_s[k];
+      const int W = (k - fk + 1) * NP;
+      const double* rk = R + k * NP;
+      const double* yb = Y + (fk - 1) * NP;  // column c >= NP multiplies Y[(fk - 1) NP + c]
+      double v0 = 0, v1 = 0;
+      for (int u = u0; u < u1; ++u) {
+        const int sl = u & SM1;
+        mbar_wait(&full[sl], (uint32_t)((fph >> sl) & 1));
+        fph ^= 1ull << sl;
+        const int cA = (u - u0) * CC, cB = min(W, cA + CC);
+        const double* Pu = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes) + a;
+        if (a < NP) {
+          int c = cA + q;
+          for (; c + LPR < cB; c += 2 * LPR) {
+            const double x0 = c < NP ? rk[c] : yb[c];
+            const double x1 = c + LPR < NP ? rk[c + LPR] : yb[c + LPR];
+            v0 += Pu[(c - cA) * NP] * x0;
+            v1 += Pu[(c + LPR - cA) * NP] * x1;
+          }
+          if (c < cB) v0 += Pu[(c - cA) * NP] * (c < NP ? rk[c] : yb[c]);
+        }
+        __syncwarp();
+        // the ring-resident tail (u >= U - S) is released only once, by the backward sweep
+        if (lane == 0 && u < U - S) mbar_arrive(&empty[sl]);
+      }
+      double v = v0 + v1;
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (q == 0 && a < NP) Y[k * NP + a] = v;
+      named_sync(1, T);
+    }
+  }
+  // backward: u_k = Y_k is final; v = P_k^T u_k, thread pair (j, half) per column, rows split in halves
+  {
+    const int half = tid & 1, a0 = half * H;
+    double* zs = z + (size_t)s0 * NP;
+    for (int k = m - 1; k >= 0; --k) {
+      const int u0 = us_s[k], u1 = us_s[k + 1], fk = fk_s[k];
+      const int W = (k - fk + 1) * NP;
+      double uk[H];
+#pragma unroll
+      for (int i = 0; i < H; ++i) uk[i] = a0 + i < NP ? Y[k * NP + a0 + i] : 0.0;
+      double* yb = Y + (fk - 1) * NP;
+      for (int u = u1 - 1; u >= u0; --u) {
+        const int sl = u & SM1;
+        if (u < U - S) {
+          mbar_wait(&full[sl], (uint32_t)((fph >> sl) & 1));
+          fph ^= 1ull << sl;
+        }
+        const int cA = (u - u0) * CC, cB = min(W, cA + CC);
+        const double* Pu = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes) + a0;
+        // every lane of a warp runs the same trip count (warp-uniform bound), so the pair shuffle is
+        // a full-warp one; columns past cB contribute nothing
+        const int cw = cA + (tid >> 5) * 16;  // first column of this warp's 16-column group
+        for (int cb = cw; cb < cB; cb += T / 2) {
+          const int c = cb + (lane >> 1);
+          double w0 = 0, w1 = 0;
+          if (c < cB) {
+            const double* col = Pu + (c - cA) * NP;
+#pragma unroll
+            for (int i = 0; i + 1 < H; i += 2) {
+              if (a0 + i < NP) w0 += col[i] * uk[i];
+              if (a0 + i + 1 < NP) w1 += col[i + 1] * uk[i + 1];
+            }
+            if ((H & 1) && a0 + H - 1 < NP) w0 += col[H - 1] * uk[H - 1];
+          }
+          double w = w0 + w1;
+          w += __shfl_xor_sync(0xffffffffu, w, 1);
+          if (half == 0 && c < cB) {
+            if (c < NP) zs[k * NP + c] = w;
+            else yb[c] += w;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sl]);
+      }
+      named_sync(1, T);
+    }
+  }
+}
+
+// P_k = [D_k | -U_k], column-major NP x ((k - f_k + 1) NP) at p_off[c]; D_k from the row-major
+// lower triangle of Dinv (upper part written as zeros).
+__global__ void k_build_panels(int np, int nc, const int* sub_ptr_of_cell, const int* first,
+                               const int64_t* u_off, const double* U, const double* Dinv, const int64_t* p_off,
+                               double* P) {
+  const int c = blockIdx.x;
+  if (c >= nc) return;
+  const int k = c - sub_ptr_of_cell[c], W = (k - first[c] + 1) * np;
+  double* Pc = P + p_off[c];
+  const double* Uc = U + u_off[c];
+  const double* Dc = Dinv + (size_t)c * np * np;
+  for (int e = threadIdx.x; e < W * np; e += blockDim.x) {
+    const int col = e / np, a = e % np;
+    Pc[e] = col < np ? (col <= a ? Dc[a * np + col] : 0.0) : -Uc[(size_t)(col - np) * np + a];
+  }
+}
+
+#define DISPATCH_P15(P, ...)                                \
+  switch (P) {                                              \
+    case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
+    case 2: { constexpr int NP_ = 6; __VA_ARGS__; } break;  \
+    case 3: { constexpr int NP_ = 10; __VA_ARGS__; } break; \
+    case 4: { constexpr int NP_ = 15; __VA_ARGS__; } break; \
+  }
+
+int panel_supported(int p) { return p >= 1 && p <= 4; }
+
+// 128 consumer threads when more than 3 CTAs share an SM (registers), else 256
+static bool panel_narrow(dgas_ctx ctx) { return ctx->panel_cps > 3; }
+
+size_t panel_base_bytes(int max_cells, int np) { return PanelLayout(max_cells, np).off_ring; }
+
+// host: panel offsets, per-cell unit starts, per-subdomain unit counts; device: the panels
+int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first) {
+  const int nc = ctx->nc, np = ctx->np, CC = ctx->panel_cc;
+  std::vector<int64_t> p_off(nc + 1, 0);
+  std::vector<int> pus(nc), sub_units(ctx->nsub), sub_of(nc);
+  for (int s = 0; s < ctx->nsub; ++s) {
+    int acc = 0;
+    for (int c = sub_ptr[s]; c < sub_ptr[s + 1]; ++c) {
+      const int k = c - sub_ptr[s], W = (k - first[c] + 1) * np;
+      sub_of[c] = sub_ptr[s];
+      pus[c] = acc;
+      acc += (W + CC - 1) / CC;
+      p_off[c + 1] = p_off[c] + ((int64_t)np * W + 1) / 2 * 2;  // 16-byte panels for TMA
+    }
+    sub_units[s] = acc;
+  }
+  ctx->p_total = p_off[nc];
+  int st;
+  if ((st = dev_upload(ctx, &ctx->d_p_off, p_off))) return st;
+  if ((st = dev_upload(ctx, &ctx->d_pus, pus))) return st;
+  if ((st = dev_upload(ctx, &ctx->d_sub_units, sub_units))) return st;
+  int* d_sub_of = nullptr;
+  if ((st = dev_upload(ctx, &d_sub_of, sub_of))) return st;
+  if ((st = dev_alloc(ctx, &ctx->d_P, (size_t)p_off[nc] + 32))) { cudaFree(d_sub_of); return st; }
+  k_build_panels<<<nc, 128, 0, ctx->stream>>>(np, nc, d_sub_of, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv,
+                                              ctx->d_p_off, ctx->d_P);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d_sub_of);
+  if (e != cudaSuccess) { ctx->detail = std::string("panel build: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
+  return 0;
+}
+
+size_t panel_smem_bytes(dgas_ctx ctx) {
+  return PanelLayout(ctx->max_sub_cells, ctx->np).off_ring + (size_t)ctx->panel_slots * ctx->panel_slot_bytes + 128;
+}
+
+int panel_set_smem(dgas_ctx ctx) {
+  const size_t smem = panel_smem_bytes(ctx);
+  cudaError_t e = cudaSuccess;
+  if (panel_narrow(ctx)) {
+    DISPATCH_P15(ctx->p, (e = cudaFuncSetAttribute(k_local_panel<NP_, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)));
+  } else {
+    DISPATCH_P15(ctx->p, (e = cudaFuncSetAttribute(k_local_panel<NP_, false>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)));
+  }
+  if (e != cudaSuccess) { ctx->detail = std::string("panel smem: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
+  return 0;
+}
+
+void launch_local_panel(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
+  const size_t smem = panel_smem_bytes(ctx);
+#define PANEL_LAUNCH(NAR)                                                                                          \
+  DISPATCH_P15(ctx->p, (k_local_panel<NP_, NAR><<<ctx->nsub, PanelCfg<NP_, NAR>::T + 32, smem, s>>>(               \
+                           mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_pus, ctx->d_sub_units, ctx->d_p_off, ctx->d_P, \
+                           r, ctx->d_rbuf, z, st, ctx->panel_slots, ctx->panel_slot_bytes, ctx->panel_cc,         \
+                           ctx->max_sub_cells, ctx->panel_keep)))
+  if (panel_narrow(ctx)) {
+    PANEL_LAUNCH(true);
+  } else {
+    PANEL_LAUNCH(false);
+  }
+#undef PANEL_LAUNCH
+}

@@ -13,21 +13,6 @@
 
 namespace {
 
-template <typename T>
-int dev_upload(dgas_ctx ctx, T** d, const std::vector<T>& h) {
-  size_t n = std::max<size_t>(h.size(), 1);
-  DGAS_CUDA(cudaMalloc((void**)d, n * sizeof(T)));
-  if (!h.empty()) DGAS_CUDA(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
-  return 0;
-}
-template <typename T>
-int dev_alloc(dgas_ctx ctx, T** d, size_t n, bool zero = true) {
-  n = std::max<size_t>(n, 1);
-  DGAS_CUDA(cudaMalloc((void**)d, n * sizeof(T)));
-  if (zero) DGAS_CUDA(cudaMemsetAsync(*d, 0, n * sizeof(T), ctx->stream));
-  return 0;
-}
-
 double shoelace(const double* xy, int n) {
   double a = 0;
   for (int i = 0; i < n; ++i) {
@@ -238,6 +223,8 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
       ctx->max_urow = std::max(ctx->max_urow, w);
     }
   ctx->u_total = u_off[nc];
+  ctx->first_h = first;
+  ctx->sub_ptr_h = sub_ptr;
   // ------------------------------------------------ coarse pieces
   std::vector<int> ov_cell, ov_coarse, ov_pptr(1, 0);
   std::vector<double> ov_xy;
@@ -465,7 +452,8 @@ static void free_ctx(dgas_ctx ctx) {
                   ctx->d_contrib_ptr, ctx->d_contrib, ctx->d_x, ctx->d_r, ctx->d_z, ctx->d_q, ctx->d_b,
                   ctx->d_p[0], ctx->d_p[1], ctx->d_r0, ctx->d_z0, ctx->d_t1, ctx->d_t2, ctx->d_partials,
                   ctx->d_state, ctx->d_astate, ctx->d_alpha, ctx->d_beta, ctx->d_lanczos, ctx->d_err,
-                  ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev, ctx->d_rpart, ctx->d_jcnt};
+                  ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev, ctx->d_rpart, ctx->d_jcnt,
+                  ctx->d_P, ctx->d_p_off, ctx->d_pus, ctx->d_sub_units};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->d_A0b) cudaFree(ctx->d_A0b);

@@ -45,7 +45,8 @@ class Info(ctypes.Structure):
                 ("last_cond", ctypes.c_double), ("last_lmin", ctypes.c_double), ("last_lmax", ctypes.c_double),
                 ("last_relres", ctypes.c_double), ("coarse_mode", ctypes.c_int32), ("launches_per_iter", ctypes.c_int32),
                 ("launches_per_solve", ctypes.c_int32), ("coarse_refine", ctypes.c_int32),
-                ("coarse_solve_relerr", ctypes.c_double), ("unroll", ctypes.c_int32)]
+                ("coarse_solve_relerr", ctypes.c_double), ("unroll", ctypes.c_int32),
+                ("local_kernel", ctypes.c_int32), ("local_ctas_per_sm", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -378,3 +378,36 @@ def test_eager_path_matches_graph(monkeypatch, name):
     assert s1 == s2 == 0 and it1 == it2 and c1 == c2
     assert torch.equal(x1, x2)
     S.close()
+
+
+# --------------------------------------------------------------------------- local-solve kernels
+@pytest.mark.parametrize("name,env,kernel", [
+    ("cfg2s", {"DGAS_LOCAL_KERNEL": "1"}, 1),
+    ("cfg4s", {"DGAS_LOCAL_KERNEL": "1"}, 1),
+    ("cfg1", {}, 2),
+    ("cfg5s_p3q1", {}, 2),
+    # tiny ring: every panel spans several units, many backward refills (producer protocol)
+    ("cfg4s", {"DGAS_LOCAL_CPS": "8", "DGAS_PANEL_SLOT_KB": "1"}, 2),
+    ("cfg3s", {"DGAS_PANEL_KEEP": "0", "DGAS_LOCAL_CPS": "3"}, 2),
+    ("cfg5s_p6q1", {}, 1),  # n_p = 28: panels not supported, envelope kernel
+])
+def test_local_kernel_variants(monkeypatch, name, env, kernel):
+    """Both local-solve kernels (envelope k_local, panel k_local_panel) and the panel kernel's ring
+    geometries give the oracle's preconditioner apply within 1e-10 (north_star tolerance)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = CASES[name]()
+    S = _solver(P)
+    assert S.info["local_kernel"] == kernel
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    for seed in range(3):
+        r = g.normal(300 + seed, S.N)
+        z = S.apply(_dev(r)).cpu().numpy()
+        zr = o.apply(r)
+        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr), seed
+    b = o.rhs()
+    ref = o.pcg(b, rtol=1e-8)
+    x, iters, cond, st = S.pcg(_dev(b))
+    assert st == 0 and abs(iters - ref["iters"]) <= 2
+    S.close()
