@@ -39,9 +39,10 @@ static int panel_configure(dgas_ctx ctx) {
   size_t target = 12 * 1024;
   if (const char* e = std::getenv("DGAS_PANEL_SLOT_KB")) target = (size_t)std::atoi(e) * 1024;
   const int maxW = ctx->max_urow + ctx->np;
-  int CC = std::min((maxW + 1) / 2 * 2, std::max(2, (int)(target / (8 * ctx->np)) / 2 * 2));
+  const int cc_min = panel_min_cc(ctx->np);
+  int CC = std::max(cc_min, std::min((maxW + 1) / 2 * 2, std::max(2, (int)(target / (8 * ctx->np)) / 2 * 2)));
   ctx->panel_slots = 0;
-  for (; CC >= 2; CC -= 2) {
+  for (; CC >= cc_min; CC -= 2) {
     const uint32_t sb = (uint32_t)(((((int64_t)CC * ctx->np + 1) / 2 * 2) * 8 + 127) / 128 * 128);
     if (per_cta <= base) break;
     int S = (int)std::min<size_t>(64, (per_cta - base) / sb);

@@ -280,6 +280,7 @@ void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s)
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);
 int spmv_set_smem(dgas_ctx ctx, size_t smem);
 int panel_supported(int p);
+int panel_min_cc(int np);
 size_t panel_base_bytes(int max_cells, int np);
 int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first);
 size_t panel_smem_bytes(dgas_ctx ctx);

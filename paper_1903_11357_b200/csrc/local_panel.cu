@@ -33,6 +33,16 @@ struct PanelCfg {
   static constexpr int H = (NP + 1) / 2;                          // rows per half in the backward step
 };
 
+// Panel layout of cell k (doubles, 16-byte aligned): D_k lower triangle packed column by column
+// (column c holds rows c..NP-1 at dcol(c), padded to DPK, even), then the WU = (k - f_k) NP columns
+// of -U_k (column j at DPK + j NP). Stream units: unit 0 = D part + U columns [0, CC0), unit t >= 1
+// = U columns [CC0 + (t-1) CC, ...), CC and CC0 = CC - E even so every unit starts 16-byte aligned
+// and fits a CC-column slot.
+__host__ __device__ constexpr int panel_dpk(int np) { return (np * (np + 1) / 2 + 1) & ~1; }
+__host__ __device__ constexpr int panel_e(int np) { return (((panel_dpk(np) + np - 1) / np) + 1) & ~1; }
+__host__ __device__ constexpr int panel_dcol(int np, int c) { return c * np - c * (c - 1) / 2; }
+__host__ __device__ inline int panel_units(int wu, int cc, int cc0) { return 1 + (wu > cc0 ? (wu - cc0 + cc - 1) / cc : 0); }
+
 // smem layout (must match panel_smem_bytes): full[64] | empty[64] | us[mc+1] | fk[mc] | po[mc] | R | Y | ring
 struct PanelLayout {
   size_t off_us, off_fk, off_po, off_R, off_Y, off_ring;
@@ -48,7 +58,7 @@ struct PanelLayout {
 
 // NARROW (7 CTAs/SM): at most 48 registers so a 256-thread coarse-solve CTA still fits beside them
 template <int NP, bool NARROW>
-__global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 1) k_local_panel(
+__global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) k_local_panel(
     int mode, const int* __restrict__ sub_ptr, const int* __restrict__ first, const int* __restrict__ pus,
     const int* __restrict__ sub_units, const int64_t* __restrict__ p_off, const double* __restrict__ P,
     const double* r_in, double* const* rbuf, double* z, const PcgState* st, int S, uint32_t slot_bytes, int CC,
@@ -90,11 +100,15 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 1) 
     if (tid != T) return;
     const uint64_t pol_first = l2_evict_first(), pol_last = keep_fwd ? l2_evict_last() : pol_first;
     uint64_t epar = 0;  // parity of the next empty-barrier phase per slot
+    constexpr int DPK = panel_dpk(NP);
+    const int CC0 = CC - panel_e(NP);
     auto issue = [&](int u, int k, uint64_t pol) {
-      const int W = (k - fk_s[k] + 1) * NP;
-      const int cA = (u - us_s[k]) * CC, cB = min(W, cA + CC);
-      const uint32_t nbytes = (uint32_t)((((int64_t)(cB - cA) * NP + 1) & ~1LL) * 8);
-      bulk_load(ring + (size_t)(u & SM1) * slot_bytes, P + po_s[k] + (int64_t)cA * NP, nbytes, &full[u & SM1], pol);
+      const int WU = (k - fk_s[k]) * NP, t = u - us_s[k];
+      int64_t off, n;
+      if (t == 0) { off = 0; n = DPK + (int64_t)min(WU, CC0) * NP; }
+      else { const int j0 = CC0 + (t - 1) * CC; off = DPK + (int64_t)j0 * NP; n = (int64_t)(min(WU, j0 + CC) - j0) * NP; }
+      const uint32_t nbytes = (uint32_t)(((n + 1) & ~1LL) * 8);
+      bulk_load(ring + (size_t)(u & SM1) * slot_bytes, P + po_s[k] + off, nbytes, &full[u & SM1], pol);
     };
     int k = 0;
     for (int u = 0; u < U; ++u) {  // forward stream: slot u & SM1 after the release of unit u - S
@@ -115,6 +129,8 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 1) 
     return;
   }
   // ---------------- consumers
+  constexpr int DPK = panel_dpk(NP);
+  const int CC0 = CC - panel_e(NP);
   const int lane = tid & 31;
   uint64_t fph = 0;  // parity of the next full-barrier phase per slot
   const double* rs = r + (size_t)s0 * NP;
@@ -125,25 +141,31 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 1) 
     const int a = tid / LPR, q = tid % LPR;
     for (int k = 0; k < m; ++k) {
       const int u0 = us_s[k], u1 = us_s[k + 1], fk = fk_s[k];
-      const int W = (k - fk + 1) * NP;
+      const int WU = (k - fk) * NP;
       const double* rk = R + k * NP;
-      const double* yb = Y + (fk - 1) * NP;  // column c >= NP multiplies Y[(fk - 1) NP + c]
+      const double* yb = Y + fk * NP;  // U column j multiplies Y[f_k NP + j]
       double v0 = 0, v1 = 0;
       for (int u = u0; u < u1; ++u) {
-        const int sl = u & SM1;
+        const int sl = u & SM1, t = u - u0;
         mbar_wait(&full[sl], (uint32_t)((fph >> sl) & 1));
         fph ^= 1ull << sl;
-        const int cA = (u - u0) * CC, cB = min(W, cA + CC);
-        const double* Pu = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes) + a;
+        const double* Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
         if (a < NP) {
-          int c = cA + q;
-          for (; c + LPR < cB; c += 2 * LPR) {
-            const double x0 = c < NP ? rk[c] : yb[c];
-            const double x1 = c + LPR < NP ? rk[c + LPR] : yb[c + LPR];
-            v0 += Pu[(c - cA) * NP] * x0;
-            v1 += Pu[(c + LPR - cA) * NP] * x1;
+          int j0, j1;
+          const double* Pu;  // U column j at Pu[j NP]
+          if (t == 0) {
+            for (int c = q; c < NP; c += LPR)  // D_k r_k, lower triangle
+              if (c <= a) v1 += Ps[panel_dcol(NP, c) + a - c] * rk[c];
+            j0 = 0; j1 = min(WU, CC0); Pu = Ps + DPK + a;
+          } else {
+            j0 = CC0 + (t - 1) * CC; j1 = min(WU, j0 + CC); Pu = Ps - j0 * NP + a;
           }
-          if (c < cB) v0 += Pu[(c - cA) * NP] * (c < NP ? rk[c] : yb[c]);
+          int j = j0 + q;
+          for (; j + LPR < j1; j += 2 * LPR) {
+            v0 += Pu[j * NP] * yb[j];
+            v1 += Pu[(j + LPR) * NP] * yb[j + LPR];
+          }
+          if (j < j1) v0 += Pu[j * NP] * yb[j];
         }
         __syncwarp();
         // the ring-resident tail (u >= U - S) is released only once, by the backward sweep
@@ -162,39 +184,53 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 1) 
     double* zs = z + (size_t)s0 * NP;
     for (int k = m - 1; k >= 0; --k) {
       const int u0 = us_s[k], u1 = us_s[k + 1], fk = fk_s[k];
-      const int W = (k - fk + 1) * NP;
-      double uk[H];
+      const int WU = (k - fk) * NP;
+      // u_k rows of this thread's half: registers (wide CTAs) or read from shared memory per use
+      // (narrow CTAs, whose 48-register cap would otherwise spill)
+      double ukr[NARROW ? 1 : H];
+      if constexpr (!NARROW) {
 #pragma unroll
-      for (int i = 0; i < H; ++i) uk[i] = a0 + i < NP ? Y[k * NP + a0 + i] : 0.0;
-      double* yb = Y + (fk - 1) * NP;
+        for (int i = 0; i < H; ++i) ukr[i] = a0 + i < NP ? Y[k * NP + a0 + i] : 0.0;
+      }
+      const double* uks = Y + k * NP + a0;
+      auto uk = [&](int i) -> double {
+        if constexpr (NARROW) return uks[i];
+        else return ukr[i];
+      };
+      double* yb = Y + fk * NP;
       for (int u = u1 - 1; u >= u0; --u) {
-        const int sl = u & SM1;
+        const int sl = u & SM1, t = u - u0;
         if (u < U - S) {
           mbar_wait(&full[sl], (uint32_t)((fph >> sl) & 1));
           fph ^= 1ull << sl;
         }
-        const int cA = (u - u0) * CC, cB = min(W, cA + CC);
-        const double* Pu = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes) + a0;
+        const double* Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+        // virtual columns x of this unit: unit 0 has the NP columns of D_k first (z_k = D_k^T u_k)
+        const int xoff = t == 0 ? NP : 0;
+        const int j0 = t == 0 ? 0 : CC0 + (t - 1) * CC, j1 = t == 0 ? min(WU, CC0) : min(WU, j0 + CC);
+        const double* Pu = t == 0 ? Ps + DPK : Ps - j0 * NP;  // U column j at Pu[j NP]
+        const int nx = xoff + j1 - j0;
         // every lane of a warp runs the same trip count (warp-uniform bound), so the pair shuffle is
-        // a full-warp one; columns past cB contribute nothing
-        const int cw = cA + (tid >> 5) * 16;  // first column of this warp's 16-column group
-        for (int cb = cw; cb < cB; cb += T / 2) {
-          const int c = cb + (lane >> 1);
+        // a full-warp one
+        for (int xb = (tid >> 5) * 16; xb < nx; xb += T / 2) {
+          const int x = xb + (lane >> 1), j = j0 + x - xoff;
+          // D column x holds rows x..NP-1 (D_k[a][x] at col[a]); U column j holds all rows. One
+          // branch-free path for both (no divergence between the D and U lanes of warp 0)
+          const bool isd = x < xoff;
+          const double* col = isd ? Ps + panel_dcol(NP, x) - x : Pu + j * NP;
+          const int lo = isd ? x : 0, hi = x < nx ? NP : 0;
           double w0 = 0, w1 = 0;
-          if (c < cB) {
-            const double* col = Pu + (c - cA) * NP;
 #pragma unroll
-            for (int i = 0; i + 1 < H; i += 2) {
-              if (a0 + i < NP) w0 += col[i] * uk[i];
-              if (a0 + i + 1 < NP) w1 += col[i + 1] * uk[i + 1];
-            }
-            if ((H & 1) && a0 + H - 1 < NP) w0 += col[H - 1] * uk[H - 1];
+          for (int i = 0; i + 1 < H; i += 2) {
+            if (a0 + i < hi && a0 + i >= lo) w0 += col[a0 + i] * uk(i);
+            if (a0 + i + 1 < hi && a0 + i + 1 >= lo) w1 += col[a0 + i + 1] * uk(i + 1);
           }
+          if ((H & 1) && a0 + H - 1 < hi && a0 + H - 1 >= lo) w0 += col[a0 + H - 1] * uk(H - 1);
           double w = w0 + w1;
           w += __shfl_xor_sync(0xffffffffu, w, 1);
-          if (half == 0 && c < cB) {
-            if (c < NP) zs[k * NP + c] = w;
-            else yb[c] += w;
+          if (half == 0 && x < nx) {
+            if (x < xoff) zs[k * NP + x] = w;
+            else yb[j] += w;
           }
         }
         __syncwarp();
@@ -205,21 +241,23 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 1) 
   }
 }
 
-// P_k = [D_k | -U_k], column-major NP x ((k - f_k + 1) NP) at p_off[c]; D_k from the row-major
-// lower triangle of Dinv (upper part written as zeros).
+// P_k = [D_k packed lower triangle | -U_k] at p_off[c] (layout above), D_k from the row-major
+// lower triangle of Dinv.
 __global__ void k_build_panels(int np, int nc, const int* sub_ptr_of_cell, const int* first,
                                const int64_t* u_off, const double* U, const double* Dinv, const int64_t* p_off,
                                double* P) {
   const int c = blockIdx.x;
   if (c >= nc) return;
-  const int k = c - sub_ptr_of_cell[c], W = (k - first[c] + 1) * np;
+  const int k = c - sub_ptr_of_cell[c], WU = (k - first[c]) * np, dpk = panel_dpk(np);
   double* Pc = P + p_off[c];
   const double* Uc = U + u_off[c];
   const double* Dc = Dinv + (size_t)c * np * np;
-  for (int e = threadIdx.x; e < W * np; e += blockDim.x) {
-    const int col = e / np, a = e % np;
-    Pc[e] = col < np ? (col <= a ? Dc[a * np + col] : 0.0) : -Uc[(size_t)(col - np) * np + a];
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int a = e / np, cc = e % np;
+    if (cc <= a) Pc[panel_dcol(np, cc) + a - cc] = Dc[a * np + cc];
   }
+  if (threadIdx.x == 0 && dpk > np * (np + 1) / 2) Pc[dpk - 1] = 0.0;
+  for (int e = threadIdx.x; e < WU * np; e += blockDim.x) Pc[dpk + e] = -Uc[e];
 }
 
 #define DISPATCH_P15(P, ...)                                \
@@ -232,6 +270,8 @@ __global__ void k_build_panels(int np, int nc, const int* sub_ptr_of_cell, const
 
 int panel_supported(int p) { return p >= 1 && p <= 4; }
 
+int panel_min_cc(int np) { return panel_e(np) + 2; }
+
 // 128 consumer threads when more than 3 CTAs share an SM (registers), else 256
 static bool panel_narrow(dgas_ctx ctx) { return ctx->panel_cps > 3; }
 
@@ -239,17 +279,17 @@ size_t panel_base_bytes(int max_cells, int np) { return PanelLayout(max_cells, n
 
 // host: panel offsets, per-cell unit starts, per-subdomain unit counts; device: the panels
 int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first) {
-  const int nc = ctx->nc, np = ctx->np, CC = ctx->panel_cc;
+  const int nc = ctx->nc, np = ctx->np, CC = ctx->panel_cc, CC0 = CC - panel_e(np), dpk = panel_dpk(np);
   std::vector<int64_t> p_off(nc + 1, 0);
   std::vector<int> pus(nc), sub_units(ctx->nsub), sub_of(nc);
   for (int s = 0; s < ctx->nsub; ++s) {
     int acc = 0;
     for (int c = sub_ptr[s]; c < sub_ptr[s + 1]; ++c) {
-      const int k = c - sub_ptr[s], W = (k - first[c] + 1) * np;
+      const int k = c - sub_ptr[s], WU = (k - first[c]) * np;
       sub_of[c] = sub_ptr[s];
       pus[c] = acc;
-      acc += (W + CC - 1) / CC;
-      p_off[c + 1] = p_off[c] + ((int64_t)np * W + 1) / 2 * 2;  // 16-byte panels for TMA
+      acc += panel_units(WU, CC, CC0);
+      p_off[c + 1] = p_off[c] + (dpk + (int64_t)np * WU + 1) / 2 * 2;  // 16-byte panels for TMA
     }
     sub_units[s] = acc;
   }
