@@ -187,6 +187,16 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     }
     st = spmv_set_smem(ctx, spmv_smem_bytes(ctx));
     if (st) return st;
+    // byte-ring SpMV (spmv_ring.cu) unless DGAS_SPMV_KERNEL=3 or the mesh exceeds its degree limit
+    ctx->spmv_kernel = 3;
+    {
+      const char* e = std::getenv("DGAS_SPMV_KERNEL");
+      if (!(e && std::atoi(e) == 3)) {
+        const int rc = spmv_ring_configure(ctx, nsm);
+        if (rc < 0) return DGAS_E_CUDA;
+        if (rc == 0) ctx->spmv_kernel = 4;
+      }
+    }
   }
   DGAS_CUDA(cudaStreamSynchronize(ctx->stream));
   return 0;

@@ -185,6 +185,10 @@ struct dgas_ctx_s {
   int* d_sub_units = nullptr;            // [nsub] stream units per subdomain
   int64_t p_total = 0;
   int panel_cc = 2, panel_slots = 2, panel_keep = 1, panel_cps = 1;
+  // SpMV kernel: 3 = k_spmv3 (fixed slots, consumer groups), 4 = k_spmv_ring (byte ring, warp per cell)
+  int spmv_kernel = 3;
+  uint32_t sr_ring_bytes = 0;
+  int sr_grid = 0, sr_G = 1;  // persistent CTAs; cells per bulk copy
   uint32_t panel_slot_bytes = 0;
 };
 
@@ -279,6 +283,9 @@ int local_threads(int p);
 void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s);
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);
 int spmv_set_smem(dgas_ctx ctx, size_t smem);
+int spmv_ring_configure(dgas_ctx ctx, int nsm);
+size_t spmv_ring_smem(dgas_ctx ctx);
+void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s);
 int panel_supported(int p);
 int panel_min_cc(int np);
 size_t panel_base_bytes(int max_cells, int np);

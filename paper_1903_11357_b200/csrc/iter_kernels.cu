@@ -929,6 +929,10 @@ size_t spmv_smem_bytes(dgas_ctx ctx) {
 }
 
 void launch_spmv(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s) {
+  if (ctx->spmv_kernel == 4) {
+    launch_spmv_ring(ctx, mode, x, y, st, s);
+    return;
+  }
   const int grid = ctx->spmv_grid, chunk = (ctx->nc + grid - 1) / grid;
   const size_t smem = spmv_smem_bytes(ctx);
 #define SPMV_LAUNCH(NG_)                                                                                       \

@@ -313,16 +313,23 @@ size_t panel_smem_bytes(dgas_ctx ctx) {
   return PanelLayout(ctx->max_sub_cells, ctx->np).off_ring + (size_t)ctx->panel_slots * ctx->panel_slot_bytes + 128;
 }
 
+// The attribute is per function (shared by every context in the process): always raise it to the
+// opt-in maximum, never to this context's size (a later, smaller context would otherwise break the
+// launches of an earlier one).
 int panel_set_smem(dgas_ctx ctx) {
   const size_t smem = panel_smem_bytes(ctx);
+  int dev = 0, mx = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaError_t e = cudaSuccess;
-  if (panel_narrow(ctx)) {
-    DISPATCH_P15(ctx->p, (e = cudaFuncSetAttribute(k_local_panel<NP_, true>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)));
-  } else {
-    DISPATCH_P15(ctx->p, (e = cudaFuncSetAttribute(k_local_panel<NP_, false>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)));
-  }
+  auto raise = [&](const void* f) {
+    cudaFuncAttributes fa;
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f);
+    if (e == cudaSuccess && (size_t)mx < smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
+  };
+  DISPATCH_P15(ctx->p, (raise((const void*)k_local_panel<NP_, true>), raise((const void*)k_local_panel<NP_, false>)));
   if (e != cudaSuccess) { ctx->detail = std::string("panel smem: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
   return 0;
 }

@@ -1,0 +1,293 @@
+// spmv_ring.cu — q = A p for the block-sparse SIPDG matrix (eq:Ah), fused with the
+// PCG direction update p = z + beta p_old and the dot product p.q (ASPCG).
+//
+// Design (HBM-bound GEMV-class work, 2 flops per 8-byte entry): each persistent CTA owns a
+// contiguous range of cell rows. A producer lane streams the cells' column-major row-blocks
+// (n_p x deg n_p, contiguous, 16-byte padded) with one cp.async.bulk per cell into a BYTE ring:
+// blocks are packed back to back (a block never straddles the ring end), so the ring holds as many
+// blocks as fit, not a fixed number of worst-case slots, and ~100 KB per CTA stay in flight.
+// Consumer warps take the CTA's cells round-robin (cell i -> warp i mod NW) and work independently:
+// no CTA or group barrier per batch, only a per-cell mbarrier (full: bytes landed; empty: the
+// warp is done, the producer may reuse the bytes). Each warp gathers the neighbour values of its
+// NEXT cell (index load one cell further ahead) while it multiplies the current one; lane
+// (a, h) = (row, column slice) reads A[col n_p + a] (consecutive lanes -> consecutive words).
+#include "internal.h"
+#include "tma.cuh"
+
+#define SR_NW 8    // consumer warps per CTA
+#define SR_NB 32   // cells in flight per CTA (mbarrier pairs)
+
+template <int NP>
+struct SrCfg {
+  static constexpr int LPR = 32 / NP > 0 ? 32 / NP : 1;   // lanes per row (column slices)
+  static constexpr int LANES = NP * LPR <= 32 ? NP * LPR : 32;
+  static constexpr int ROWS_PER_PASS = NP <= 32 ? NP : 32;
+  static constexpr int E = (16 * NP + 31) / 32;           // gathered entries per lane (deg <= 16)
+  static constexpr int XS = 32 * E;                        // gathered values per warp
+};
+
+// smem layout (must match spmv_ring_smem): full | empty | vst | pst | ao[chunk+1] | nptr[chunk+1] | xs | ring
+struct SrLayout {
+  size_t off_ao, off_np, off_xs, off_ring;
+  __host__ __device__ SrLayout(int chunk, int xs_per_warp) {
+    off_ao = (size_t)4 * SR_NB * 8;
+    off_np = off_ao + (size_t)(chunk + 1) * 8;
+    off_xs = (off_np + (size_t)(chunk + 1) * 4 + 15) & ~(size_t)15;
+    off_ring = (off_xs + (size_t)SR_NW * xs_per_warp * 8 + 127) & ~(size_t)127;
+  }
+};
+
+template <int NP>
+__global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
+    int mode, int nc, int chunk, const int* __restrict__ nbr_ptr, const int* __restrict__ nbr,
+    const int64_t* __restrict__ a_off, const double* __restrict__ A, const double* x, double* y, const double* z,
+    double* const* pbuf, PcgState* st, double* partials, double* alpha_hist, uint32_t ring_bytes, int G) {
+  constexpr int LPR = SrCfg<NP>::LPR, E = SrCfg<NP>::E, XS = SrCfg<NP>::XS;
+  constexpr int NTT = (SR_NW + 1) * 32;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ double red[NTT / 32];
+  __shared__ double wdot[NTT / 32];
+  int it = 0;
+  double beta = 0;
+  const double* pold = nullptr;
+  double* pnew = nullptr;
+  if (mode == 1) {
+    if (st->done) return;
+    it = st->it;
+    beta = it > 0 ? st->beta : 0.0;
+    pold = pbuf[it & 1];
+    pnew = pbuf[(it + 1) & 1];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c0 = min(nc, blockIdx.x * chunk), c1 = min(nc, c0 + chunk), n = c1 - c0;
+  const SrLayout Ly(chunk, XS);
+  unsigned char* smb = reinterpret_cast<unsigned char*>(sm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smb);
+  uint64_t* empty = full + SR_NB;
+  uint64_t* vst = empty + SR_NB;                      // virtual start of each in-flight block
+  uint64_t* pst = vst + SR_NB;                        // its physical ring offset
+  int64_t* ao = reinterpret_cast<int64_t*>(smb + Ly.off_ao);  // a_off[c0 .. c1]
+  int* nptr = reinterpret_cast<int*>(smb + Ly.off_np);        // nbr_ptr[c0 .. c1]
+  double* xs_all = reinterpret_cast<double*>(smb + Ly.off_xs);  // [SR_NW][XS] gathered values
+  unsigned char* ring = smb + Ly.off_ring;
+  for (int k = threadIdx.x; k <= n; k += NTT) { ao[k] = a_off[c0 + k]; nptr[k] = nbr_ptr[c0 + k]; }
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < SR_NB; ++t) { mbar_init(&full[t], 1); mbar_init(&empty[t], G); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  double mydot = 0;
+  if (w == SR_NW) {
+    // ---------------- producer lane: cell i at virtual bytes [V_i, V_i + len_i), physical V_i mod RB
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first();
+      const uint64_t RB = ring_bytes;
+      uint64_t V = 0, Pp = 0;  // virtual and physical write positions
+      int tail = 0;
+      const int ng = (n + G - 1) / G;
+      for (int gi = 0; gi < ng; ++gi) {  // group gi = cells [gi G, gi G + G): one bulk copy
+        const int64_t o0 = ao[gi * G], o1 = ao[min(n, gi * G + G)];
+        const uint32_t len = (uint32_t)((o1 - o0) * 8);
+        if (Pp + len > RB) { V += RB - Pp; Pp = 0; }  // do not straddle the ring end
+        // free space: every byte before the oldest unreleased group's start is free
+        while (gi - tail >= SR_NB || (tail < gi && V + len > vst[tail % SR_NB] + RB)) {
+          mbar_wait(&empty[tail % SR_NB], (uint32_t)((tail / SR_NB) & 1));
+          ++tail;
+        }
+        vst[gi % SR_NB] = V;
+        pst[gi % SR_NB] = Pp;
+        bulk_load(ring + Pp, A + o0, len, &full[gi % SR_NB], pol);
+        V += len;
+        Pp += len;
+      }
+    }
+  } else {
+    // ---------------- consumer warp w: cells i = w, w + NW, ...
+    double* xs = xs_all + w * XS;
+    auto colval = [&](int64_t id) -> double {
+      return mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
+    };
+    // gather pipeline: idx of cell i + 2 NW, values of cell i + NW
+    int idxA[E], idxB[E];  // idxB: indices of the cell whose values are in vB (kept for clarity)
+    double vB[E];
+    auto load_idx = [&](int i, int* idx) {
+      if (i >= n) {
+#pragma unroll
+        for (int t = 0; t < E; ++t) idx[t] = -1;
+        return;
+      }
+      const int lo = nptr[i], W = (nptr[i + 1] - lo) * NP;
+#pragma unroll
+      for (int t = 0; t < E; ++t) {
+        const int e = lane + 32 * t;
+        idx[t] = e < W ? __ldg(nbr + lo + e / NP) * NP + e % NP : -1;
+      }
+    };
+    auto load_val = [&](const int* idx, double* v) {
+#pragma unroll
+      for (int t = 0; t < E; ++t) v[t] = idx[t] >= 0 ? colval(idx[t]) : 0.0;
+    };
+    {
+      int idx0[E];
+      load_idx(w, idx0);
+      double v0[E];
+      load_val(idx0, v0);
+#pragma unroll
+      for (int t = 0; t < E; ++t) xs[lane + 32 * t] = v0[t];
+      load_idx(w + SR_NW, idxB);
+      load_val(idxB, vB);
+      load_idx(w + 2 * SR_NW, idxA);
+    }
+    __syncwarp();
+    const int a = lane % NP, h = lane / NP;  // row, column slice (h < LPR)
+    for (int i = w; i < n; i += SR_NW) {
+      const int c = c0 + i;
+      const int W = (nptr[i + 1] - nptr[i]) * NP;
+      // own p_new (mode 1), loaded before the wait so its latency overlaps
+      double pn = 0;
+      if (mode == 1 && h == 0 && lane < NP) {
+        const size_t id = (size_t)c * NP + a;
+        pn = it > 0 ? z[id] + beta * pold[id] : z[id];
+      }
+      const int gi = i / G, gs = gi % SR_NB;
+      mbar_wait(&full[gs], (uint32_t)((gi / SR_NB) & 1));
+      const double* Ab = reinterpret_cast<const double*>(ring + pst[gs]) + (ao[i] - ao[gi * G]);
+      double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      if (h < LPR) {
+        int col = h;
+        for (; col + 3 * LPR < W; col += 4 * LPR) {
+          s0 += Ab[col * NP + a] * xs[col];
+          s1 += Ab[(col + LPR) * NP + a] * xs[col + LPR];
+          s2 += Ab[(col + 2 * LPR) * NP + a] * xs[col + 2 * LPR];
+          s3 += Ab[(col + 3 * LPR) * NP + a] * xs[col + 3 * LPR];
+        }
+        for (; col < W; col += LPR) s0 += Ab[col * NP + a] * xs[col];
+      }
+      double v = (s0 + s1) + (s2 + s3);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[gs]);  // this cell's bytes consumed (G arrivals free the group)
+      // row sums: lane a (h = 0) adds the partials of lanes a + NP h2
+      double tot = v;
+#pragma unroll
+      for (int h2 = 1; h2 < LPR; ++h2) {
+        const double o = __shfl_sync(0xffffffffu, v, (a + NP * h2) & 31);
+        tot += o;
+      }
+      if (h == 0 && lane < NP) {
+        const size_t id = (size_t)c * NP + a;
+        y[id] = tot;
+        if (mode == 1) {
+          pnew[id] = pn;
+          mydot += pn * tot;
+        }
+      }
+      // publish the next cell's gathered values (xs is not read again for cell i), advance the pipeline
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < E; ++t) xs[lane + 32 * t] = vB[t];
+      load_val(idxA, vB);
+#pragma unroll
+      for (int t = 0; t < E; ++t) idxB[t] = idxA[t];
+      load_idx(i + 3 * SR_NW, idxA);
+      __syncwarp();
+    }
+  }
+  if (mode != 1) return;
+  mydot = warp_sum(mydot);
+  if (lane == 0) wdot[w] = mydot;
+  __syncthreads();
+  double tot[1] = {0};
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NTT / 32; ++k) tot[0] += wdot[k];
+  double res[1];
+  __shared__ bool am_last;
+  // deterministic last-CTA sum of the per-CTA partials (same protocol as iter_kernels.cu)
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = tot[0];
+    __threadfence();
+    am_last = atomicAdd(&st->cnt[0], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double sacc = 0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += NTT) sacc += __ldcg(partials + k);
+  sacc = warp_sum(sacc);
+  if (lane == 0) red[w] = sacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double pq = 0;
+    for (int k = 0; k < NTT / 32; ++k) pq += red[k];
+    res[0] = pq;
+    st->cnt[0] = 0;
+    st->pq = pq;
+    if (!(pq > 0) || !isfinite(pq)) { st->done = 1; st->status = DGAS_E_BREAKDOWN; }
+    else { st->alpha = st->gamma / pq; alpha_hist[it] = st->alpha; }
+  }
+}
+
+#define DISPATCH_PSR(P, ...)                                \
+  switch (P) {                                              \
+    case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
+    case 2: { constexpr int NP_ = 6; __VA_ARGS__; } break;  \
+    case 3: { constexpr int NP_ = 10; __VA_ARGS__; } break; \
+    case 4: { constexpr int NP_ = 15; __VA_ARGS__; } break; \
+    case 5: { constexpr int NP_ = 21; __VA_ARGS__; } break; \
+    case 6: { constexpr int NP_ = 28; __VA_ARGS__; } break; \
+  }
+
+static size_t sr_base_bytes(dgas_ctx ctx, int chunk) {
+  int xs = 0;
+  DISPATCH_PSR(ctx->p, (xs = SrCfg<NP_>::XS));
+  return SrLayout(chunk, xs).off_ring;
+}
+
+static int sr_chunk(dgas_ctx ctx) { return (ctx->nc + ctx->sr_grid - 1) / ctx->sr_grid; }
+
+size_t spmv_ring_smem(dgas_ctx ctx) { return sr_base_bytes(ctx, sr_chunk(ctx)) + ctx->sr_ring_bytes; }
+
+// degree limit of the gather (16 neighbours incl. self) and a ring that holds the largest block
+int spmv_ring_configure(dgas_ctx ctx, int nsm) {
+  if (ctx->max_deg > 16) return 1;
+  int dev = 0, optin = 232448, smem_sm = 233472;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  int cps = 2;
+  if (const char* e = std::getenv("DGAS_SR_CPS")) cps = std::max(1, std::atoi(e));
+  size_t per = (size_t)smem_sm / cps - 2048;
+  per = std::min(per, (size_t)optin - 2048);
+  ctx->sr_grid = std::min(ctx->nc, cps * nsm);
+  const size_t base = sr_base_bytes(ctx, sr_chunk(ctx));
+  int64_t maxblk = 0;
+  for (int c = 0; c < ctx->nc; ++c) maxblk = std::max(maxblk, ctx->a_off_h[c + 1] - ctx->a_off_h[c]);
+  size_t rb = per > base ? (per - base) / 128 * 128 : 0;
+  if (const char* e = std::getenv("DGAS_SR_RING_KB")) rb = std::min(rb, (size_t)std::atoi(e) * 1024);
+  // cells per bulk copy: ~16 KB per copy (small row-blocks, e.g. 4 KB on config 3, cap the TMA rate)
+  const double avg = (double)ctx->a_off_h[ctx->nc] * 8.0 / ctx->nc;
+  int G = std::max(1, std::min(8, (int)std::lround(16384.0 / avg)));
+  if (const char* e = std::getenv("DGAS_SR_G")) G = std::max(1, std::min(SR_NW, std::atoi(e)));
+  while (G > 1 && rb < (size_t)G * maxblk * 8 * 2) --G;  // groups start at chunk offsets: bound by G blocks
+  if (rb < (size_t)G * maxblk * 8 * 2) return 1;
+  ctx->sr_G = G;
+  ctx->sr_ring_bytes = (uint32_t)rb;
+  // per-function attribute shared by every context: raise it to the opt-in maximum (see panel_set_smem)
+  cudaError_t e = cudaSuccess;
+  DISPATCH_PSR(ctx->p, ({
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, k_spmv_ring<NP_>);
+    if (e == cudaSuccess && (size_t)optin < spmv_ring_smem(ctx) + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_spmv_ring<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  }));
+  if (e != cudaSuccess) { ctx->detail = std::string("spmv ring smem: ") + cudaGetErrorString(e); return -1; }
+  return 0;
+}
+
+void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s) {
+  const int grid = ctx->sr_grid, chunk = sr_chunk(ctx);
+  const size_t smem = spmv_ring_smem(ctx);
+  DISPATCH_PSR(ctx->p, (k_spmv_ring<NP_><<<grid, (SR_NW + 1) * 32, smem, s>>>(
+                           mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr, ctx->d_a_off, ctx->d_A, x, y, ctx->d_z,
+                           ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha, ctx->sr_ring_bytes, ctx->sr_G)));
+}

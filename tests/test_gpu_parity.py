@@ -411,3 +411,35 @@ def test_local_kernel_variants(monkeypatch, name, env, kernel):
     x, iters, cond, st = S.pcg(_dev(b))
     assert st == 0 and abs(iters - ref["iters"]) <= 2
     S.close()
+
+
+@pytest.mark.parametrize("name,env", [
+    ("cfg2s", {"DGAS_SPMV_KERNEL": "3"}),
+    ("cfg4s", {"DGAS_SPMV_KERNEL": "3"}),
+    # small byte ring: many wrap-arounds and producer waits on the oldest block
+    ("cfg4s", {"DGAS_SR_RING_KB": "40", "DGAS_SR_CPS": "4"}),
+    ("cfg5s_p6q6", {"DGAS_SR_RING_KB": "120"}),
+    ("cfg1", {}),
+])
+def test_spmv_kernel_variants(monkeypatch, name, env):
+    """Both SpMV kernels (slot ring k_spmv3, byte ring k_spmv_ring) match the oracle's A x, and the
+    fused PCG path built on them matches the oracle's iteration count."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = CASES[name]()
+    S = _solver(P)
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    rng = np.random.default_rng(5)
+    kap = _kappa_gram(o, rng.choice(P.n_cells, size=min(64, P.n_cells), replace=False))
+    tol = max(1e-13, 20 * kap * _EPS)  # as test_spmv_rhs: two correct assemblies differ by ~kappa eps
+    for seed in range(2):
+        xv = g.normal(400 + seed, S.N)
+        yv = S.spmv(_dev(xv)).cpu().numpy()
+        yr = o.spmv(xv)
+        assert np.all(np.abs(yv - yr) <= tol * o.spmv_abs(xv) + 1e-300), seed
+    b = o.rhs()
+    ref = o.pcg(b, rtol=1e-8)
+    x, iters, cond, st = S.pcg(_dev(b))
+    assert st == 0 and abs(iters - ref["iters"]) <= 2
+    S.close()
