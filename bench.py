@@ -262,7 +262,7 @@ def main():
                                  f"> 126 MB L2"),
                    "parallelism": "replicas" if world > 1 else "single-gpu", "setup_s": t_setup,
                    "coarse_solver": ["dense-inverse", "band", "nested-dissection"][info["coarse_mode"]],
-                   "local_kernel": {1: "envelope (all subdomains resident)", 2: "panel (L2 reuse)"}.get(info["local_kernel"]),
+                   "local_kernel": {1: "envelope", 2: "panel"}.get(info["local_kernel"]),
                    "local_ctas_per_sm": info["local_ctas_per_sm"]},
         "dof_iters_per_s": value * N / max(world, 1) * world,
         "ms_per_apply": kt["apply_total"],

@@ -35,20 +35,28 @@ static int panel_configure(dgas_ctx ctx) {
   if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;
   size_t per_cta = ((size_t)smem_sm - std::min((size_t)smem_sm / 2, reserve)) / cps - 1024;
   per_cta = std::min(per_cta, (size_t)optin);
-  const size_t base = panel_base_bytes(ctx->max_sub_cells, ctx->np) + 128;
-  size_t target = 12 * 1024;
+  const size_t base = panel_base_bytes(ctx->max_sub_cells, ctx->np, cps > 3) + 128;
+  // ring: S (a power of two) slots of about `target` bytes that together fill the budget; CC columns
+  // per slot (even, at least panel_min_cc, at most the widest panel)
+  size_t target = 8 * 1024;
   if (const char* e = std::getenv("DGAS_PANEL_SLOT_KB")) target = (size_t)std::atoi(e) * 1024;
   const int maxW = ctx->max_urow + ctx->np;
-  const int cc_min = panel_min_cc(ctx->np);
-  int CC = std::max(cc_min, std::min((maxW + 1) / 2 * 2, std::max(2, (int)(target / (8 * ctx->np)) / 2 * 2)));
+  const int cc_min = panel_min_cc(ctx->np), cc_max = std::max(cc_min, (maxW + 1) / 2 * 2);
   ctx->panel_slots = 0;
-  for (; CC >= cc_min; CC -= 2) {
-    const uint32_t sb = (uint32_t)(((((int64_t)CC * ctx->np + 1) / 2 * 2) * 8 + 127) / 128 * 128);
-    if (per_cta <= base) break;
-    int S = (int)std::min<size_t>(64, (per_cta - base) / sb);
-    int S2 = 1;
-    while (S2 * 2 <= S) S2 *= 2;
-    if (S2 >= 2) { ctx->panel_slots = S2; ctx->panel_slot_bytes = sb; ctx->panel_cc = CC; break; }
+  if (per_cta > base) {
+    const size_t B = per_cta - base;
+    int S = 2;
+    while (S < 64 && B / (2 * S) >= target) S *= 2;
+    for (; S >= 2; S /= 2) {
+      int CC = (int)std::min<size_t>(cc_max, (B / S) / (8 * ctx->np)) / 2 * 2;
+      if (CC < cc_min) continue;
+      const uint32_t sb = (uint32_t)(((((int64_t)CC * ctx->np + 1) / 2 * 2) * 8 + 127) / 128 * 128);
+      while (S < 64 && (size_t)2 * S * sb <= B) S *= 2;  // CC capped at the widest panel: more slots
+      ctx->panel_slots = S;
+      ctx->panel_slot_bytes = sb;
+      ctx->panel_cc = CC;
+      break;
+    }
   }
   if (ctx->panel_slots < 2) { ctx->local_kernel = 1; return 0; }  // subdomain too large: envelope kernel
   ctx->panel_keep = 1;

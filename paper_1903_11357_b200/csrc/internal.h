@@ -288,7 +288,7 @@ size_t spmv_ring_smem(dgas_ctx ctx);
 void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s);
 int panel_supported(int p);
 int panel_min_cc(int np);
-size_t panel_base_bytes(int max_cells, int np);
+size_t panel_base_bytes(int max_cells, int np, bool narrow);
 int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first);
 size_t panel_smem_bytes(dgas_ctx ctx);
 int panel_set_smem(dgas_ctx ctx);

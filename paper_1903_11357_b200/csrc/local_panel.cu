@@ -43,15 +43,17 @@ __host__ __device__ constexpr int panel_e(int np) { return (((panel_dpk(np) + np
 __host__ __device__ constexpr int panel_dcol(int np, int c) { return c * np - c * (c - 1) / 2; }
 __host__ __device__ inline int panel_units(int wu, int cc, int cc0) { return 1 + (wu > cc0 ? (wu - cc0 + cc - 1) / cc : 0); }
 
-// smem layout (must match panel_smem_bytes): full[64] | empty[64] | us[mc+1] | fk[mc] | po[mc] | R | Y | ring
+// smem layout (must match panel_smem_bytes): full[64] | empty[64] | us[mc+1] | fk[mc] | po[mc] | [R] | Y | ring
+// R (r_i staged) only in wide CTAs (latency-bound: r_k read from shared memory on the chain); narrow
+// CTAs (HBM-bound, shared memory goes to the ring) read r_k from global memory one step ahead.
 struct PanelLayout {
   size_t off_us, off_fk, off_po, off_R, off_Y, off_ring;
-  __host__ __device__ PanelLayout(int mc, int np) {
+  __host__ __device__ PanelLayout(int mc, int np, bool stage_r) {
     off_us = 1024;
     off_fk = off_us + (((size_t)(mc + 1) * 4 + 15) & ~(size_t)15);
     off_po = off_fk + (((size_t)mc * 4 + 15) & ~(size_t)15);
-    off_R = off_po + (size_t)mc * 8;
-    off_Y = off_R + (((size_t)mc * np * 8 + 15) & ~(size_t)15);
+    off_R = (off_po + (size_t)mc * 8 + 15) & ~(size_t)15;
+    off_Y = off_R + (stage_r ? (((size_t)mc * np * 8 + 15) & ~(size_t)15) : 0);
     off_ring = (off_Y + (size_t)mc * np * 8 + 127) & ~(size_t)127;
   }
 };
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
     r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
   }
   const int s = blockIdx.x, s0 = sub_ptr[s], m = sub_ptr[s + 1] - s0;
-  const PanelLayout L(max_cells, NP);
+  const PanelLayout L(max_cells, NP, !NARROW);
   unsigned char* smb = reinterpret_cast<unsigned char*>(sm);
   uint64_t* full = reinterpret_cast<uint64_t*>(smb);
   uint64_t* empty = full + 64;
@@ -134,15 +136,26 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
   const int lane = tid & 31;
   uint64_t fph = 0;  // parity of the next full-barrier phase per slot
   const double* rs = r + (size_t)s0 * NP;
-  for (int e = tid; e < m * NP; e += T) R[e] = rs[e];
-  named_sync(1, T);
+  if constexpr (!NARROW) {
+    for (int e = tid; e < m * NP; e += T) R[e] = rs[e];
+    named_sync(1, T);
+  }
   // forward: thread (a, q) accumulates row a of P_k over columns c = q (mod LPR)
   {
     const int a = tid / LPR, q = tid % LPR;
+    constexpr int RN = (NP + LPR - 1) / LPR;  // D_k columns (r_k entries) per thread
+    double rk[RN];  // narrow: r_k entries c = q + LPR t, prefetched one step ahead (overwritten after use)
+    if constexpr (NARROW) {
+#pragma unroll
+      for (int t = 0; t < RN; ++t) rk[t] = q + LPR * t < NP ? rs[q + LPR * t] : 0.0;
+    }
     for (int k = 0; k < m; ++k) {
       const int u0 = us_s[k], u1 = us_s[k + 1], fk = fk_s[k];
       const int WU = (k - fk) * NP;
-      const double* rk = R + k * NP;
+      if constexpr (!NARROW) {
+#pragma unroll
+        for (int t = 0; t < RN; ++t) rk[t] = q + LPR * t < NP ? R[k * NP + q + LPR * t] : 0.0;
+      }
       const double* yb = Y + fk * NP;  // U column j multiplies Y[f_k NP + j]
       double v0 = 0, v1 = 0;
       for (int u = u0; u < u1; ++u) {
@@ -154,8 +167,16 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
           int j0, j1;
           const double* Pu;  // U column j at Pu[j NP]
           if (t == 0) {
-            for (int c = q; c < NP; c += LPR)  // D_k r_k, lower triangle
-              if (c <= a) v1 += Ps[panel_dcol(NP, c) + a - c] * rk[c];
+#pragma unroll
+            for (int t = 0; t < RN; ++t) {  // D_k r_k, lower triangle
+              const int c = q + LPR * t;
+              if (c < NP && c <= a) v1 += Ps[panel_dcol(NP, c) + a - c] * rk[t];
+            }
+            if constexpr (NARROW) {  // prefetch r_{k+1}
+#pragma unroll
+              for (int t = 0; t < RN; ++t)
+                rk[t] = k + 1 < m && q + LPR * t < NP ? rs[(k + 1) * NP + q + LPR * t] : 0.0;
+            }
             j0 = 0; j1 = min(WU, CC0); Pu = Ps + DPK + a;
           } else {
             j0 = CC0 + (t - 1) * CC; j1 = min(WU, j0 + CC); Pu = Ps - j0 * NP + a;
@@ -275,7 +296,7 @@ int panel_min_cc(int np) { return panel_e(np) + 2; }
 // 128 consumer threads when more than 3 CTAs share an SM (registers), else 256
 static bool panel_narrow(dgas_ctx ctx) { return ctx->panel_cps > 3; }
 
-size_t panel_base_bytes(int max_cells, int np) { return PanelLayout(max_cells, np).off_ring; }
+size_t panel_base_bytes(int max_cells, int np, bool narrow) { return PanelLayout(max_cells, np, !narrow).off_ring; }
 
 // host: panel offsets, per-cell unit starts, per-subdomain unit counts; device: the panels
 int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first) {
@@ -310,7 +331,8 @@ int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector
 }
 
 size_t panel_smem_bytes(dgas_ctx ctx) {
-  return PanelLayout(ctx->max_sub_cells, ctx->np).off_ring + (size_t)ctx->panel_slots * ctx->panel_slot_bytes + 128;
+  return PanelLayout(ctx->max_sub_cells, ctx->np, !panel_narrow(ctx)).off_ring +
+         (size_t)ctx->panel_slots * ctx->panel_slot_bytes + 128;
 }
 
 // The attribute is per function (shared by every context in the process): always raise it to the
