@@ -121,6 +121,8 @@ struct dgas_ctx_s {
   int* d_cov = nullptr;
   int* d_fov_ptr = nullptr;       // fine cell -> pieces CSR (first = owner)
   int* d_fov = nullptr;
+  int2* d_rrec = nullptr;         // [nov] restriction order (cov): (cell, piece | owner << 31)
+  int2* d_prec = nullptr;         // [nov] prolongation order (fov): (piece, coarse element)
   int* d_ctri_ptr = nullptr;      // coarse J -> fan triangles (piece, t)
   int* d_ctri = nullptr;
   double* d_Cc = nullptr;         // [ncoarse][nq*nq]

@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk
 #define RT 256
 template <int NP, int NQ>
 __global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj, int cpj, const int* __restrict__ cov_ptr,
-                                                 const int* __restrict__ cov, const int* __restrict__ ov_cell,
-                                                 const int* __restrict__ fov_ptr, const int* __restrict__ fov,
+                                                 const int2* __restrict__ rrec,
                                                  const double* __restrict__ G, const double* r_in, double* const* rbuf,
                                                  const double* q, double* const* pbuf, double* x, const double* b,
                                                  double* r0, double* rpart, unsigned* jcnt, PcgState* st,
@@ -385,26 +384,45 @@ __global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj,
 #pragma unroll
   for (int k = 0; k < NQ; ++k) accq[k] = 0;
   double rr = 0, bb = 0;
-  if (J < ncoarse)
-    for (int k = cov_ptr[J] + gw * PPW + lane / L; k < cov_ptr[J + 1]; k += TW * PPW) {
-      if (a >= NP) continue;
-      const int o = cov[k], cell = ov_cell[o];
-      const bool owner = fov[fov_ptr[cell]] == o;
-      const size_t id = (size_t)cell * NP + a;
-      double rv;
-      if (mode == 0) rv = rold[id];
-      else if (mode == 1) rv = rold[id] - alpha * q[id];
-      else rv = b[id] - q[id];
-      if (owner && mode >= 1) {
-        rnew[id] = rv;
-        rr += rv * rv;
-        if (mode == 1) x[id] += alpha * pnew[id];
-        else bb += b[id] * b[id];
-      }
-      const double* Go = G + ((size_t)o * NP + a) * NQ;
+  if (J < ncoarse) {
+    // packed records (cell, piece | owner << 31): one load per piece, the next one prefetched
+    const int ke = cov_ptr[J + 1], kstep = TW * PPW;
+    int k = cov_ptr[J] + gw * PPW + lane / L;
+    int2 rec = k < ke ? rrec[k] : make_int2(0, 0);
+    for (; k < ke; k += kstep) {
+      const int2 nrec = k + kstep < ke ? rrec[k + kstep] : rec;
+      if (a < NP) {
+        const int cell = rec.x, o = rec.y & 0x7fffffff;
+        const bool owner = rec.y < 0;
+        const size_t id = (size_t)cell * NP + a;
+        const double* Go = G + ((size_t)o * NP + a) * NQ;
+        double gv[NQ];
+        if constexpr (NQ % 2 == 0) {
 #pragma unroll
-      for (int c = 0; c < NQ; ++c) accq[c] += Go[c] * rv;
+          for (int c = 0; c < NQ; c += 2) {
+            const double2 g2 = __ldg(reinterpret_cast<const double2*>(Go + c));
+            gv[c] = g2.x; gv[c + 1] = g2.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NQ; ++c) gv[c] = __ldg(Go + c);
+        }
+        double rv;
+        if (mode == 0) rv = rold[id];
+        else if (mode == 1) rv = rold[id] - alpha * q[id];
+        else rv = b[id] - q[id];
+        if (owner && mode >= 1) {
+          rnew[id] = rv;
+          rr += rv * rv;
+          if (mode == 1) x[id] += alpha * pnew[id];
+          else bb += b[id] * b[id];
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) accq[c] += gv[c] * rv;
+      }
+      rec = nrec;
     }
+  }
 #pragma unroll
   for (int c = 0; c < NQ; ++c) {
     const double v = warp_sum(accq[c]);
@@ -734,7 +752,7 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
 #define PW 8
 template <int NP, int NQ>
 __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int* __restrict__ fov_ptr,
-                                                     const int* __restrict__ fov, const int* __restrict__ ov_coarse,
+                                                     const int2* __restrict__ prec,
                                                      const double* __restrict__ G, const double* z0, double* z,
                                                      double* const* rbuf, PcgState* st, double* partials,
                                                      double* beta_hist, cudaGraphConditionalHandle h, int use_h) {
@@ -758,7 +776,8 @@ __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int
     size_t id = (size_t)c * NP + a;
     double v = z[id];
     for (int k = fov_ptr[c]; k < fov_ptr[c + 1]; ++k) {
-      const int o = fov[k], J = ov_coarse[o];
+      const int2 pr = prec[k];  // (piece, coarse element)
+      const int o = pr.x, J = pr.y;
       const double* Go = G + ((size_t)o * NP + a) * NQ;
 #pragma unroll
       for (int b = 0; b < NQ; ++b) v += Go[b] * z0[(size_t)J * NQ + b];
@@ -977,8 +996,7 @@ void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cuda
   const int wpj = ctx->restrict_wpj, cpj = ctx->restrict_cpj;
   const int grid = cpj > 1 ? ctx->ncoarse * cpj : (ctx->ncoarse + (RT / 32 / wpj) - 1) / (RT / 32 / wpj);
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_restrict<NP_, NQ_><<<grid, RT, 0, s>>>(
-                                            mode, ctx->ncoarse, wpj, cpj, ctx->d_cov_ptr, ctx->d_cov, ctx->d_ov_cell,
-                                            ctx->d_fov_ptr, ctx->d_fov, ctx->d_G, r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf,
+                                            mode, ctx->ncoarse, wpj, cpj, ctx->d_cov_ptr, ctx->d_rrec, ctx->d_G, r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf,
                                             ctx->d_x, ctx->d_b, ctx->d_r0, ctx->d_rpart, ctx->d_jcnt, st,
                                             ctx->d_partials))));
 }
@@ -1109,7 +1127,7 @@ void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, doubl
   unsigned grid = 1;
   DISPATCH_P(ctx->p, (grid = (ctx->nc + PW * ProlongCfg<NP_>::CPW - 1) / (PW * ProlongCfg<NP_>::CPW)));
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_prolong<NP_, NQ_><<<grid, PW * 32, 0, s>>>(
-                                            mode, ctx->nc, ctx->d_fov_ptr, ctx->d_fov, ctx->d_ov_coarse, ctx->d_G,
+                                            mode, ctx->nc, ctx->d_fov_ptr, ctx->d_prec, ctx->d_G,
                                             ctx->d_z0, z, ctx->d_rbuf, st, ctx->d_partials, ctx->d_beta, h,
                                             use_handle))));
 }

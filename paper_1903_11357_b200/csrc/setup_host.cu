@@ -389,6 +389,21 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
   if ((st = dev_upload(ctx, &ctx->d_cov, cov))) return bail(st, ctx->detail);
   if ((st = dev_upload(ctx, &ctx->d_fov_ptr, fov_ptr))) return bail(st, ctx->detail);
   if ((st = dev_upload(ctx, &ctx->d_fov, fov))) return bail(st, ctx->detail);
+  {
+    // packed piece records: one load gives everything the restriction / prolongation needs
+    // (restriction order: cell and piece with the owner bit; prolongation order: piece and coarse element)
+    std::vector<int2> rrec(nov), prec(nov);
+    for (int J = 0; J < ctx->ncoarse; ++J)
+      for (int k = cov_ptr[J]; k < cov_ptr[J + 1]; ++k) {
+        const int o = cov[k], cell = ov_cell[o];
+        const bool owner = fov[fov_ptr[cell]] == o;
+        rrec[k] = make_int2(cell, o | (owner ? (int)0x80000000u : 0));
+      }
+    for (int c = 0; c < nc; ++c)
+      for (int k = fov_ptr[c]; k < fov_ptr[c + 1]; ++k) prec[k] = make_int2(fov[k], ov_coarse[fov[k]]);
+    if ((st = dev_upload(ctx, &ctx->d_rrec, rrec))) return bail(st, ctx->detail);
+    if ((st = dev_upload(ctx, &ctx->d_prec, prec))) return bail(st, ctx->detail);
+  }
   if ((st = dev_upload(ctx, &ctx->d_ctri_ptr, ctri_ptr))) return bail(st, ctx->detail);
   if ((st = dev_upload(ctx, &ctx->d_ctri, ctri))) return bail(st, ctx->detail);
   if ((st = dev_alloc(ctx, &ctx->d_Cc, (size_t)ctx->ncoarse * nq * nq))) return bail(st, ctx->detail);
@@ -453,7 +468,7 @@ static void free_ctx(dgas_ctx ctx) {
                   ctx->d_p[0], ctx->d_p[1], ctx->d_r0, ctx->d_z0, ctx->d_t1, ctx->d_t2, ctx->d_partials,
                   ctx->d_state, ctx->d_astate, ctx->d_alpha, ctx->d_beta, ctx->d_lanczos, ctx->d_err,
                   ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev, ctx->d_rpart, ctx->d_jcnt,
-                  ctx->d_P, ctx->d_p_off, ctx->d_pus, ctx->d_sub_units};
+                  ctx->d_P, ctx->d_p_off, ctx->d_pus, ctx->d_sub_units, ctx->d_rrec, ctx->d_prec};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->d_A0b) cudaFree(ctx->d_A0b);
