@@ -27,8 +27,8 @@
 template <int NP, bool NARROW = false>
 struct PanelCfg {
   static constexpr int T = (NP > 4 && !NARROW) ? 256 : 128;       // consumer threads
-  static constexpr int ROWS = NP > 8 ? 16 : (NP > 4 ? 8 : 4);     // row slots in the forward step
-  static constexpr int LPR = T / ROWS;                            // lanes per row (16 or 32)
+  static constexpr int ROWS = NP > 16 ? 32 : NP > 8 ? 16 : (NP > 4 ? 8 : 4);  // row slots in the forward step
+  static constexpr int LPR = T / ROWS;                            // lanes per row (4 .. 32)
   static constexpr int NW = T / 32;
   static constexpr int H = (NP + 1) / 2;                          // rows per half in the backward step
 };
@@ -287,8 +287,12 @@ __global__ void k_build_panels(int np, int nc, const int* sub_ptr_of_cell, const
     case 2: { constexpr int NP_ = 6; __VA_ARGS__; } break;  \
     case 3: { constexpr int NP_ = 10; __VA_ARGS__; } break; \
     case 4: { constexpr int NP_ = 15; __VA_ARGS__; } break; \
+    case 5: { constexpr int NP_ = 21; __VA_ARGS__; } break; \
+    case 6: { constexpr int NP_ = 28; __VA_ARGS__; } break; \
   }
 
+// p = 5, 6 compile (n_p = 21, 28) but are slower than the envelope kernel (config 5 p = q = 6:
+// 1228 vs 1440 PCG it/s, measured), so the panel kernel is used for p <= 4 only
 int panel_supported(int p) { return p >= 1 && p <= 4; }
 
 int panel_min_cc(int np) { return panel_e(np) + 2; }

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(ND_T) k_nd_factor(const int* __restrict__ fron
 
 // ------------------------------------------------------------------ solve: forward level
 // work item (front, first row of U); t assembled in shared memory by every CTA of the front
-__global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict__ work, const int* __restrict__ nF,
+__global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict__ work, int nwork, const int* __restrict__ nF,
                                                  const int* __restrict__ nU, const int* __restrict__ offT,
                                                  const int* __restrict__ offu, const int* __restrict__ offFe,
                                                  const int* __restrict__ Fe, const int64_t* __restrict__ offM,
@@ -160,7 +160,11 @@ __global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict_
                                                  int mode) {
   extern __shared__ double t[];
   if (mode >= 1 && st->done) return;
-  const int2 wi = work[blockIdx.x];
+  // grid-stride over the level's work items: a level runs in one wave of at most nd_grid CTAs, which
+  // fit beside the local-solve CTAs the coarse chain runs concurrently with
+  for (int wk = blockIdx.x; wk < nwork; wk += gridDim.x) {
+  if (wk != (int)blockIdx.x) __syncthreads();  // t of the previous item fully consumed
+  const int2 wi = work[wk];
   const int f = wi.x, row0 = wi.y;
   const int nf = nF[f], nu = nU[f];
   for (int k = threadIdx.x; k < nf; k += ND_T) {
@@ -188,10 +192,11 @@ __global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict_
     v = warp_sum(v);
     if (lane == 0) ug[offu[f] + r] = t[nf + r] - v;
   }
+  }
 }
 
 // ------------------------------------------------------------------ solve: backward level
-__global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict__ work, const int* __restrict__ nF,
+__global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict__ work, int nwork, const int* __restrict__ nF,
                                                  const int* __restrict__ nU, const int* __restrict__ offT,
                                                  const int* __restrict__ offFe, const int* __restrict__ Fe,
                                                  const int* __restrict__ offUe, const int* __restrict__ Ue,
@@ -201,7 +206,9 @@ __global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict_
                                                  const PcgState* st, int mode) {
   extern __shared__ double sh[];
   if (mode >= 1 && st->done) return;
-  const int2 wi = work[blockIdx.x];
+  for (int wk = blockIdx.x; wk < nwork; wk += gridDim.x) {  // grid-stride (see k_nd_fwd)
+  if (wk != (int)blockIdx.x) __syncthreads();
+  const int2 wi = work[wk];
   const int f = wi.x, row0 = wi.y;
   const int nf = nF[f], nu = nU[f];
   double* tF = sh;
@@ -227,6 +234,7 @@ __global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict_
       const size_t g = (size_t)Fe[offFe[f] + j / nq] * nq + j % nq;
       z0[g] = v * dsc[g];
     }
+  }
   }
 }
 
@@ -342,14 +350,14 @@ static void nd_solve_once(dgas_ctx ctx, int mode, const PcgState* st, cudaStream
   for (int L = 0; L < P.nlev; ++L) {
     const int n = P.h_wf_ptr[L + 1] - P.h_wf_ptr[L];
     if (n)
-      k_nd_fwd<<<n, ND_T, shf, s>>>(ctx->nq, P.d_wf + P.h_wf_ptr[L], P.d_nF, P.d_nU, P.d_offT, P.d_offu, P.d_offFe,
+      k_nd_fwd<<<std::min(n, ctx->nd_grid), ND_T, shf, s>>>(ctx->nq, P.d_wf + P.h_wf_ptr[L], n, P.d_nF, P.d_nU, P.d_offT, P.d_offu, P.d_offFe,
                                     P.d_Fe, P.d_offM, P.d_childptr, P.d_childs, P.d_cmap_ptr, P.d_cmap, P.d_M, P.d_dsc,
                                     rin, P.d_T, P.d_u, st, mode);
   }
   for (int L = P.nlev - 1; L >= 0; --L) {
     const int n = P.h_wb_ptr[L + 1] - P.h_wb_ptr[L];
     if (n)
-      k_nd_bwd<<<n, ND_T, shb, s>>>(ctx->nq, P.d_wb + P.h_wb_ptr[L], P.d_nF, P.d_nU, P.d_offT, P.d_offFe, P.d_Fe,
+      k_nd_bwd<<<std::min(n, ctx->nd_grid), ND_T, shb, s>>>(ctx->nq, P.d_wb + P.h_wb_ptr[L], n, P.d_nF, P.d_nU, P.d_offT, P.d_offFe, P.d_Fe,
                                     P.d_offUe, P.d_Ue, P.d_offX, P.d_offM, P.d_X, P.d_MT, P.d_dsc, P.d_T, zout, st,
                                     mode);
   }

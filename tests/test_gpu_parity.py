@@ -389,7 +389,8 @@ def test_eager_path_matches_graph(monkeypatch, name):
     # tiny ring: every panel spans several units, many backward refills (producer protocol)
     ("cfg4s", {"DGAS_LOCAL_CPS": "8", "DGAS_PANEL_SLOT_KB": "1"}, 2),
     ("cfg3s", {"DGAS_PANEL_KEEP": "0", "DGAS_LOCAL_CPS": "3"}, 2),
-    ("cfg5s_p6q1", {}, 1),  # n_p = 28: panels not supported, envelope kernel
+    ("cfg5s_p6q1", {}, 1),  # n_p = 28: envelope kernel (faster there)
+    ("cfg5s_p4q4", {"DGAS_LOCAL_CPS": "7"}, 2),  # 128-thread CTAs on a small problem
 ])
 def test_local_kernel_variants(monkeypatch, name, env, kernel):
     """Both local-solve kernels (envelope k_local, panel k_local_panel) and the panel kernel's ring
