@@ -11,6 +11,21 @@
 #define ND_T 256
 #define ND_ROWS 32  // rows of a front per CTA in the solve
 
+// Solve-phase operator loads (X_F, M_F, M_F^T) carry an L2 evict-last policy: the chain of level
+// launches is latency-bound and runs beside the HBM-saturating local solves, so it should find its
+// factors in L2 (the streamed SpMV / local-solve copies are evict-first). DGAS_ND_L2=0 disables it.
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t nd_policy(int keep) {
+  uint64_t pol;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // ------------------------------------------------------------------ setup: assemble front matrices
 __global__ void __launch_bounds__(ND_T) k_nd_assemble(int nq, const int* __restrict__ fronts, const int* nF, const int* nU,
                                                       const int64_t* offS, const int64_t* offUpd, const int* asm_ptr,
@@ -157,8 +172,9 @@ __global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict_
                                                  const int* __restrict__ cmap_ptr, const int* __restrict__ cmap,
                                                  const double* __restrict__ Mg, const double* __restrict__ dsc,
                                                  const double* r0, double* Tg, double* ug, const PcgState* st,
-                                                 int mode) {
+                                                 int mode, int keep) {
   extern __shared__ double t[];
+  const uint64_t pol = nd_policy(keep);
   if (mode >= 1 && st->done) return;
   // grid-stride over the level's work items: a level runs in one wave of at most nd_grid CTAs, which
   // fit beside the local-solve CTAs the coarse chain runs concurrently with
@@ -188,7 +204,7 @@ __global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict_
   for (int r = row0 + w; r < rend; r += ND_T / 32) {
     const double* mr = M + (size_t)r * nf;
     double v = 0;
-    for (int k = lane; k < nf; k += 32) v += mr[k] * t[k];
+    for (int k = lane; k < nf; k += 32) v += ld_keep(mr + k, pol) * t[k];
     v = warp_sum(v);
     if (lane == 0) ug[offu[f] + r] = t[nf + r] - v;
   }
@@ -203,8 +219,9 @@ __global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict_
                                                  const int64_t* __restrict__ offX, const int64_t* __restrict__ offM,
                                                  const double* __restrict__ Xg, const double* __restrict__ MTg,
                                                  const double* __restrict__ dsc, const double* Tg, double* z0,
-                                                 const PcgState* st, int mode) {
+                                                 const PcgState* st, int mode, int keep) {
   extern __shared__ double sh[];
+  const uint64_t pol = nd_policy(keep);
   if (mode >= 1 && st->done) return;
   for (int wk = blockIdx.x; wk < nwork; wk += gridDim.x) {  // grid-stride (see k_nd_fwd)
   if (wk != (int)blockIdx.x) __syncthreads();
@@ -227,8 +244,8 @@ __global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict_
     const double* xr = X + (size_t)j * nf;
     const double* mr = MT + (size_t)j * nu;
     double v = 0;
-    for (int k = lane; k < nf; k += 32) v += xr[k] * tF[k];
-    for (int k = lane; k < nu; k += 32) v -= mr[k] * xU[k];
+    for (int k = lane; k < nf; k += 32) v += ld_keep(xr + k, pol) * tF[k];
+    for (int k = lane; k < nu; k += 32) v -= ld_keep(mr + k, pol) * xU[k];
     v = warp_sum(v);
     if (lane == 0) {
       const size_t g = (size_t)Fe[offFe[f] + j / nq] * nq + j % nq;
@@ -352,14 +369,14 @@ static void nd_solve_once(dgas_ctx ctx, int mode, const PcgState* st, cudaStream
     if (n)
       k_nd_fwd<<<std::min(n, ctx->nd_grid), ND_T, shf, s>>>(ctx->nq, P.d_wf + P.h_wf_ptr[L], n, P.d_nF, P.d_nU, P.d_offT, P.d_offu, P.d_offFe,
                                     P.d_Fe, P.d_offM, P.d_childptr, P.d_childs, P.d_cmap_ptr, P.d_cmap, P.d_M, P.d_dsc,
-                                    rin, P.d_T, P.d_u, st, mode);
+                                    rin, P.d_T, P.d_u, st, mode, ctx->nd_l2);
   }
   for (int L = P.nlev - 1; L >= 0; --L) {
     const int n = P.h_wb_ptr[L + 1] - P.h_wb_ptr[L];
     if (n)
       k_nd_bwd<<<std::min(n, ctx->nd_grid), ND_T, shb, s>>>(ctx->nq, P.d_wb + P.h_wb_ptr[L], n, P.d_nF, P.d_nU, P.d_offT, P.d_offFe, P.d_Fe,
                                     P.d_offUe, P.d_Ue, P.d_offX, P.d_offM, P.d_X, P.d_MT, P.d_dsc, P.d_T, zout, st,
-                                    mode);
+                                    mode, ctx->nd_l2);
   }
 }
 

@@ -253,7 +253,10 @@ int spmv_ring_configure(dgas_ctx ctx, int nsm) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  int cps = 2;
+  // 2 CTAs/SM; 1 (one ~220 KB ring) when row-blocks are large (n_p = 28: 44 KB per cell, so a 110 KB
+  // ring holds only two; measured config 5 p = q = 6: SpMV 0.159 -> 0.118 ms)
+  const double avg_blk = (double)ctx->a_off_h[ctx->nc] * 8.0 / ctx->nc;
+  int cps = avg_blk > 24576.0 ? 1 : 2;
   if (const char* e = std::getenv("DGAS_SR_CPS")) cps = std::max(1, std::atoi(e));
   size_t per = (size_t)smem_sm / cps - 2048;
   per = std::min(per, (size_t)optin - 2048);
@@ -264,7 +267,7 @@ int spmv_ring_configure(dgas_ctx ctx, int nsm) {
   size_t rb = per > base ? (per - base) / 128 * 128 : 0;
   if (const char* e = std::getenv("DGAS_SR_RING_KB")) rb = std::min(rb, (size_t)std::atoi(e) * 1024);
   // cells per bulk copy: ~16 KB per copy (small row-blocks, e.g. 4 KB on config 3, cap the TMA rate)
-  const double avg = (double)ctx->a_off_h[ctx->nc] * 8.0 / ctx->nc;
+  const double avg = avg_blk;
   int G = std::max(1, std::min(8, (int)std::lround(16384.0 / avg)));
   if (const char* e = std::getenv("DGAS_SR_G")) G = std::max(1, std::min(SR_NW, std::atoi(e)));
   while (G > 1 && rb < (size_t)G * maxblk * 8 * 2) --G;  // groups start at chunk offsets: bound by G blocks
