@@ -256,7 +256,7 @@ int spmv_ring_configure(dgas_ctx ctx, int nsm) {
   // 2 CTAs/SM; 1 (one ~220 KB ring) when row-blocks are large (n_p = 28: 44 KB per cell, so a 110 KB
   // ring holds only two; measured config 5 p = q = 6: SpMV 0.159 -> 0.118 ms)
   const double avg_blk = (double)ctx->a_off_h[ctx->nc] * 8.0 / ctx->nc;
-  int cps = avg_blk > 24576.0 ? 1 : 2;
+  int cps = avg_blk > 18432.0 ? 1 : 2;  // p = 5 (~23 KB): 0.086 -> 0.071 ms
   if (const char* e = std::getenv("DGAS_SR_CPS")) cps = std::max(1, std::atoi(e));
   size_t per = (size_t)smem_sm / cps - 2048;
   per = std::min(per, (size_t)optin - 2048);
