@@ -92,8 +92,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
   {
     // restriction: about 4 warp steps (32 / L pieces each) per warp; 1..8 warps per coarse element in one
     // CTA, then more CTAs per coarse element (cpj) while the grid stays within the partials buffer
-    const int lanes = ctx->np <= 4 ? 4 : ctx->np <= 8 ? 8 : ctx->np <= 16 ? 16 : 32;
-    const int64_t per_warp = 4 * (32 / lanes);
+    const int64_t per_warp = 4 * pack_ppw(ctx->np);  // pieces per warp step (n_p lanes per piece)
     const int64_t need = (ctx->nov + ctx->ncoarse * per_warp - 1) / (ctx->ncoarse * per_warp);  // warps per J
     int w = 1;
     while (w < 8 && w < need) w *= 2;

@@ -291,6 +291,7 @@ int spmv_ring_configure(dgas_ctx ctx, int nsm);
 size_t spmv_ring_smem(dgas_ctx ctx);
 void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s);
 int panel_supported(int p);
+int pack_ppw(int np);
 int panel_min_cc(int np);
 size_t panel_base_bytes(int max_cells, int np, bool narrow);
 int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first);

@@ -53,7 +53,15 @@ __device__ inline bool last_block(const double* mine, double* partials, unsigned
   return true;
 }
 
-// lanes per cell row (or overlap piece) in the cell-wise vector kernels, cells per warp
+// restriction / prolongation: n_p lanes per piece (cell), 32 / n_p pieces per warp (lanes beyond
+// idle): 94% of the lanes busy at n_p = 10, 15 (62% / 94% with power-of-two groups)
+template <int NP>
+struct PackCfg {
+  static constexpr int PPW = 32 / NP > 0 ? 32 / NP : 1;
+};
+int pack_ppw(int np) { return 32 / np > 0 ? 32 / np : 1; }
+
+// lanes per cell row in the block-Jacobi kernel (shuffles within power-of-two lane groups), cells per warp
 template <int NP>
 struct ProlongCfg {
   static constexpr int L = NP <= 4 ? 4 : NP <= 8 ? 8 : NP <= 16 ? 16 : 32;  // lanes per cell
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj,
                                                  const double* q, double* const* pbuf, double* x, const double* b,
                                                  double* r0, double* rpart, unsigned* jcnt, PcgState* st,
                                                  double* partials) {
-  constexpr int L = ProlongCfg<NP>::L, PPW = 32 / L;
+  constexpr int L = NP, PPW = PackCfg<NP>::PPW;
   __shared__ double red[RT / 32];
   __shared__ double part[RT / 32][NQ];
   __shared__ double wsum[RT / 32][2];
@@ -387,7 +395,8 @@ __global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj,
   if (J < ncoarse) {
     // packed records (cell, piece | owner << 31): one load per piece, the next one prefetched
     const int ke = cov_ptr[J + 1], kstep = TW * PPW;
-    int k = cov_ptr[J] + gw * PPW + lane / L;
+    const bool act = lane / L < PPW;
+    int k = act ? cov_ptr[J] + gw * PPW + lane / L : ke;
     int2 rec = k < ke ? rrec[k] : make_int2(0, 0);
     for (; k < ke; k += kstep) {
       const int2 nrec = k + kstep < ke ? rrec[k + kstep] : rec;
@@ -756,7 +765,7 @@ __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int
                                                      const double* __restrict__ G, const double* z0, double* z,
                                                      double* const* rbuf, PcgState* st, double* partials,
                                                      double* beta_hist, cudaGraphConditionalHandle h, int use_h) {
-  constexpr int L = ProlongCfg<NP>::L, CPW = ProlongCfg<NP>::CPW;
+  constexpr int L = NP, CPW = PackCfg<NP>::PPW;
   __shared__ double red[PW];
   __shared__ double wd[PW];
   int it = 0;
@@ -772,7 +781,7 @@ __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = (blockIdx.x * PW + w) * CPW + lane / L, a = lane % L;
   double d = 0;
-  if (c < nc && a < NP) {
+  if (lane / L < CPW && c < nc) {
     size_t id = (size_t)c * NP + a;
     double v = z[id];
     for (int k = fov_ptr[c]; k < fov_ptr[c + 1]; ++k) {
@@ -1125,7 +1134,7 @@ void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, doubl
                     cudaGraphConditionalHandle h, int use_handle) {
   (void)r;
   unsigned grid = 1;
-  DISPATCH_P(ctx->p, (grid = (ctx->nc + PW * ProlongCfg<NP_>::CPW - 1) / (PW * ProlongCfg<NP_>::CPW)));
+  DISPATCH_P(ctx->p, (grid = (ctx->nc + PW * PackCfg<NP_>::PPW - 1) / (PW * PackCfg<NP_>::PPW)));
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_prolong<NP_, NQ_><<<grid, PW * 32, 0, s>>>(
                                             mode, ctx->nc, ctx->d_fov_ptr, ctx->d_prec, ctx->d_G,
                                             ctx->d_z0, z, ctx->d_rbuf, st, ctx->d_partials, ctx->d_beta, h,
