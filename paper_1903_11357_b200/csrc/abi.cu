@@ -116,6 +116,14 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     if ((st2 = nd_calibrate(ctx))) return st2;
   }
   if (const char* e = std::getenv("DGAS_UNROLL")) ctx->unroll = std::max(1, std::min(8, std::atoi(e)));
+  {
+    // persistent prolongation: 4 CTAs of 256 threads per SM (64 registers; DGAS_PROLONG_CTAS_PER_SM)
+    int dev = 0, nsm = 148, per = 4;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (const char* e = std::getenv("DGAS_PROLONG_CTAS_PER_SM")) per = std::max(1, std::atoi(e));
+    ctx->prolong_grid = per * nsm;
+  }
   ctx->n_coarse_ctas = ctx->coarse_dense ? (int)std::min<int64_t>(592, std::max<int64_t>(1, ctx->N0 / 32)) : 1;
   {
     // TMA ring of the local-solve CTAs: unit = CC columns of a row-block (about the average row-block

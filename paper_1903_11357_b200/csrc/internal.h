@@ -125,6 +125,8 @@ struct dgas_ctx_s {
   int* d_fov = nullptr;
   int2* d_rrec = nullptr;         // [nov] restriction order (cov): (cell, piece | owner << 31)
   int2* d_prec = nullptr;         // [nov] prolongation order (fov): (piece, coarse element)
+  int4* d_crec = nullptr;         // [nc] per cell: (first piece, its coarse element, #pieces, fov index)
+  int prolong_grid = 1 << 30;     // persistent CTAs of k_prolong
   int* d_ctri_ptr = nullptr;      // coarse J -> fan triangles (piece, t)
   int* d_ctri = nullptr;
   double* d_Cc = nullptr;         // [ncoarse][nq*nq]

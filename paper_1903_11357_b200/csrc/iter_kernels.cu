@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
 // mode 2: PCG iteration (beta = gamma_new / gamma, history, it++, maxit, graph condition).
 #define PW 8
 template <int NP, int NQ>
-__global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int* __restrict__ fov_ptr,
+__global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int4* __restrict__ crec,
                                                      const int2* __restrict__ prec,
                                                      const double* __restrict__ G, const double* z0, double* z,
                                                      double* const* rbuf, PcgState* st, double* partials,
@@ -778,21 +778,44 @@ __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int
     it = st->it;
     r = rbuf[mode == 1 ? 0 : ((it + 1) & 1)];
   }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = (blockIdx.x * PW + w) * CPW + lane / L, a = lane % L;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, a = lane % L;
+  const bool act = lane / L < CPW;
   double d = 0;
-  if (lane / L < CPW && c < nc) {
-    size_t id = (size_t)c * NP + a;
-    double v = z[id];
-    for (int k = fov_ptr[c]; k < fov_ptr[c + 1]; ++k) {
-      const int2 pr = prec[k];  // (piece, coarse element)
-      const int o = pr.x, J = pr.y;
-      const double* Go = G + ((size_t)o * NP + a) * NQ;
+  // persistent grid-stride over groups of CPW cells per warp (few CTAs: few last-block atomics);
+  // the next group's cell record is loaded before the current group is processed
+  const int ngroups = (nc + CPW - 1) / CPW, gstep = gridDim.x * PW;
+  int g = blockIdx.x * PW + w;
+  int c = g * CPW + lane / L;
+  int4 rc = act && c < nc ? crec[c] : make_int4(0, 0, 0, 0);
+  for (; g < ngroups; g += gstep) {
+    const int gn = g + gstep, cn = gn * CPW + lane / L;
+    const int4 rcn = act && gn < ngroups && cn < nc ? crec[cn] : rc;
+    if (act && c < nc) {
+      const size_t id = (size_t)c * NP + a;
+      double v = z[id];
+      const double rv = mode >= 1 ? r[id] : 0.0;
+      // first piece from the cell record (o, J, n, k), further pieces (non-nested) from prec
+      for (int t = 0; t < rc.z; ++t) {
+        int o = rc.x, J = rc.y;
+        if (t > 0) { const int2 pr = prec[rc.w + t]; o = pr.x; J = pr.y; }
+        const double* Go = G + ((size_t)o * NP + a) * NQ;
+        const double* zj = z0 + (size_t)J * NQ;
+        if constexpr (NQ % 2 == 0) {
 #pragma unroll
-      for (int b = 0; b < NQ; ++b) v += Go[b] * z0[(size_t)J * NQ + b];
+          for (int b = 0; b < NQ; b += 2) {
+            const double2 g2 = __ldg(reinterpret_cast<const double2*>(Go + b));
+            v += g2.x * zj[b] + g2.y * zj[b + 1];
+          }
+        } else {
+#pragma unroll
+          for (int b = 0; b < NQ; ++b) v += __ldg(Go + b) * zj[b];
+        }
+      }
+      z[id] = v;
+      d += rv * v;
     }
-    z[id] = v;
-    if (mode >= 1) d = r[id] * v;
+    rc = rcn;
+    c = cn;
   }
   if (mode == 0) return;
   d = warp_sum(d);
@@ -1135,8 +1158,9 @@ void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, doubl
   (void)r;
   unsigned grid = 1;
   DISPATCH_P(ctx->p, (grid = (ctx->nc + PW * PackCfg<NP_>::PPW - 1) / (PW * PackCfg<NP_>::PPW)));
+  grid = std::min<unsigned>(grid, (unsigned)ctx->prolong_grid);
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_prolong<NP_, NQ_><<<grid, PW * 32, 0, s>>>(
-                                            mode, ctx->nc, ctx->d_fov_ptr, ctx->d_prec, ctx->d_G,
+                                            mode, ctx->nc, ctx->d_crec, ctx->d_prec, ctx->d_G,
                                             ctx->d_z0, z, ctx->d_rbuf, st, ctx->d_partials, ctx->d_beta, h,
                                             use_handle))));
 }

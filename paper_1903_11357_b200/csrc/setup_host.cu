@@ -399,8 +399,13 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
         const bool owner = fov[fov_ptr[cell]] == o;
         rrec[k] = make_int2(cell, o | (owner ? (int)0x80000000u : 0));
       }
-    for (int c = 0; c < nc; ++c)
+    std::vector<int4> crec(nc);
+    for (int c = 0; c < nc; ++c) {
       for (int k = fov_ptr[c]; k < fov_ptr[c + 1]; ++k) prec[k] = make_int2(fov[k], ov_coarse[fov[k]]);
+      const int o = fov[fov_ptr[c]];
+      crec[c] = make_int4(o, ov_coarse[o], fov_ptr[c + 1] - fov_ptr[c], fov_ptr[c]);
+    }
+    if ((st = dev_upload(ctx, &ctx->d_crec, crec))) return bail(st, ctx->detail);
     if ((st = dev_upload(ctx, &ctx->d_rrec, rrec))) return bail(st, ctx->detail);
     if ((st = dev_upload(ctx, &ctx->d_prec, prec))) return bail(st, ctx->detail);
   }
@@ -468,7 +473,7 @@ static void free_ctx(dgas_ctx ctx) {
                   ctx->d_p[0], ctx->d_p[1], ctx->d_r0, ctx->d_z0, ctx->d_t1, ctx->d_t2, ctx->d_partials,
                   ctx->d_state, ctx->d_astate, ctx->d_alpha, ctx->d_beta, ctx->d_lanczos, ctx->d_err,
                   ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev, ctx->d_rpart, ctx->d_jcnt,
-                  ctx->d_P, ctx->d_p_off, ctx->d_pus, ctx->d_sub_units, ctx->d_rrec, ctx->d_prec};
+                  ctx->d_P, ctx->d_p_off, ctx->d_pus, ctx->d_sub_units, ctx->d_rrec, ctx->d_prec, ctx->d_crec};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->d_A0b) cudaFree(ctx->d_A0b);
