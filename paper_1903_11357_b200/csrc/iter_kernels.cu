@@ -354,8 +354,11 @@ __global__ void __launch_bounds__(SP_T + 32) k_spmv3(int mode, int nc, int chunk
 // (deterministic). L lanes per piece (ProlongCfg), 32/L pieces per warp step; per-lane accumulation,
 // one warp reduction per coarse dof at the end.
 #define RT 256
+#ifndef RESTRICT_MINB
+#define RESTRICT_MINB 1  // 6 (40 registers, spills): cfg3 +1%, cfg4 -2% (measured)
+#endif
 template <int NP, int NQ>
-__global__ void __launch_bounds__(RT) k_restrict(int mode, int ncoarse, int wpj, int cpj, const int* __restrict__ cov_ptr,
+__global__ void __launch_bounds__(RT, RESTRICT_MINB) k_restrict(int mode, int ncoarse, int wpj, int cpj, const int* __restrict__ cov_ptr,
                                                  const int2* __restrict__ rrec,
                                                  const double* __restrict__ G, const double* r_in, double* const* rbuf,
                                                  const double* q, double* const* pbuf, double* x, const double* b,
