@@ -148,6 +148,8 @@ def main():
     ap.add_argument("--impl", default="dgas", choices=["dgas", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--local-f32", action="store_true",
+                    help="NEXT-4 variant outside the fp64 contract: fp32-stored local factors (never the headline)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0)); world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -157,6 +159,8 @@ def main():
     import numpy as np
     import torch
 
+    if args.local_f32:
+        os.environ["DGAS_PANEL_F32"] = "1"
     from paper_1903_11357_b200 import dgas
     torch.cuda.set_device(local)
     if world > 1:
@@ -280,6 +284,9 @@ def main():
                             + info["launches_per_solve"] * args.steps),
         "clocks": clk.summary(),
     }
+    if args.local_f32:
+        line["variant"] = "NEXT-4: fp32-stored local factors, fp64 arithmetic (outside the fp64 contract; not the headline)"
+        line["dtype"] = "f64 (local factors stored f32)"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cb = cpu_baseline(args.config, P)

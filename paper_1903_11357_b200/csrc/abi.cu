@@ -41,16 +41,18 @@ static int panel_configure(dgas_ctx ctx) {
   size_t target = 8 * 1024;
   if (const char* e = std::getenv("DGAS_PANEL_SLOT_KB")) target = (size_t)std::atoi(e) * 1024;
   const int maxW = ctx->max_urow + ctx->np;
-  const int cc_min = panel_min_cc(ctx->np), cc_max = std::max(cc_min, (maxW + 1) / 2 * 2);
+  if (const char* e = std::getenv("DGAS_PANEL_F32")) ctx->panel_f32 = std::atoi(e) != 0;
+  const int al = panel_al(ctx->panel_f32), esz = ctx->panel_f32 ? 4 : 8;
+  const int cc_min = panel_min_cc(ctx->np, ctx->panel_f32), cc_max = std::max(cc_min, (maxW + al - 1) / al * al);
   ctx->panel_slots = 0;
   if (per_cta > base) {
     const size_t B = per_cta - base;
     int S = 2;
     while (S < 64 && B / (2 * S) >= target) S *= 2;
     for (; S >= 2; S /= 2) {
-      int CC = (int)std::min<size_t>(cc_max, (B / S) / (8 * ctx->np)) / 2 * 2;
+      int CC = (int)std::min<size_t>(cc_max, (B / S) / (esz * ctx->np)) / al * al;
       if (CC < cc_min) continue;
-      const uint32_t sb = (uint32_t)(((((int64_t)CC * ctx->np + 1) / 2 * 2) * 8 + 127) / 128 * 128);
+      const uint32_t sb = (uint32_t)(((((int64_t)CC * ctx->np + al - 1) / al * al) * esz + 127) / 128 * 128);
       while (S < 64 && (size_t)2 * S * sb <= B) S *= 2;  // CC capped at the widest panel: more slots
       ctx->panel_slots = S;
       ctx->panel_slot_bytes = sb;

@@ -191,6 +191,7 @@ struct dgas_ctx_s {
   int* d_sub_units = nullptr;            // [nsub] stream units per subdomain
   int64_t p_total = 0;
   int panel_cc = 2, panel_slots = 2, panel_keep = 1, panel_cps = 1;
+  int panel_f32 = 0;   // NEXT-4 variant (DGAS_PANEL_F32=1): fp32-stored panels, fp64 arithmetic
   // SpMV kernel: 3 = k_spmv3 (fixed slots, consumer groups), 4 = k_spmv_ring (byte ring, warp per cell)
   int spmv_kernel = 3;
   uint32_t sr_ring_bytes = 0;
@@ -294,7 +295,8 @@ size_t spmv_ring_smem(dgas_ctx ctx);
 void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s);
 int panel_supported(int p);
 int pack_ppw(int np);
-int panel_min_cc(int np);
+int panel_min_cc(int np, int f32);
+int panel_al(int f32);
 size_t panel_base_bytes(int max_cells, int np, bool narrow);
 int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first);
 size_t panel_smem_bytes(dgas_ctx ctx);

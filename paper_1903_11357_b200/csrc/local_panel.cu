@@ -38,8 +38,15 @@ struct PanelCfg {
 // of -U_k (column j at DPK + j NP). Stream units: unit 0 = D part + U columns [0, CC0), unit t >= 1
 // = U columns [CC0 + (t-1) CC, ...), CC and CC0 = CC - E even so every unit starts 16-byte aligned
 // and fits a CC-column slot.
-__host__ __device__ constexpr int panel_dpk(int np) { return (np * (np + 1) / 2 + 1) & ~1; }
-__host__ __device__ constexpr int panel_e(int np) { return (((panel_dpk(np) + np - 1) / np) + 1) & ~1; }
+// TS = storage type of the panels: double (the fp64 contract) or float (NEXT-4 variant: fp32-stored
+// factors, fp64 arithmetic). A = elements per 16 bytes; every count below is a multiple of A.
+template <typename TS> __host__ __device__ constexpr int panel_al() { return 16 / (int)sizeof(TS); }
+template <typename TS> __host__ __device__ constexpr int panel_dpk(int np) {
+  return (np * (np + 1) / 2 + panel_al<TS>() - 1) / panel_al<TS>() * panel_al<TS>();
+}
+template <typename TS> __host__ __device__ constexpr int panel_e(int np) {
+  return ((panel_dpk<TS>(np) + np - 1) / np + panel_al<TS>() - 1) / panel_al<TS>() * panel_al<TS>();
+}
 __host__ __device__ constexpr int panel_dcol(int np, int c) { return c * np - c * (c - 1) / 2; }
 __host__ __device__ inline int panel_units(int wu, int cc, int cc0) { return 1 + (wu > cc0 ? (wu - cc0 + cc - 1) / cc : 0); }
 
@@ -59,10 +66,10 @@ struct PanelLayout {
 };
 
 // NARROW (7 CTAs/SM): at most 48 registers so a 256-thread coarse-solve CTA still fits beside them
-template <int NP, bool NARROW>
+template <int NP, bool NARROW, typename TS>
 __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) k_local_panel(
     int mode, const int* __restrict__ sub_ptr, const int* __restrict__ first, const int* __restrict__ pus,
-    const int* __restrict__ sub_units, const int64_t* __restrict__ p_off, const double* __restrict__ P,
+    const int* __restrict__ sub_units, const int64_t* __restrict__ p_off, const TS* __restrict__ P,
     const double* r_in, double* const* rbuf, double* z, const PcgState* st, int S, uint32_t slot_bytes, int CC,
     int max_cells, int keep_fwd) {
   using C = PanelCfg<NP, NARROW>;
@@ -102,14 +109,14 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
     if (tid != T) return;
     const uint64_t pol_first = l2_evict_first(), pol_last = keep_fwd ? l2_evict_last() : pol_first;
     uint64_t epar = 0;  // parity of the next empty-barrier phase per slot
-    constexpr int DPK = panel_dpk(NP);
-    const int CC0 = CC - panel_e(NP);
+    constexpr int DPK = panel_dpk<TS>(NP), AL = panel_al<TS>();
+    const int CC0 = CC - panel_e<TS>(NP);
     auto issue = [&](int u, int k, uint64_t pol) {
       const int WU = (k - fk_s[k]) * NP, t = u - us_s[k];
       int64_t off, n;
       if (t == 0) { off = 0; n = DPK + (int64_t)min(WU, CC0) * NP; }
       else { const int j0 = CC0 + (t - 1) * CC; off = DPK + (int64_t)j0 * NP; n = (int64_t)(min(WU, j0 + CC) - j0) * NP; }
-      const uint32_t nbytes = (uint32_t)(((n + 1) & ~1LL) * 8);
+      const uint32_t nbytes = (uint32_t)((n + AL - 1) / AL * AL * (int64_t)sizeof(TS));
       bulk_load(ring + (size_t)(u & SM1) * slot_bytes, P + po_s[k] + off, nbytes, &full[u & SM1], pol);
     };
     int k = 0;
@@ -131,8 +138,8 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
     return;
   }
   // ---------------- consumers
-  constexpr int DPK = panel_dpk(NP);
-  const int CC0 = CC - panel_e(NP);
+  constexpr int DPK = panel_dpk<TS>(NP);
+  const int CC0 = CC - panel_e<TS>(NP);
   const int lane = tid & 31;
   uint64_t fph = 0;  // parity of the next full-barrier phase per slot
   const double* rs = r + (size_t)s0 * NP;
@@ -162,15 +169,15 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
         const int sl = u & SM1, t = u - u0;
         mbar_wait(&full[sl], (uint32_t)((fph >> sl) & 1));
         fph ^= 1ull << sl;
-        const double* Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+        const TS* Ps = reinterpret_cast<const TS*>(ring + (size_t)sl * slot_bytes);
         if (a < NP) {
           int j0, j1;
-          const double* Pu;  // U column j at Pu[j NP]
+          const TS* Pu;  // U column j at Pu[j NP]
           if (t == 0) {
 #pragma unroll
             for (int t = 0; t < RN; ++t) {  // D_k r_k, lower triangle
               const int c = q + LPR * t;
-              if (c < NP && c <= a) v1 += Ps[panel_dcol(NP, c) + a - c] * rk[t];
+              if (c < NP && c <= a) v1 += (double)Ps[panel_dcol(NP, c) + a - c] * rk[t];
             }
             if constexpr (NARROW) {  // prefetch r_{k+1}
 #pragma unroll
@@ -183,10 +190,10 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
           }
           int j = j0 + q;
           for (; j + LPR < j1; j += 2 * LPR) {
-            v0 += Pu[j * NP] * yb[j];
-            v1 += Pu[(j + LPR) * NP] * yb[j + LPR];
+            v0 += (double)Pu[j * NP] * yb[j];
+            v1 += (double)Pu[(j + LPR) * NP] * yb[j + LPR];
           }
-          if (j < j1) v0 += Pu[j * NP] * yb[j];
+          if (j < j1) v0 += (double)Pu[j * NP] * yb[j];
         }
         __syncwarp();
         // the ring-resident tail (u >= U - S) is released only once, by the backward sweep
@@ -225,11 +232,11 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
           mbar_wait(&full[sl], (uint32_t)((fph >> sl) & 1));
           fph ^= 1ull << sl;
         }
-        const double* Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+        const TS* Ps = reinterpret_cast<const TS*>(ring + (size_t)sl * slot_bytes);
         // virtual columns x of this unit: unit 0 has the NP columns of D_k first (z_k = D_k^T u_k)
         const int xoff = t == 0 ? NP : 0;
         const int j0 = t == 0 ? 0 : CC0 + (t - 1) * CC, j1 = t == 0 ? min(WU, CC0) : min(WU, j0 + CC);
-        const double* Pu = t == 0 ? Ps + DPK : Ps - j0 * NP;  // U column j at Pu[j NP]
+        const TS* Pu = t == 0 ? Ps + DPK : Ps - j0 * NP;  // U column j at Pu[j NP]
         const int nx = xoff + j1 - j0;
         // every lane of a warp runs the same trip count (warp-uniform bound), so the pair shuffle is
         // a full-warp one
@@ -238,15 +245,15 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
           // D column x holds rows x..NP-1 (D_k[a][x] at col[a]); U column j holds all rows. One
           // branch-free path for both (no divergence between the D and U lanes of warp 0)
           const bool isd = x < xoff;
-          const double* col = isd ? Ps + panel_dcol(NP, x) - x : Pu + j * NP;
+          const TS* col = isd ? Ps + panel_dcol(NP, x) - x : Pu + j * NP;
           const int lo = isd ? x : 0, hi = x < nx ? NP : 0;
           double w0 = 0, w1 = 0;
 #pragma unroll
           for (int i = 0; i + 1 < H; i += 2) {
-            if (a0 + i < hi && a0 + i >= lo) w0 += col[a0 + i] * uk(i);
-            if (a0 + i + 1 < hi && a0 + i + 1 >= lo) w1 += col[a0 + i + 1] * uk(i + 1);
+            if (a0 + i < hi && a0 + i >= lo) w0 += (double)col[a0 + i] * uk(i);
+            if (a0 + i + 1 < hi && a0 + i + 1 >= lo) w1 += (double)col[a0 + i + 1] * uk(i + 1);
           }
-          if ((H & 1) && a0 + H - 1 < hi && a0 + H - 1 >= lo) w0 += col[a0 + H - 1] * uk(H - 1);
+          if ((H & 1) && a0 + H - 1 < hi && a0 + H - 1 >= lo) w0 += (double)col[a0 + H - 1] * uk(H - 1);
           double w = w0 + w1;
           w += __shfl_xor_sync(0xffffffffu, w, 1);
           if (half == 0 && x < nx) {
@@ -264,21 +271,22 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
 
 // P_k = [D_k packed lower triangle | -U_k] at p_off[c] (layout above), D_k from the row-major
 // lower triangle of Dinv.
+template <typename TS>
 __global__ void k_build_panels(int np, int nc, const int* sub_ptr_of_cell, const int* first,
                                const int64_t* u_off, const double* U, const double* Dinv, const int64_t* p_off,
-                               double* P) {
+                               TS* P) {
   const int c = blockIdx.x;
   if (c >= nc) return;
-  const int k = c - sub_ptr_of_cell[c], WU = (k - first[c]) * np, dpk = panel_dpk(np);
-  double* Pc = P + p_off[c];
+  const int k = c - sub_ptr_of_cell[c], WU = (k - first[c]) * np, dpk = panel_dpk<TS>(np);
+  TS* Pc = P + p_off[c];
   const double* Uc = U + u_off[c];
   const double* Dc = Dinv + (size_t)c * np * np;
   for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
     const int a = e / np, cc = e % np;
-    if (cc <= a) Pc[panel_dcol(np, cc) + a - cc] = Dc[a * np + cc];
+    if (cc <= a) Pc[panel_dcol(np, cc) + a - cc] = (TS)Dc[a * np + cc];
   }
-  if (threadIdx.x == 0 && dpk > np * (np + 1) / 2) Pc[dpk - 1] = 0.0;
-  for (int e = threadIdx.x; e < WU * np; e += blockDim.x) Pc[dpk + e] = -Uc[e];
+  for (int e = np * (np + 1) / 2 + threadIdx.x; e < dpk; e += blockDim.x) Pc[e] = (TS)0;
+  for (int e = threadIdx.x; e < WU * np; e += blockDim.x) Pc[dpk + e] = (TS)(-Uc[e]);
 }
 
 #define DISPATCH_P15(P, ...)                                \
@@ -287,15 +295,14 @@ __global__ void k_build_panels(int np, int nc, const int* sub_ptr_of_cell, const
     case 2: { constexpr int NP_ = 6; __VA_ARGS__; } break;  \
     case 3: { constexpr int NP_ = 10; __VA_ARGS__; } break; \
     case 4: { constexpr int NP_ = 15; __VA_ARGS__; } break; \
-    case 5: { constexpr int NP_ = 21; __VA_ARGS__; } break; \
-    case 6: { constexpr int NP_ = 28; __VA_ARGS__; } break; \
   }
 
-// p = 5, 6 compile (n_p = 21, 28) but are slower than the envelope kernel (config 5 p = q = 6:
-// 1228 vs 1440 PCG it/s, measured), so the panel kernel is used for p <= 4 only
+// p = 5, 6 (n_p = 21, 28) were measured slower than the envelope kernel (config 5 p = q = 6: 1228 vs
+// 1440 PCG it/s), so the panel kernel is built and used for p <= 4 only
 int panel_supported(int p) { return p >= 1 && p <= 4; }
 
-int panel_min_cc(int np) { return panel_e(np) + 2; }
+int panel_al(int f32) { return f32 ? panel_al<float>() : panel_al<double>(); }
+int panel_min_cc(int np, int f32) { return f32 ? panel_e<float>(np) + 4 : panel_e<double>(np) + 2; }
 
 // 128 consumer threads when more than 3 CTAs share an SM (registers), else 256
 static bool panel_narrow(dgas_ctx ctx) { return ctx->panel_cps > 3; }
@@ -303,8 +310,10 @@ static bool panel_narrow(dgas_ctx ctx) { return ctx->panel_cps > 3; }
 size_t panel_base_bytes(int max_cells, int np, bool narrow) { return PanelLayout(max_cells, np, !narrow).off_ring; }
 
 // host: panel offsets, per-cell unit starts, per-subdomain unit counts; device: the panels
-int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first) {
-  const int nc = ctx->nc, np = ctx->np, CC = ctx->panel_cc, CC0 = CC - panel_e(np), dpk = panel_dpk(np);
+template <typename TS>
+static int panel_setup_t(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first) {
+  const int nc = ctx->nc, np = ctx->np, CC = ctx->panel_cc, CC0 = CC - panel_e<TS>(np), dpk = panel_dpk<TS>(np);
+  constexpr int AL = panel_al<TS>();
   std::vector<int64_t> p_off(nc + 1, 0);
   std::vector<int> pus(nc), sub_units(ctx->nsub), sub_of(nc);
   for (int s = 0; s < ctx->nsub; ++s) {
@@ -314,7 +323,7 @@ int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector
       sub_of[c] = sub_ptr[s];
       pus[c] = acc;
       acc += panel_units(WU, CC, CC0);
-      p_off[c + 1] = p_off[c] + (dpk + (int64_t)np * WU + 1) / 2 * 2;  // 16-byte panels for TMA
+      p_off[c + 1] = p_off[c] + (dpk + (int64_t)np * WU + AL - 1) / AL * AL;  // 16-byte panels for TMA
     }
     sub_units[s] = acc;
   }
@@ -325,13 +334,17 @@ int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector
   if ((st = dev_upload(ctx, &ctx->d_sub_units, sub_units))) return st;
   int* d_sub_of = nullptr;
   if ((st = dev_upload(ctx, &d_sub_of, sub_of))) return st;
-  if ((st = dev_alloc(ctx, &ctx->d_P, (size_t)p_off[nc] + 32))) { cudaFree(d_sub_of); return st; }
-  k_build_panels<<<nc, 128, 0, ctx->stream>>>(np, nc, d_sub_of, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv,
-                                              ctx->d_p_off, ctx->d_P);
+  if ((st = dev_alloc(ctx, &ctx->d_P, ((size_t)p_off[nc] * sizeof(TS) + 7) / 8 + 32))) { cudaFree(d_sub_of); return st; }
+  k_build_panels<TS><<<nc, 128, 0, ctx->stream>>>(np, nc, d_sub_of, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv,
+                                                  ctx->d_p_off, reinterpret_cast<TS*>(ctx->d_P));
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   cudaFree(d_sub_of);
   if (e != cudaSuccess) { ctx->detail = std::string("panel build: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
   return 0;
+}
+
+int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first) {
+  return ctx->panel_f32 ? panel_setup_t<float>(ctx, sub_ptr, first) : panel_setup_t<double>(ctx, sub_ptr, first);
 }
 
 size_t panel_smem_bytes(dgas_ctx ctx) {
@@ -355,22 +368,25 @@ int panel_set_smem(dgas_ctx ctx) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
   };
-  DISPATCH_P15(ctx->p, (raise((const void*)k_local_panel<NP_, true>), raise((const void*)k_local_panel<NP_, false>)));
+  DISPATCH_P15(ctx->p, (raise((const void*)k_local_panel<NP_, true, double>),
+                        raise((const void*)k_local_panel<NP_, false, double>),
+                        raise((const void*)k_local_panel<NP_, true, float>),
+                        raise((const void*)k_local_panel<NP_, false, float>)));
   if (e != cudaSuccess) { ctx->detail = std::string("panel smem: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
   return 0;
 }
 
 void launch_local_panel(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
   const size_t smem = panel_smem_bytes(ctx);
-#define PANEL_LAUNCH(NAR)                                                                                          \
-  DISPATCH_P15(ctx->p, (k_local_panel<NP_, NAR><<<ctx->nsub, PanelCfg<NP_, NAR>::T + 32, smem, s>>>(               \
-                           mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_pus, ctx->d_sub_units, ctx->d_p_off, ctx->d_P, \
-                           r, ctx->d_rbuf, z, st, ctx->panel_slots, ctx->panel_slot_bytes, ctx->panel_cc,         \
-                           ctx->max_sub_cells, ctx->panel_keep)))
-  if (panel_narrow(ctx)) {
-    PANEL_LAUNCH(true);
+#define PANEL_LAUNCH(NAR, TS)                                                                                      \
+  DISPATCH_P15(ctx->p, (k_local_panel<NP_, NAR, TS><<<ctx->nsub, PanelCfg<NP_, NAR>::T + 32, smem, s>>>(           \
+                           mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_pus, ctx->d_sub_units, ctx->d_p_off,         \
+                           reinterpret_cast<const TS*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->panel_slots,        \
+                           ctx->panel_slot_bytes, ctx->panel_cc, ctx->max_sub_cells, ctx->panel_keep)))
+  if (ctx->panel_f32) {
+    if (panel_narrow(ctx)) { PANEL_LAUNCH(true, float); } else { PANEL_LAUNCH(false, float); }
   } else {
-    PANEL_LAUNCH(false);
+    if (panel_narrow(ctx)) { PANEL_LAUNCH(true, double); } else { PANEL_LAUNCH(false, double); }
   }
 #undef PANEL_LAUNCH
 }

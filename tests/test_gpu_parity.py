@@ -444,3 +444,29 @@ def test_spmv_kernel_variants(monkeypatch, name, env):
     x, iters, cond, st = S.pcg(_dev(b))
     assert st == 0 and abs(iters - ref["iters"]) <= 2
     S.close()
+
+
+@pytest.mark.parametrize("name", ["cfg4s", "cfg3s", "cfg2s"])
+def test_panel_f32_variant(monkeypatch, name):
+    """SURVEY §8(f) NEXT-4, outside the fp64 contract: local factors stored in fp32 (fp64 arithmetic).
+    The apply is then an fp32-rounded exact solve (relative error ~1e-7, bounded here by 1e-5), and
+    PCG, whose residuals stay fp64, still reaches rtol 1e-8 with the oracle's solution (1e-7) and
+    about its iteration count."""
+    monkeypatch.setenv("DGAS_PANEL_F32", "1")
+    P = CASES[name]()
+    S = _solver(P)
+    assert S.info["local_kernel"] == 2
+    o = O.Oracle(P)
+    o.setup_schwarz()
+    r = g.normal(500, S.N)
+    z = S.apply(_dev(r)).cpu().numpy()
+    zr = o.apply(r)
+    rel = np.linalg.norm(z - zr) / np.linalg.norm(zr)
+    assert 1e-12 < rel <= 1e-5, rel  # really fp32-stored, and still a close preconditioner
+    b = o.rhs()
+    ref = o.pcg(b, rtol=1e-8)
+    x, iters, cond, st = S.pcg(_dev(b))
+    assert st == 0 and abs(iters - ref["iters"]) <= max(2, ref["iters"] // 20)
+    xh = x.cpu().numpy()
+    assert np.linalg.norm(xh - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+    S.close()
