@@ -24,13 +24,19 @@
 #include "internal.h"
 #include "tma.cuh"
 
+#ifndef PANEL_NARROW_TPC
+#define PANEL_NARROW_TPC 1
+#endif
 template <int NP, bool NARROW = false>
 struct PanelCfg {
   static constexpr int T = (NP > 4 && !NARROW) ? 256 : 128;       // consumer threads
   static constexpr int ROWS = NP > 16 ? 32 : NP > 8 ? 16 : (NP > 4 ? 8 : 4);  // row slots in the forward step
   static constexpr int LPR = T / ROWS;                            // lanes per row (4 .. 32)
   static constexpr int NW = T / 32;
-  static constexpr int H = (NP + 1) / 2;                          // rows per half in the backward step
+  // backward step: TPC threads per column (rows split into TPC slices of H): 2 in wide CTAs (more
+  // columns per pass than there are), 1 in narrow CTAs (one pass over ~NP cols per 128 threads)
+  static constexpr int TPC = NARROW ? PANEL_NARROW_TPC : 2;
+  static constexpr int H = (NP + TPC - 1) / TPC;
 };
 
 // Panel layout of cell k (doubles, 16-byte aligned): D_k lower triangle packed column by column
@@ -73,7 +79,7 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
     const double* r_in, double* const* rbuf, double* z, const PcgState* st, int S, uint32_t slot_bytes, int CC,
     int max_cells, int keep_fwd) {
   using C = PanelCfg<NP, NARROW>;
-  constexpr int T = C::T, LPR = C::LPR, NW = C::NW, H = C::H;
+  constexpr int T = C::T, LPR = C::LPR, NW = C::NW, H = C::H, TPC = C::TPC;
   extern __shared__ __align__(128) double sm[];
   const double* r = r_in;
   if (mode >= 1) {
@@ -206,9 +212,9 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
       named_sync(1, T);
     }
   }
-  // backward: u_k = Y_k is final; v = P_k^T u_k, thread pair (j, half) per column, rows split in halves
+  // backward: u_k = Y_k is final; v = P_k^T u_k, TPC threads per column, rows split in slices of H
   {
-    const int half = tid & 1, a0 = half * H;
+    const int half = tid % TPC, a0 = half * H;
     double* zs = z + (size_t)s0 * NP;
     for (int k = m - 1; k >= 0; --k) {
       const int u0 = us_s[k], u1 = us_s[k + 1], fk = fk_s[k];
@@ -240,8 +246,8 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
         const int nx = xoff + j1 - j0;
         // every lane of a warp runs the same trip count (warp-uniform bound), so the pair shuffle is
         // a full-warp one
-        for (int xb = (tid >> 5) * 16; xb < nx; xb += T / 2) {
-          const int x = xb + (lane >> 1), j = j0 + x - xoff;
+        for (int xb = (tid >> 5) * (32 / TPC); xb < nx; xb += T / TPC) {
+          const int x = xb + lane / TPC, j = j0 + x - xoff;
           // D column x holds rows x..NP-1 (D_k[a][x] at col[a]); U column j holds all rows. One
           // branch-free path for both (no divergence between the D and U lanes of warp 0)
           const bool isd = x < xoff;
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
           }
           if ((H & 1) && a0 + H - 1 < hi && a0 + H - 1 >= lo) w0 += (double)col[a0 + H - 1] * uk(H - 1);
           double w = w0 + w1;
-          w += __shfl_xor_sync(0xffffffffu, w, 1);
+          if constexpr (TPC == 2) w += __shfl_xor_sync(0xffffffffu, w, 1);
           if (half == 0 && x < nx) {
             if (x < xoff) zs[k * NP + x] = w;
             else yb[j] += w;
