@@ -27,15 +27,20 @@
 #ifndef PANEL_NARROW_TPC
 #define PANEL_NARROW_TPC 1
 #endif
+#ifndef PANEL_WIDE_TPC
+#define PANEL_WIDE_TPC(NP) ((NP) > 10 ? 2 : 1)
+#endif
 template <int NP, bool NARROW = false>
 struct PanelCfg {
   static constexpr int T = (NP > 4 && !NARROW) ? 256 : 128;       // consumer threads
   static constexpr int ROWS = NP > 16 ? 32 : NP > 8 ? 16 : (NP > 4 ? 8 : 4);  // row slots in the forward step
   static constexpr int LPR = T / ROWS;                            // lanes per row (4 .. 32)
   static constexpr int NW = T / 32;
-  // backward step: TPC threads per column (rows split into TPC slices of H): 2 in wide CTAs (more
-  // columns per pass than there are), 1 in narrow CTAs (one pass over ~NP cols per 128 threads)
-  static constexpr int TPC = NARROW ? PANEL_NARROW_TPC : 2;
+  // backward step: TPC threads per column (rows split into TPC slices of H). Narrow CTAs (HBM-bound):
+  // 1 (no pair shuffle, fewer passes; cfg4 local 0.303 -> 0.289 ms). Wide CTAs (latency-bound): 1 up
+  // to n_p = 10 (cfg1/2, cfg5 p1-p3 +1-3%), 2 at n_p = 15 (a 15-long dot per thread is too long a
+  // chain: cfg5 p4q4 -8% with 1)
+  static constexpr int TPC = NARROW ? PANEL_NARROW_TPC : PANEL_WIDE_TPC(NP);
   static constexpr int H = (NP + TPC - 1) / TPC;
 };
 
