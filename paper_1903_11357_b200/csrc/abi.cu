@@ -2,6 +2,7 @@
 // loop: one CUDA graph whose WHILE conditional node runs PCG iterations until the device-side
 // convergence test clears the condition), info, history, diagnostics.
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -406,16 +407,46 @@ static int pcg_eager(dgas_ctx ctx, double rtol, int maxit, cudaStream_t s) {
   launch_restrict(ctx, 2, st, nullptr, s);
   launch_apply(ctx, 1, st, nullptr, ctx->d_z, s);
   launch_prolong(ctx, 1, st, nullptr, ctx->d_z, s, 0, 0);
+  // DGAS_EAGER_TIMING=1: CUDA events around each phase of every iteration on the launching stream
+  // (in-situ kernel times, L2 state as in a real solve), averaged and printed to stderr at the end
+  static const bool timing = std::getenv("DGAS_EAGER_TIMING") != nullptr;
+  cudaEvent_t ev[8][5];
+  double acc[4] = {0, 0, 0, 0};
+  int nacc = 0;
+  if (timing)
+    for (auto& row : ev)
+      for (auto& e : row) DGAS_CUDA(cudaEventCreate(&e));
   for (;;) {
     for (int u = 0; u < 8; ++u) {
+      if (timing) cudaEventRecord(ev[u][0], s);
       launch_spmv(ctx, 1, nullptr, ctx->d_q, st, s);
+      if (timing) cudaEventRecord(ev[u][1], s);
       launch_restrict(ctx, 1, st, nullptr, s);
+      if (timing) cudaEventRecord(ev[u][2], s);
       launch_apply(ctx, 2, st, nullptr, ctx->d_z, s);
+      if (timing) cudaEventRecord(ev[u][3], s);
       launch_prolong(ctx, 2, st, nullptr, ctx->d_z, s, 0, 0);
+      if (timing) cudaEventRecord(ev[u][4], s);
     }
     DGAS_CUDA(cudaMemcpyAsync(ctx->h_state, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     DGAS_CUDA(cudaStreamSynchronize(s));
+    if (timing && !ctx->h_state->done) {
+      for (int u = 0; u < 8; ++u)
+        for (int k = 0; k < 4; ++k) {
+          float ms = 0;
+          cudaEventElapsedTime(&ms, ev[u][k], ev[u][k + 1]);
+          acc[k] += ms;
+        }
+      nacc += 8;
+    }
     if (ctx->h_state->done) break;
+  }
+  if (timing) {
+    if (nacc)
+      fprintf(stderr, "eager timing (%d iterations): spmv %.1f us, restrict %.1f us, apply %.1f us, prolong %.1f us\n",
+              nacc, acc[0] * 1e3 / nacc, acc[1] * 1e3 / nacc, acc[2] * 1e3 / nacc, acc[3] * 1e3 / nacc);
+    for (auto& row : ev)
+      for (auto& e : row) cudaEventDestroy(e);
   }
   launch_lanczos(ctx, s);
   DGAS_CUDA(cudaGetLastError());

@@ -126,13 +126,30 @@ def test_apply_parity(name):
         assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr), seed
 
 
-def _oracle_spread(o, b, ref, rtol=1e-8):
-    """Iteration counts of the oracle itself under 1e-13 relative perturbations of b: when the
-    residual plateaus near rtol the stopping iteration is not unique under rounding (R22)."""
+def _oracle_spread(o, b, ref, rtol=1e-8, P=None):
+    """Iteration counts of the oracle itself under last-bit perturbations: 1e-13 relative noise on b
+    and (P given) 1-ulp noise on G, i.e. two correct assemblies of the coarse operator (DESIGN.md
+    R30). When the residual plateaus near rtol the stopping iteration is not unique under rounding
+    (R22); measured on cfg4s (rho jumps 1e8): b probes 208-209, G probes 206-208, GPU 205-209 with an
+    apply that agrees to 1.4e-13."""
     its = [ref["iters"]]
     for s in range(3):
         its.append(o.pcg(b * (1 + 1e-13 * g.normal(500 + s, b.shape[0])), rtol=rtol)["iters"])
+    if P is not None:
+        for seed in (1, 2, 3):
+            o2 = O.Oracle(P)
+            o2.set_perturb(2.2e-16, seed)
+            o2.setup_schwarz()
+            its.append(o2.pcg(b, rtol=rtol)["iters"])
     return min(its), max(its)
+
+
+def _iters_ok(o, b, ref, iters, P):
+    """north_star: within 2 of the oracle; else inside the oracle's own rounding spread +- 2 (R22)."""
+    if abs(iters - ref["iters"]) <= 2:
+        return True
+    lo, hi = _oracle_spread(o, b, ref, P=P)
+    return lo - 2 <= iters <= hi + 2
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -145,7 +162,7 @@ def test_pcg_parity(name):
     a, bet = S.history()
     assert st == 0 and ref["status"] == 0
     if abs(iters - ref["iters"]) > 2:
-        lo, hi = _oracle_spread(o, b, ref)
+        lo, hi = _oracle_spread(o, b, ref, P=P)
         assert lo - 2 <= iters <= hi + 2, (iters, ref["iters"], lo, hi)
     if iters == ref["iters"]:
         assert np.linalg.norm(x - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
@@ -315,8 +332,8 @@ def test_nested_dissection_coarse_path(monkeypatch, name, leaf):
     ref = o.pcg(b, rtol=1e-8)
     x, iters, cond, st = S.pcg(_dev(b), rtol=1e-8)
     assert st == 0
-    if abs(iters - ref["iters"]) > 2:  # R22: the oracle's own spread under 1e-13 perturbations of b
-        lo, hi = _oracle_spread(o, b, ref)
+    if abs(iters - ref["iters"]) > 2:  # R22: the oracle's own spread under last-bit perturbations
+        lo, hi = _oracle_spread(o, b, ref, P=P)
         assert lo - 2 <= iters <= hi + 2, (iters, ref["iters"], lo, hi)
 
 
@@ -410,7 +427,7 @@ def test_local_kernel_variants(monkeypatch, name, env, kernel):
     b = o.rhs()
     ref = o.pcg(b, rtol=1e-8)
     x, iters, cond, st = S.pcg(_dev(b))
-    assert st == 0 and abs(iters - ref["iters"]) <= 2
+    assert st == 0 and _iters_ok(o, b, ref, iters, P), (iters, ref["iters"])
     S.close()
 
 
@@ -442,7 +459,7 @@ def test_spmv_kernel_variants(monkeypatch, name, env):
     b = o.rhs()
     ref = o.pcg(b, rtol=1e-8)
     x, iters, cond, st = S.pcg(_dev(b))
-    assert st == 0 and abs(iters - ref["iters"]) <= 2
+    assert st == 0 and _iters_ok(o, b, ref, iters, P), (iters, ref["iters"])
     S.close()
 
 
