@@ -120,6 +120,46 @@ static int finish_setup_buffers(dgas_ctx ctx) {
   }
   if (const char* e = std::getenv("DGAS_UNROLL")) ctx->unroll = std::max(1, std::min(8, std::atoi(e)));
   {
+    // chunked restriction: pieces of each coarse element in chunks of <= 4 warp steps (32/n_p pieces
+    // per step); persistent grid of 4 x 256-thread CTAs per SM
+    const char* e = std::getenv("DGAS_RESTRICT");
+    if (!(e && std::atoi(e) == 1)) {
+      std::vector<int> cov_ptr(ctx->ncoarse + 1);
+      DGAS_CUDA(cudaMemcpy(cov_ptr.data(), ctx->d_cov_ptr, (ctx->ncoarse + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+      const int per = 4 * pack_ppw(ctx->np);
+      std::vector<int4> ch;
+      std::vector<int> jp(ctx->ncoarse + 1, 0);
+      for (int J = 0; J < ctx->ncoarse; ++J) {
+        // at most 64 chunks per coarse element (its last warp adds the chunk partials serially; the
+        // paper regime has thousands of pieces per element)
+        const int npc = cov_ptr[J + 1] - cov_ptr[J];
+        const int ppw = pack_ppw(ctx->np);
+        const int cs = std::max(per, (npc + 63) / 64 + ppw - 1) / ppw * ppw;
+        int t = 0;
+        for (int k = cov_ptr[J]; k < cov_ptr[J + 1]; k += cs, ++t)
+          ch.push_back(make_int4(J, k, std::min(cov_ptr[J + 1], k + cs), t));
+        jp[J + 1] = (int)ch.size();
+      }
+      ctx->nchunk = (int)ch.size();
+      DGAS_CUDA(cudaMalloc((void**)&ctx->d_chunks, std::max<size_t>(1, ch.size()) * sizeof(int4)));
+      DGAS_CUDA(cudaMemcpy(ctx->d_chunks, ch.data(), ch.size() * sizeof(int4), cudaMemcpyHostToDevice));
+      DGAS_CUDA(cudaMalloc((void**)&ctx->d_jchunk_ptr, jp.size() * sizeof(int)));
+      DGAS_CUDA(cudaMemcpy(ctx->d_jchunk_ptr, jp.data(), jp.size() * sizeof(int), cudaMemcpyHostToDevice));
+      DGAS_CUDA(cudaMalloc((void**)&ctx->d_cpart, std::max<size_t>(1, ch.size()) * ctx->nq * sizeof(double)));
+      DGAS_CUDA(cudaMalloc((void**)&ctx->d_jcnt2, ctx->ncoarse * sizeof(unsigned)));
+      DGAS_CUDA(cudaMemset(ctx->d_jcnt2, 0, ctx->ncoarse * sizeof(unsigned)));
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      int per_sm = 4;
+      if (const char* e2 = std::getenv("DGAS_RESTRICT_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e2));
+      const int warps = restrict_chunk_threads() / 32;
+      ctx->rc_grid = std::max(1, std::min(per_sm * nsm, (ctx->nchunk + warps - 1) / warps));
+      // the last-CTA sum of r.r reads one partial per CTA: within the partials buffer
+      ctx->rc_grid = std::min(ctx->rc_grid, std::max(1, ctx->partial_cap / 2 - 1));
+    }
+  }
+  {
     // persistent prolongation: 4 CTAs of 256 threads per SM (64 registers; DGAS_PROLONG_CTAS_PER_SM)
     int dev = 0, nsm = 148, per = 4;
     cudaGetDevice(&dev);

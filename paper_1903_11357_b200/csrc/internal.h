@@ -127,6 +127,12 @@ struct dgas_ctx_s {
   int2* d_prec = nullptr;         // [nov] prolongation order (fov): (piece, coarse element)
   int4* d_crec = nullptr;         // [nc] per cell: (first piece, its coarse element, #pieces, fov index)
   int prolong_grid = 1 << 30;     // persistent CTAs of k_prolong
+  // chunked restriction (k_restrict_chunk; DGAS_RESTRICT=1 selects k_restrict)
+  int4* d_chunks = nullptr;       // [nchunk] (J, first piece, end piece, chunk index within J)
+  int* d_jchunk_ptr = nullptr;    // [ncoarse+1] chunks of J
+  double* d_cpart = nullptr;      // [nchunk][nq] chunk partial sums
+  unsigned* d_jcnt2 = nullptr;    // [ncoarse] chunk arrival counters
+  int nchunk = 0, rc_grid = 0;
   int* d_ctri_ptr = nullptr;      // coarse J -> fan triangles (piece, t)
   int* d_ctri = nullptr;
   double* d_Cc = nullptr;         // [ncoarse][nq*nq]
@@ -295,6 +301,7 @@ size_t spmv_ring_smem(dgas_ctx ctx);
 void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s);
 int panel_supported(int p);
 int pack_ppw(int np);
+int restrict_chunk_threads();
 int panel_min_cc(int np, int f32);
 int panel_al(int f32);
 size_t panel_base_bytes(int max_cells, int np, bool narrow);

@@ -60,6 +60,7 @@ struct PackCfg {
   static constexpr int PPW = 32 / NP > 0 ? 32 / NP : 1;
 };
 int pack_ppw(int np) { return 32 / np > 0 ? 32 / np : 1; }
+int restrict_chunk_threads() { return 256; }  // RC_T
 
 // lanes per cell row in the block-Jacobi kernel (shuffles within power-of-two lane groups), cells per warp
 template <int NP>
@@ -477,6 +478,137 @@ __global__ void __launch_bounds__(RT, RESTRICT_MINB) k_restrict(int mode, int nc
     for (int k = 0; k < RT / 32; ++k) { mine[0] += wsum[k][0]; mine[1] += wsum[k][1]; }
   double tot[2];
   if (last_block<RT, 2>(mine, partials, &st->cnt[1], tot, red)) {
+    if (threadIdx.x == 0) {
+      st->rr = tot[0];
+      if (mode == 2) { st->bb = tot[1]; st->rtol2_bb *= tot[1]; }
+      if (!isfinite(tot[0])) { st->done = 1; st->status = DGAS_E_BREAKDOWN; }
+      else if (tot[0] <= st->rtol2_bb) { st->done = 1; st->status = DGAS_OK; if (mode == 1) st->it = it + 1; }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ restriction, chunked (default)
+// Same arithmetic as k_restrict, organised for latency: the pieces of every coarse element J are cut
+// into chunks of at most PPW * RC_STEPS pieces (host table: J, first, last piece); persistent warps
+// take chunks round-robin and work independently (no CTA barrier until the end). A warp writes its
+// chunk's n_q partial sums; the last warp to finish a chunk of J (per-J counter) adds J's chunk
+// partials in chunk order (deterministic) into r0[J]. r.r (and b.b) go through the usual
+// deterministic last-CTA sum.
+#define RC_T 256
+template <int NP, int NQ>
+__global__ void __launch_bounds__(RC_T) k_restrict_chunk(int mode, int nchunk, const int4* __restrict__ chunks,
+                                                         const int* __restrict__ jchunk_ptr,
+                                                         const int2* __restrict__ rrec, const double* __restrict__ G,
+                                                         const double* r_in, double* const* rbuf, const double* q,
+                                                         double* const* pbuf, double* x, const double* b, double* r0,
+                                                         double* cpart, unsigned* jcnt, PcgState* st,
+                                                         double* partials) {
+  constexpr int L = NP, PPW = PackCfg<NP>::PPW;
+  __shared__ double red[RC_T / 32];
+  __shared__ double wsum[RC_T / 32][2];
+  int it = 0;
+  double alpha = 0;
+  const double* rold = r_in;
+  double* rnew = nullptr;
+  const double* pnew = nullptr;
+  if (mode >= 1) {
+    if (st->done) return;
+    it = st->it;
+    if (mode == 1) {
+      alpha = st->alpha;
+      rold = rbuf[it & 1];
+      rnew = rbuf[(it + 1) & 1];
+      pnew = pbuf[(it + 1) & 1];
+    } else {
+      rnew = rbuf[0];
+    }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, a = lane % L;
+  const bool act = lane / L < PPW;
+  double rr = 0, bb = 0;
+  const int wstep = gridDim.x * (RC_T / 32);
+  for (int ch = blockIdx.x * (RC_T / 32) + w; ch < nchunk; ch += wstep) {
+    const int4 cd = chunks[ch];  // (J, first piece, end piece, chunk index within J)
+    double accq[NQ];
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) accq[c] = 0;
+    const int ke = cd.z;
+    int k = act ? cd.y + lane / L : ke;
+    int2 rec = k < ke ? rrec[k] : make_int2(0, 0);
+    for (; k < ke; k += PPW) {
+      const int2 nrec = k + PPW < ke ? rrec[k + PPW] : rec;
+      const int cell = rec.x, o = rec.y & 0x7fffffff;
+      const bool owner = rec.y < 0;
+      const size_t id = (size_t)cell * NP + a;
+      const double* Go = G + ((size_t)o * NP + a) * NQ;
+      double gv[NQ];
+      if constexpr (NQ % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < NQ; c += 2) {
+          const double2 g2 = __ldg(reinterpret_cast<const double2*>(Go + c));
+          gv[c] = g2.x; gv[c + 1] = g2.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) gv[c] = __ldg(Go + c);
+      }
+      double rv;
+      if (mode == 0) rv = rold[id];
+      else if (mode == 1) rv = rold[id] - alpha * q[id];
+      else rv = b[id] - q[id];
+      if (owner && mode >= 1) {
+        rnew[id] = rv;
+        rr += rv * rv;
+        if (mode == 1) x[id] += alpha * pnew[id];
+        else bb += b[id] * b[id];
+      }
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) accq[c] += gv[c] * rv;
+      rec = nrec;
+    }
+    double mine[NQ];
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) mine[c] = warp_sum(accq[c]);
+    const int J = cd.x, nch = jchunk_ptr[J + 1] - jchunk_ptr[J];
+    if (nch == 1) {
+      if (lane < NQ) {
+        double v = 0;
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) if (c == lane) v = mine[c];
+        r0[(size_t)J * NQ + lane] = v;
+      }
+    } else {
+      if (lane < NQ) {
+        double v = 0;
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) if (c == lane) v = mine[c];
+        cpart[(size_t)ch * NQ + lane] = v;
+      }
+      __threadfence();
+      __syncwarp();
+      unsigned last = 0;
+      if (lane == 0) last = atomicAdd(&jcnt[J], 1u) == (unsigned)nch - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        if (lane < NQ) {
+          double v = 0;
+          for (int c2 = jchunk_ptr[J]; c2 < jchunk_ptr[J + 1]; ++c2) v += __ldcg(cpart + (size_t)c2 * NQ + lane);
+          r0[(size_t)J * NQ + lane] = v;
+        }
+        if (lane == 0) jcnt[J] = 0;
+      }
+    }
+  }
+  if (mode == 0) return;
+  rr = warp_sum(rr); bb = warp_sum(bb);
+  if (lane == 0) { wsum[w][0] = rr; wsum[w][1] = bb; }
+  __syncthreads();
+  double mine2[2] = {0, 0};
+  if (threadIdx.x == 0)
+    for (int k2 = 0; k2 < RC_T / 32; ++k2) { mine2[0] += wsum[k2][0]; mine2[1] += wsum[k2][1]; }
+  double tot[2];
+  if (last_block<RC_T, 2>(mine2, partials, &st->cnt[1], tot, red)) {
     if (threadIdx.x == 0) {
       st->rr = tot[0];
       if (mode == 2) { st->bb = tot[1]; st->rtol2_bb *= tot[1]; }
@@ -1028,6 +1160,13 @@ int spmv_set_smem(dgas_ctx ctx, size_t smem) {
 }
 
 void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cudaStream_t s) {
+  if (ctx->d_chunks) {
+    DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_restrict_chunk<NP_, NQ_><<<ctx->rc_grid, RC_T, 0, s>>>(
+                                              mode, ctx->nchunk, ctx->d_chunks, ctx->d_jchunk_ptr, ctx->d_rrec, ctx->d_G,
+                                              r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf, ctx->d_x, ctx->d_b, ctx->d_r0,
+                                              ctx->d_cpart, ctx->d_jcnt2, st, ctx->d_partials))));
+    return;
+  }
   const int wpj = ctx->restrict_wpj, cpj = ctx->restrict_cpj;
   const int grid = cpj > 1 ? ctx->ncoarse * cpj : (ctx->ncoarse + (RT / 32 / wpj) - 1) / (RT / 32 / wpj);
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_restrict<NP_, NQ_><<<grid, RT, 0, s>>>(

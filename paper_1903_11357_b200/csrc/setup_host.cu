@@ -586,7 +586,8 @@ static void free_ctx(dgas_ctx ctx) {
                   ctx->d_p[0], ctx->d_p[1], ctx->d_r0, ctx->d_z0, ctx->d_t1, ctx->d_t2, ctx->d_partials,
                   ctx->d_state, ctx->d_astate, ctx->d_alpha, ctx->d_beta, ctx->d_lanczos, ctx->d_err,
                   ctx->d_r2, ctx->d_pbuf, ctx->d_rbuf, ctx->d_perm_dev, ctx->d_rpart, ctx->d_jcnt,
-                  ctx->d_P, ctx->d_p_off, ctx->d_pus, ctx->d_sub_units, ctx->d_rrec, ctx->d_prec, ctx->d_crec};
+                  ctx->d_P, ctx->d_p_off, ctx->d_pus, ctx->d_sub_units, ctx->d_rrec, ctx->d_prec, ctx->d_crec,
+                  ctx->d_chunks, ctx->d_jchunk_ptr, ctx->d_cpart, ctx->d_jcnt2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->d_A0b) cudaFree(ctx->d_A0b);
