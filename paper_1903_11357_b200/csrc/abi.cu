@@ -255,6 +255,11 @@ static int finish_setup_buffers(dgas_ctx ctx) {
         const int rc = spmv_ring_configure(ctx, nsm);
         if (rc < 0) return DGAS_E_CUDA;
         if (rc == 0) ctx->spmv_kernel = 4;
+        // separate direction-update pass when the vectors are large (config 3, 21 MB each: the fused
+        // gather of z and p_old costs more than one extra stream; measured +3.9% PCG it/s there,
+        // neutral on config 4, -1..2% on small configs)
+        ctx->spmv_psplit = ctx->N * 8 > 12 * 1024 * 1024;
+        if (const char* e2 = std::getenv("DGAS_SPMV_PSPLIT")) ctx->spmv_psplit = std::atoi(e2) != 0;
       }
     }
   }
@@ -615,7 +620,7 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   }
   // body: spmv, restrict, coarse (side stream), local, prolong; solve: 2 perm in, init_state,
   // init (spmv, restrict, coarse, local, prolong), lanczos, perm out
-  info->launches_per_iter = 4 + coarse_launches;
+  info->launches_per_iter = 4 + coarse_launches + (ctx->spmv_kernel == 4 && ctx->spmv_psplit ? 1 : 0);
   info->launches_per_solve = 3 + (4 + coarse_launches) + 2;
   return DGAS_OK;
 }

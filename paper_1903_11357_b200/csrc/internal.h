@@ -202,6 +202,7 @@ struct dgas_ctx_s {
   int spmv_kernel = 3;
   uint32_t sr_ring_bytes = 0;
   int sr_grid = 0, sr_G = 1;  // persistent CTAs; cells per bulk copy
+  int spmv_psplit = 0;        // PCG direction update as a separate pass before the SpMV (DGAS_SPMV_PSPLIT)
   uint32_t panel_slot_bytes = 0;
 };
 

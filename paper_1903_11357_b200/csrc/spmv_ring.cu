@@ -51,12 +51,15 @@ __global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
   double beta = 0;
   const double* pold = nullptr;
   double* pnew = nullptr;
-  if (mode == 1) {
+  // mode 3 (PCG, p_new precomputed by k_pupdate): gather p_new, no p write; else as mode 1
+  const bool pcg = mode == 1 || mode == 3;
+  if (pcg) {
     if (st->done) return;
     it = st->it;
     beta = it > 0 ? st->beta : 0.0;
     pold = pbuf[it & 1];
     pnew = pbuf[(it + 1) & 1];
+    if (mode == 3) x = pnew;
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c0 = min(nc, blockIdx.x * chunk), c1 = min(nc, c0 + chunk), n = c1 - c0;
@@ -145,9 +148,9 @@ __global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
       const int W = (nptr[i + 1] - nptr[i]) * NP;
       // own p_new (mode 1), loaded before the wait so its latency overlaps
       double pn = 0;
-      if (mode == 1 && h == 0 && lane < NP) {
+      if (pcg && h == 0 && lane < NP) {
         const size_t id = (size_t)c * NP + a;
-        pn = it > 0 ? z[id] + beta * pold[id] : z[id];
+        pn = mode == 3 ? x[id] : it > 0 ? z[id] + beta * pold[id] : z[id];
       }
       const int gi = i / G, gs = gi % SR_NB;
       mbar_wait(&full[gs], (uint32_t)((gi / SR_NB) & 1));
@@ -176,8 +179,8 @@ __global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
       if (h == 0 && lane < NP) {
         const size_t id = (size_t)c * NP + a;
         y[id] = tot;
-        if (mode == 1) {
-          pnew[id] = pn;
+        if (pcg) {
+          if (mode == 1) pnew[id] = pn;
           mydot += pn * tot;
         }
       }
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
       __syncwarp();
     }
   }
-  if (mode != 1) return;
+  if (!pcg) return;
   mydot = warp_sum(mydot);
   if (lane == 0) wdot[w] = mydot;
   __syncthreads();
@@ -287,7 +290,26 @@ int spmv_ring_configure(dgas_ctx ctx, int nsm) {
   return 0;
 }
 
+// p_new = z + beta p_old (PCG direction update as its own streaming pass, DGAS_SPMV_PSPLIT=1): the
+// SpMV then gathers one freshly written vector instead of two
+__global__ void __launch_bounds__(256) k_pupdate(int64_t n, const double* z, double* const* pbuf, const PcgState* st) {
+  if (st->done) return;
+  const int it = st->it;
+  const double beta = it > 0 ? st->beta : 0.0;
+  const double* pold = pbuf[it & 1];
+  double* pnew = pbuf[(it + 1) & 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    pnew[i] = it > 0 ? z[i] + beta * pold[i] : z[i];
+}
+
 void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s) {
+  if (mode == 1 && ctx->spmv_psplit) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    k_pupdate<<<nsm * 8, 256, 0, s>>>(ctx->N, ctx->d_z, ctx->d_pbuf, st);
+    mode = 3;
+  }
   const int grid = ctx->sr_grid, chunk = sr_chunk(ctx);
   const size_t smem = spmv_ring_smem(ctx);
   DISPATCH_PSR(ctx->p, (k_spmv_ring<NP_><<<grid, (SR_NW + 1) * 32, smem, s>>>(

@@ -438,6 +438,9 @@ def test_local_kernel_variants(monkeypatch, name, env, kernel):
     ("cfg4s", {"DGAS_SR_RING_KB": "40", "DGAS_SR_CPS": "4"}),
     ("cfg5s_p6q6", {"DGAS_SR_RING_KB": "120"}),
     ("cfg1", {}),
+    # separate direction-update pass (default only for large vectors) on small problems
+    ("cfg4s", {"DGAS_SPMV_PSPLIT": "1"}),
+    ("cfg5s_p6q6", {"DGAS_SPMV_PSPLIT": "1"}),
 ])
 def test_spmv_kernel_variants(monkeypatch, name, env):
     """Both SpMV kernels (slot ring k_spmv3, byte ring k_spmv_ring) match the oracle's A x, and the
