@@ -20,7 +20,7 @@ _P = ctypes.c_void_p
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", _LIB, _SRC])
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -56,6 +56,10 @@ def lib():
         L.or_get_A0.argtypes = [_P, _P]
         L.or_coarse_basis.argtypes = [_P, ctypes.c_int, _P, _P]
         L.or_pcg.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P]
+        L.or_pcg_ext.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P,
+                                 ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P]
+        L.or_set_threads.argtypes = [ctypes.c_int]
+        L.or_get_threads.restype = ctypes.c_int
         L.or_lanczos.argtypes = [ctypes.c_int, _P, _P, _P]
         L.or_triangle_rule.argtypes = [ctypes.c_int, _P]
         L.or_gauss_legendre.argtypes = [ctypes.c_int, _P, _P]
@@ -243,6 +247,35 @@ class Oracle:
         lz = lanczos(al[:k], be[:max(k - 1, 0)]) if k >= 1 else (np.nan, np.nan, np.nan)
         return dict(status=st, x=x, iters=k, alphas=al[:k], betas=be[:max(k - 1, 0)], resid=res[:k],
                     lmin=lz[0], lmax=lz[1], cond=lz[2])
+
+
+    def pcg_history(self, b, idx, rtol=1e-8, maxit=5000, extra=2, n_hist=5):
+        """PCG as pcg(), also keeping x[idx] after each of the last n_hist iterations and running `extra`
+        iterations past the stop test (reference outputs for full-size parity, tools/make_golden.py).
+        Returns pcg()'s dict (iters = stopping iteration; alphas/betas of the stopping run) plus
+        hist = {j: x_j[idx]} for the iterations j kept and iters_run."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        x = np.zeros(self.N)
+        it = ctypes.c_int(0); run = ctypes.c_int(0)
+        al = np.zeros(maxit + extra); be = np.zeros(maxit + extra); res = np.zeros(maxit + extra)
+        hist = np.zeros((n_hist, idx.shape[0]))
+        st = lib().or_pcg_ext(self.h, _ptr(b), _ptr(x), rtol, maxit, 1, ctypes.byref(it), _ptr(al), _ptr(be),
+                              _ptr(res), idx.shape[0], _ptr(idx), n_hist, _ptr(hist), extra, ctypes.byref(run))
+        k, kr = it.value, run.value
+        lz = lanczos(al[:k], be[:max(k - 1, 0)]) if k >= 1 else (np.nan, np.nan, np.nan)
+        kept = {j: hist[j % n_hist].copy() for j in range(max(1, kr - n_hist + 1), kr + 1)}
+        return dict(status=st, iters=k, iters_run=kr, alphas=al[:k], betas=be[:max(k - 1, 0)], resid=res[:kr],
+                    lmin=lz[0], lmax=lz[1], cond=lz[2], hist=kept, x=x)
+
+
+def set_threads(n):
+    """OpenMP threads for the independent-subdomain loops (bitwise-identical results for any n)."""
+    lib().or_set_threads(int(n))
+
+
+def get_threads():
+    return lib().or_get_threads()
 
 
 def lanczos(alphas, betas):

@@ -1,11 +1,14 @@
 // oracle/oracle.cpp — TEST INFRASTRUCTURE ONLY.
 //
-// A plain, slow, single-threaded CPU implementation of what the hot path computes, written from
+// A plain, slow CPU implementation of what the hot path computes, written from
 // arXiv 1903.11357 in fp64 (plus a long-double variant of the preconditioner for the
 // sensitivity check of DESIGN.md reading R30). It shares NO code with the CUDA path
 // (paper_1903_11357_b200/): its own topology, quadrature (Golub–Welsch Gauss–Legendre), basis,
 // assembly, Cholesky, PCG and Lanczos. Only tests/, __graft_entry__.smoke() and bench.py's
 // cpu_baseline / --impl reference legs may load it. The product path never calls it.
+// Threads: everything is sequential except the loops over independent subdomains (local Cholesky
+// factors, local solves), which OpenMP may spread over or_set_threads(n) threads; each subdomain's
+// arithmetic is the same plain loop whatever the thread count, so results are bitwise identical.
 //
 // Citations: P:n = /root/reference/PAPER.md line n (the reference is not present at run time).
 //   SIPDG form            P:83-98  (eq:Ah, eq:lifting_R_2, eq:Sigma), harmonic average P:53-59,
@@ -30,6 +33,9 @@
 #include <type_traits>
 #include <utility>
 #include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace orc {
 
@@ -606,7 +612,11 @@ int or_setup_schwarz(void* h, int ncoarse, int q, int n_ov, const int* ov_fine, 
   c->FL.Lloc.assign(c->nsub, {});
   std::vector<char> want(c->nsub, n_sample < 0 ? 1 : 0);
   for (int k = 0; k < n_sample; ++k) want[sample[k]] = 1;
-  if (use_local)
+  // subdomains are independent: factored in parallel (OpenMP, one subdomain per thread; the
+  // arithmetic of each factor is the same plain loop whatever the thread count)
+  int bad_sub = -1, bad_ld = 0;
+  if (use_local) {
+#pragma omp parallel for schedule(dynamic)
     for (int s = 0; s < c->nsub; ++s) {
       if (!want[s]) continue;
       const auto& cells = c->sub_cells[s];
@@ -623,12 +633,23 @@ int or_setup_schwarz(void* h, int ncoarse, int q, int n_ov, const int* ov_fine, 
         }
       if (long_double_too) {
         std::vector<long double> ML(M.begin(), M.end());
-        if (!cholesky(n, ML)) return fail(c, -3, "local block not SPD (long double)");
+        if (!cholesky(n, ML)) {
+#pragma omp critical
+          { bad_ld = 1; bad_sub = s; }
+        }
         c->FL.Lloc[s] = std::move(ML);
       }
-      if (!cholesky(n, M)) { char b[64]; std::snprintf(b, 64, "local %d not SPD", s); return fail(c, -3, b); }
+      if (!cholesky(n, M)) {
+#pragma omp critical
+        { if (bad_sub < 0 || s < bad_sub) bad_sub = s; }
+      }
       c->F.Lloc[s] = std::move(M);
     }
+  }
+  if (bad_sub >= 0) {
+    if (bad_ld) return fail(c, -3, "local block not SPD (long double)");
+    char b[64]; std::snprintf(b, 64, "local %d not SPD", bad_sub); return fail(c, -3, b);
+  }
   if (!use_coarse) { c->have_schwarz = true; return 0; }
   // --- coarse basis psi_J: bbox-Legendre products of degree q orthonormalised over D_J (R8)
   c->ov_fine.assign(ov_fine, ov_fine + n_ov);
@@ -800,10 +821,13 @@ int apply_t(Ctx* c, const Factors<T>& F, const double* r, double* z, const std::
   int np = c->np, nq = c->nq;
   int64_t N = (int64_t)c->nc * np;
   std::vector<T> zz(N, T(0));
-  if (c->use_local)
+  if (c->use_local) {
+    for (int s = 0; s < c->nsub; ++s)
+      if (!(only && !(*only)[s]) && F.Lloc[s].empty()) return -1;
+    // independent subdomain solves (disjoint cells): parallel over subdomains, same arithmetic
+#pragma omp parallel for schedule(dynamic)
     for (int s = 0; s < c->nsub; ++s) {
       if (only && !(*only)[s]) continue;
-      if (F.Lloc[s].empty()) return -1;
       const auto& cells = c->sub_cells[s];
       int n = (int)cells.size() * np;
       std::vector<T> x(n);
@@ -813,6 +837,7 @@ int apply_t(Ctx* c, const Factors<T>& F, const double* r, double* z, const std::
       for (int k = 0; k < (int)cells.size(); ++k)
         for (int a = 0; a < np; ++a) zz[(int64_t)cells[k] * np + a] += x[k * np + a];
     }
+  }
   if (c->use_coarse) {
     int64_t N0 = (int64_t)c->ncoarse * nq;
     std::vector<T> r0(N0, T(0));
@@ -895,9 +920,27 @@ void or_coarse_basis(void* h, int J, double* C, double* bbox) {
 // Hestenes–Stiefel PCG from x0 (normally 0): stop when ||r_k||_2 <= rtol ||b||_2 (checked after the
 // x/r update, before the preconditioner). alpha/beta recorded for the Lanczos estimate.
 // returns 0 converged, 1 not converged, -4 breakdown. precond: 1 = Schwarz, 0 = identity.
+// or_pcg_ext: the same iteration, plus (for stored reference outputs) the iterate x restricted to the
+// dofs idx[0..n_idx) after every iteration j, kept in a ring hist[(j % n_hist) * n_idx + t], and
+// `extra` further iterations after the stop test fires (stop test skipped, *iters = the stopping
+// iteration, *iters_run = iterations actually performed). or_pcg = or_pcg_ext with no history.
+int or_pcg_ext(void* h, const double* b, double* x, double rtol, int maxit, int precond, int* iters, double* alphas,
+               double* betas, double* resid, int n_idx, const int64_t* idx, int n_hist, double* hist, int extra,
+               int* iters_run);
 int or_pcg(void* h, const double* b, double* x, double rtol, int maxit, int precond, int* iters, double* alphas,
            double* betas, double* resid) {
+  int run = 0;
+  return or_pcg_ext(h, b, x, rtol, maxit, precond, iters, alphas, betas, resid, 0, nullptr, 0, nullptr, 0, &run);
+}
+int or_pcg_ext(void* h, const double* b, double* x, double rtol, int maxit, int precond, int* iters, double* alphas,
+               double* betas, double* resid, int n_idx, const int64_t* idx, int n_hist, double* hist, int extra,
+               int* iters_run) {
   Ctx* c = (Ctx*)h;
+  *iters_run = 0;
+  auto record = [&](int j) {
+    if (n_hist > 0)
+      for (int t = 0; t < n_idx; ++t) hist[(int64_t)(j % n_hist) * n_idx + t] = x[idx[t]];
+  };
   int64_t N = (int64_t)c->nc * c->np;
   std::vector<double> r(N), z(N), p(N), q(N);
   or_spmv(h, x, q.data());
@@ -917,7 +960,10 @@ int or_pcg(void* h, const double* b, double* x, double rtol, int maxit, int prec
   double gamma = 0;
   for (int64_t i = 0; i < N; ++i) { p[i] = z[i]; gamma += r[i] * z[i]; }
   if (!(gamma > 0) || !std::isfinite(gamma)) return -4;
-  for (int k = 0; k < maxit; ++k) {
+  int stop = -1;  // iteration at which the stop test fired (history mode continues `extra` more)
+  for (int k = 0; k < maxit + extra; ++k) {
+    if (stop < 0 && k >= maxit) break;
+    if (stop >= 0 && k >= stop + extra) break;
     or_spmv(h, p.data(), q.data());
     double pq = 0;
     for (int64_t i = 0; i < N; ++i) pq += p[i] * q[i];
@@ -927,8 +973,13 @@ int or_pcg(void* h, const double* b, double* x, double rtol, int maxit, int prec
     double rr = 0;
     for (int64_t i = 0; i < N; ++i) { x[i] += alpha * p[i]; r[i] -= alpha * q[i]; rr += r[i] * r[i]; }
     if (resid) resid[k] = std::sqrt(rr) / bnorm;
-    *iters = k + 1;
-    if (std::sqrt(rr) <= rtol * bnorm) return 0;
+    *iters_run = k + 1;
+    record(k + 1);
+    if (stop < 0) *iters = k + 1;
+    if (stop < 0 && std::sqrt(rr) <= rtol * bnorm) {
+      stop = k + 1;
+      if (extra == 0) return 0;
+    }
     if (prec(r, z)) return -1;
     double gnew = 0;
     for (int64_t i = 0; i < N; ++i) gnew += r[i] * z[i];
@@ -938,7 +989,22 @@ int or_pcg(void* h, const double* b, double* x, double rtol, int maxit, int prec
     gamma = gnew;
     for (int64_t i = 0; i < N; ++i) p[i] = z[i] + beta * p[i];
   }
+  return stop >= 0 ? 0 : 1;
+}
+
+void or_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+int or_get_threads() {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
   return 1;
+#endif
 }
 
 // Lanczos tridiagonal from the CG coefficients (R12):

@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed for " + ", ".join(failed))
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,
-                           "-cudart", "static"])
+                           "-cudart", "shared", "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
     for o in objs:
         os.remove(o)
     return LIB

@@ -1,8 +1,9 @@
 // internal.h — context layout and device helpers of libdgas (B200 / sm_100a).
 //
 // Internal numbering: cells are renumbered subdomain-major (so R_i is a contiguous range,
-// PAPER.md:129-137) and, inside a subdomain, in reverse Cuthill–McKee order of the face graph so the
-// local Cholesky factors stay inside a narrow block envelope.
+// PAPER.md:129-137) and, inside a subdomain, in the face-graph ordering with the smallest block
+// envelope among reverse Cuthill–McKee and several Sloan orderings (setup_host.cu), so the local
+// Cholesky factors stay inside a narrow block envelope (DESIGN.md §5 "Local factors").
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

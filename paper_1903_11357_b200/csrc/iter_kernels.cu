@@ -1,11 +1,13 @@
 // iter_kernels.cu — per-iteration kernels of ASPCG with the additive Schwarz
 // preconditioner P^-1 = Q A0^-1 Q^T + sum_i E_i A_i^-1 E_i^T (R8).
 //
-// One PCG iteration = 4 launches (all fp64, HBM-bound GEMV-class work, no tensor cores):
-//   k_spmv     p = z + beta p_old (fused), q = A p, p.q  -> alpha          (I1, I7)
-//   k_restrict x += alpha p, r -= alpha q, r.r -> convergence; r0 = Q^T r (I2, I3)
-//   k_apply    [coarse CTAs] z0 = A0^-1 r0   ||   [subdomain CTAs] z_i = A_i^-1 r_i   (I4, I5)
-//   k_prolong  z += Q z0, r.z -> beta, iteration bookkeeping, graph condition   (I6)
+// One PCG iteration (captured in a CUDA graph WHILE node, abi.cu):
+//   k_spmv_ring (spmv_ring.cu)  p = z + beta p_old (fused), q = A p, p.q -> alpha      (I1, I7)
+//                               [k_spmv3 here: the slot-ring variant, DGAS_SPMV_KERNEL=3]
+//   k_restrict_chunk            x += alpha p, r -= alpha q, r.r -> stop test; r0 = Q^T r  (I2, I3)
+//   k_coarse | k_nd_fwd/bwd     z0 = A0^-1 r0 on a forked stream                        (I4)
+//   k_local_panel | k_local     z_i = A_i^-1 r_i for all subdomains                     (I5)
+//   k_prolong                   z += Q z0, r.z -> beta, bookkeeping, graph condition    (I6)
 // Reductions are deterministic: per-CTA partials, the last CTA to arrive sums them in a fixed order.
 #include <cfloat>
 
@@ -68,91 +70,6 @@ struct ProlongCfg {
   static constexpr int L = NP <= 4 ? 4 : NP <= 8 ? 8 : NP <= 16 ? 16 : 32;  // lanes per cell
   static constexpr int CPW = 32 / L;                                         // cells per warp
 };
-
-// ------------------------------------------------------------------ SpMV (+ fused direction update)
-// mode 0: y = A x.   mode 1 (PCG): p_new = z + beta p_old (beta = 0 at it = 0), q = A p_new, p.q.
-// One warp per cell row; the row block is n x (deg n) row-major, lanes stride its columns.
-#define SPMV_WARPS 8
-template <int NP>
-__global__ void __launch_bounds__(SPMV_WARPS * 32) k_spmv(int mode, int nc, const int* __restrict__ nbr_ptr,
-                                                          const int* __restrict__ nbr, const int64_t* __restrict__ a_off,
-                                                          const double* __restrict__ A, const double* x, double* y,
-                                                          const double* z, double* const* pbuf, PcgState* st,
-                                                          double* partials, double* alpha_hist) {
-  constexpr int MAXT = (16 * NP + 31) / 32;
-  __shared__ double red[SPMV_WARPS];
-  __shared__ double wdot[SPMV_WARPS];
-  int it = 0;
-  double beta = 0;
-  const double* pold = nullptr;
-  double* pnew = nullptr;
-  if (mode == 1) {
-    if (st->done) return;
-    it = st->it;
-    beta = it > 0 ? st->beta : 0.0;
-    pold = pbuf[it & 1];
-    pnew = pbuf[(it + 1) & 1];
-  }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * SPMV_WARPS + w;
-  double mydot = 0;
-  if (c < nc) {
-    const int lo = nbr_ptr[c], deg = nbr_ptr[c + 1] - lo, W = deg * NP;
-    const double* row = A + a_off[c];
-    double pv[MAXT];
-#pragma unroll
-    for (int t = 0; t < MAXT; ++t) {
-      int col = lane + 32 * t;
-      pv[t] = 0;
-      if (col < W) {
-        int j = __ldg(nbr + lo + col / NP), b = col % NP;
-        size_t id = (size_t)j * NP + b;
-        pv[t] = mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
-      }
-    }
-    double acc[NP];
-#pragma unroll
-    for (int a = 0; a < NP; ++a) {
-      double v = 0;
-#pragma unroll
-      for (int t = 0; t < MAXT; ++t) {
-        int col = lane + 32 * t;
-        if (col < W) v += __ldcs(row + (size_t)a * W + col) * pv[t];
-      }
-      acc[a] = v;
-    }
-#pragma unroll
-    for (int a = 0; a < NP; ++a) acc[a] = warp_sum(acc[a]);
-    double out = 0;
-#pragma unroll
-    for (int a = 0; a < NP; ++a) if (lane == a) out = acc[a];
-    if (lane < NP) {
-      size_t id = (size_t)c * NP + lane;
-      y[id] = out;
-      if (mode == 1) {
-        double pn = it > 0 ? z[id] + beta * pold[id] : z[id];
-        pnew[id] = pn;
-        mydot = pn * out;
-      }
-    }
-  }
-  if (mode != 1) return;
-  mydot = warp_sum(mydot);
-  if (lane == 0) wdot[w] = mydot;
-  __syncthreads();
-  double tot[1] = {0};
-  if (threadIdx.x == 0)
-    for (int k = 0; k < SPMV_WARPS; ++k) tot[0] += wdot[k];
-  double res[1];
-  if (last_block<SPMV_WARPS * 32, 1>(tot, partials, &st->cnt[0], res, red)) {
-    if (threadIdx.x == 0) {
-      double pq = res[0];
-      st->pq = pq;
-      if (!(pq > 0) || !isfinite(pq)) { st->done = 1; st->status = DGAS_E_BREAKDOWN; }
-      else { st->alpha = st->gamma / pq; alpha_hist[it] = st->alpha; }
-    }
-  }
-}
 
 // ------------------------------------------------------------------ SpMV: persistent, batched, TMA ring
 // Each CTA owns a contiguous range of cell rows, processed in batches of G cells whose (contiguous,

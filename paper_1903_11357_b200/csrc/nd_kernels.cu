@@ -313,6 +313,20 @@ int nd_setup_run(dgas_ctx ctx) {
     P.h_wf_ptr[L + 1] = (int)wf.size();
     P.h_wb_ptr[L + 1] = (int)wb.size();
   }
+  if (std::getenv("DGAS_VERBOSE")) {
+    for (int L = 0; L < P.nlev; ++L) {
+      int mf = 0, mu = 0;
+      int64_t by = 0;
+      for (int k = P.h_lev_ptr[L]; k < P.h_lev_ptr[L + 1]; ++k) {
+        const int f = P.h_lev_fronts[k];
+        mf = std::max(mf, P.h_nF[f]); mu = std::max(mu, P.h_nU[f]);
+        by += ((int64_t)P.h_nF[f] * P.h_nF[f] + 2 * (int64_t)P.h_nF[f] * P.h_nU[f]) * 8;
+      }
+      fprintf(stderr, "dgas: ND level %d: %d fronts, max nF %d, max nU %d, %.2f MB, work fwd %d bwd %d\n", L,
+              P.h_lev_ptr[L + 1] - P.h_lev_ptr[L], mf, mu, by / 1e6, P.h_wf_ptr[L + 1] - P.h_wf_ptr[L],
+              P.h_wb_ptr[L + 1] - P.h_wb_ptr[L]);
+    }
+  }
   if ((st = up(ctx, &P.d_wf, wf)) || (st = up(ctx, &P.d_wb, wb))) return st;
   DGAS_CUDA(cudaMalloc((void**)&P.d_rb, (ctx->N0 + 1) * 8));
   DGAS_CUDA(cudaMalloc((void**)&P.d_zb, (ctx->N0 + 1) * 8));
@@ -450,9 +464,18 @@ int nd_set_smem(dgas_ctx ctx) {
   int dev = 0, mx = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if ((int)std::max(shf, shb) > mx) { ctx->detail = "nested-dissection front too large for shared memory"; return DGAS_E_INVALID_ARG; }
-  DGAS_CUDA(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shf));
-  DGAS_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
+  // The limit is a per-function (process-wide) attribute shared by every context: raise it to the
+  // opt-in maximum rather than this context's front size, so a later context with smaller fronts
+  // never lowers it under an earlier one's launches (or its instantiated PCG graph).
+  cudaFuncAttributes ff{}, fb{};
+  DGAS_CUDA(cudaFuncGetAttributes(&ff, k_nd_fwd));
+  DGAS_CUDA(cudaFuncGetAttributes(&fb, k_nd_bwd));
+  if (shf + ff.sharedSizeBytes > (size_t)mx || shb + fb.sharedSizeBytes > (size_t)mx) {
+    ctx->detail = "nested-dissection front too large for shared memory";
+    return DGAS_E_INVALID_ARG;
+  }
+  DGAS_CUDA(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)ff.sharedSizeBytes));
+  DGAS_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fb.sharedSizeBytes));
   return 0;
 }
 
