@@ -78,6 +78,27 @@ def test_P3b_interior_face_block():
     assert np.abs(Bpp - (vol + bnd + face_pp)).max() < 1e-12
 
 
+def test_P3c_harmonic_h_and_rho_unequal_cells():
+    """Unit square next to a 2x1 rectangle: the off-diagonal block pins <h> and <rho> as HARMONIC
+    averages over the face (eq:Sigma P:94-98; R1), which the equal-square P3b cannot."""
+    G = _golden()
+    P = _square(1)
+    P2 = copy.copy(P)
+    P2.xy = np.array([[0, 0], [1, 0], [3, 0], [0, 1], [1, 1], [3, 1]], float)
+    P2.cell_ptr = np.array([0, 4, 8], np.int32)
+    P2.cell_vtx = np.array([0, 1, 4, 3, 1, 2, 5, 4], np.int32)
+    P2.part = np.zeros(2, np.int32); P2.parent = np.zeros(2, np.int32)
+    for rho, key in (([1.0, 1.0], "P3c_rho1_Bpm"), ([1.0, 3.0], "P3c_rho13_Bpm")):
+        P2.kappa = np.array(rho)
+        o = O.Oracle(P2)
+        Bpm, ok = o.block(0, 1)
+        Bmp, _ = o.block(1, 0)
+        ref = np.array(G[key])
+        assert ok
+        assert np.abs(Bpm - ref).max() < 1e-13, (key, Bpm, ref)
+        assert np.abs(Bmp - ref.T).max() < 1e-13
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_P4_symmetric_spd(cfg):
     P = g.config(cfg, scale="small")

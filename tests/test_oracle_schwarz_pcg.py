@@ -304,3 +304,62 @@ def test_paper_ex1_rho_one_identical():
     a = _ex1("convex", True, 1.0, 1, levels=1)
     b = _ex1("convex", False, 1.0, 1, levels=1)
     assert a["iters"] == b["iters"] and np.array_equal(a["x"], b["x"])
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_band_coarse_path_matches_dense(cfg):
+    """The band-Cholesky coarse factor/solve (used by the oracle when N0 > dense_max, i.e. full-size
+    config 3) against the dense Cholesky path (pinned by P8/P9 above): z = Q A0^-1 Q^T r + local
+    solves, eq. P:160-165, must agree to rounding. Iterative refinement (R30) can only
+    move the band solve closer to the dense one."""
+    P = g.config(cfg, scale="small")
+    od = O.Oracle(P)
+    od.setup_schwarz()
+    ob = O.Oracle(P)
+    ob.setup_schwarz(dense_max=0)
+    # the band path really ran: A0 is not stored densely
+    with pytest.raises(O.OracleError):
+        ob.A0()
+    A0 = od.A0()
+    kap = np.linalg.cond(A0)
+    for seed in range(3):
+        r = g.normal(70 + seed, od.N)
+        zd = od.apply(r)
+        zb = ob.apply(r)
+        assert np.linalg.norm(zb - zd) <= max(1e-12, 10 * kap * 2.2e-16) * np.linalg.norm(zd), (seed, kap)
+    # coarse part alone against numpy's dense solve of the same A0
+    oc = O.Oracle(P)
+    oc.setup_schwarz(dense_max=0, use_local=False)
+    r = g.normal(80, od.N)
+    Q = _Q_dense(od)
+    zc_ref = Q @ np.linalg.solve(A0, Q.T @ r)
+    zc = oc.apply(r)
+    assert np.linalg.norm(zc - zc_ref) <= 10 * kap * 2.2e-16 * np.linalg.norm(zc_ref)
+    oc.set_refine(1)
+    zc1 = oc.apply(r)
+    assert np.linalg.norm(zc1 - zc_ref) <= 2 * np.linalg.norm(zc - zc_ref) + 1e-14 * np.linalg.norm(zc_ref)
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_apply_sampled_is_full_apply_restricted(cfg):
+    """or_apply_sampled (full-size sampled parity) is the full apply P^-1 r restricted to the
+    cells of the sampled subdomains, and zero elsewhere: equal to the full apply there, bit for bit
+    (same coarse solve, same local solves), whether or not the other subdomains were factored."""
+    P = g.config(cfg, scale="small")
+    sample = [0, P.n_sub // 2, P.n_sub - 1]
+    of = O.Oracle(P)
+    of.setup_schwarz()
+    os_ = O.Oracle(P)
+    os_.setup_schwarz(sample=sample)
+    r = g.normal(90, of.N)
+    z = of.apply(r)
+    zs = os_.apply_sampled(r, sample)
+    zs2 = of.apply_sampled(r, sample)
+    mask = np.repeat(np.isin(P.part, sample), of.np_)
+    assert mask.any() and (~mask).any()
+    assert np.array_equal(zs[mask], z[mask])
+    assert np.array_equal(zs2[mask], z[mask])
+    assert not zs[~mask].any() and not zs2[~mask].any()
+    # the unsampled setup really lacks the other factors
+    with pytest.raises(O.OracleError):
+        os_.apply(r)
