@@ -114,6 +114,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
   if (ctx->coarse_mode == 2) {
     if (const char* e = std::getenv("DGAS_ND_GRID")) ctx->nd_grid = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("DGAS_ND_L2")) ctx->nd_l2 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("DGAS_ND_TOL")) ctx->nd_tol = std::atof(e);
     int st2 = nd_set_smem(ctx);
     if (st2) return st2;
     if ((st2 = nd_calibrate(ctx))) return st2;

@@ -78,6 +78,7 @@ struct dgas_ctx_s {
   int coarse_mode = 0;       // 0 dense explicit inverse, 1 band Cholesky (tile sweeps), 2 nested dissection
   int nd_grid = 1 << 30;     // max CTAs per ND solve level (grid-stride over work items; DGAS_ND_GRID)
   int nd_l2 = 1;             // ND solve operator loads evict-last in L2 (DGAS_ND_L2)
+  double nd_tol = 3e-11;     // coarse-solve relative error above which refinement steps are added (Z30; DGAS_ND_TOL)
   NdPlan nd;
   double* d_A0b = nullptr;   // A0 blocks per coarse pair (n_pairs x nq x nq)
   int max_sub_cells = 0, max_urow = 0, max_deg = 0;

@@ -405,13 +405,15 @@ __global__ void k_nd_testvec(int64_t n, double* v) {
   v[i] = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
 }
 
-// Choose the iterative-refinement steps of the multifrontal coarse solve (R30): solve
-// A0 z = A0 v for a fixed test vector v; when its relative error ||z - v|| / ||v|| exceeds 1e-9, add
-// refinement steps while each one cuts the error by at least 4x (at most 2). Measured on config 4
-// (kappa(A0) = 8e8, 9e6 after diagonal scaling): LAPACK Cholesky 5.8e-11, explicit dense inverse
-// 3.5e-6, this solve 4.4e-10, with one refinement step 7.7e-12 -- but the refinement step doubles the
-// coarse chain, which then no longer hides behind the local solves (-17% PCG it/s), so it is only
-// taken beyond 1e-9.
+// Choose the iterative-refinement steps of the multifrontal coarse solve (R30):
+// solve A0 z = A0 v for a fixed test vector v; while its relative error ||z - v|| / ||v|| exceeds
+// nd_tol = 3e-11, add refinement steps as long as each one cuts the error by at least 4x (at most 2).
+// Measured on config 4 (kappa(A0) = 8e8, 9e6 after diagonal scaling): LAPACK Cholesky 5.8e-11,
+// explicit dense inverse 3.5e-6, this solve 2.9e-10, with one refinement step 2.4e-11. The step doubles
+// the coarse chain, which then sticks out of the local solves on config 4 (2100 -> 1826 PCG it/s);
+// configs 3 and 5 (4e-12, 1.2e-11) need none. A persistent dependency-driven single-launch solve and
+// a 4-rows-per-warp GEMV were tried for this and measured slower (beside the local solves only one
+// 256-thread CTA per SM fits, and both designs hold fewer loads in flight than this one).
 int nd_calibrate(dgas_ctx ctx) {
   NdPlan& P = ctx->nd;
   if (P.refine_env >= 0) return 0;
@@ -440,7 +442,7 @@ int nd_calibrate(dgas_ctx ctx) {
   double err = measure(0);
   P.calib_err0 = err;
   int best = 0;
-  for (int r = 1; r <= 2 && err > 1e-9; ++r) {
+  for (int r = 1; r <= 2 && err > ctx->nd_tol; ++r) {
     const double e = measure(r);
     if (!(e >= 0) || !(e < 0.25 * err)) break;
     err = e;

@@ -44,6 +44,9 @@ CASES = {
     "cfg4s": lambda: g.config(4, scale="small"),
     "cfg5s_p1q1": lambda: g.config(5, 1, 1, scale="small"),
     "cfg5s_p3q1": lambda: g.config(5, 3, 1, scale="small"),
+    "cfg5s_p4q1": lambda: g.config(5, 4, 1, scale="small"),
+    "cfg5s_p5q1": lambda: g.config(5, 5, 1, scale="small"),
+    "cfg5s_p5q5": lambda: g.config(5, 5, 5, scale="small"),
     "cfg5s_p4q4": lambda: g.config(5, 4, 4, scale="small"),
     "cfg5s_p6q1": lambda: g.config(5, 6, 1, scale="small"),
     "cfg5s_p6q6": lambda: g.config(5, 6, 6, scale="small"),
@@ -144,46 +147,55 @@ def _oracle_spread(o, b, ref, rtol=1e-8, P=None):
     return min(its), max(its)
 
 
-def _iters_ok(o, b, ref, iters, P):
-    """north_star: within 2 of the oracle; else inside the oracle's own rounding spread +- 2 (R22)."""
+def _iters_ok(o, b, ref, iters, P, label=""):
+    """north_star: within 2 of the oracle. Else (R22: the stopping iteration is not unique under
+    rounding when the residual plateaus near rtol) inside the oracle's OWN spread [lo, hi] under
+    last-bit perturbations of b and G -- one allowance or the other, never both stacked. The spread
+    branch is logged so the test output shows how often it fires."""
     if abs(iters - ref["iters"]) <= 2:
         return True
     lo, hi = _oracle_spread(o, b, ref, P=P)
-    return lo - 2 <= iters <= hi + 2
+    print(f"\n[spread branch] {label}: GPU iters {iters}, oracle {ref['iters']}, oracle spread [{lo}, {hi}]")
+    return lo <= iters <= hi
 
 
-@pytest.mark.parametrize("name", list(CASES))
-def test_pcg_parity(name):
-    P, o, S = _pair(name)
-    b = o.rhs()
+def _pcg_parity(S, o, P, b, label, x_tol=1e-7):
+    """Full PCG parity against the oracle on the same b (north_star): iterations (_iters_ok), x within
+    1e-7 relative (at the common iteration count when the stops differ), Lanczos K within
+    1% (or the oracle's own spread / interlacing when the RHS excites an extreme eigenvector only at
+    rounding level, R22), and the first CG coefficients to rounding."""
     ref = o.pcg(b, rtol=1e-8)
     x, iters, cond, st = S.pcg(_dev(b), rtol=1e-8)
     x = x.cpu().numpy()
     a, bet = S.history()
     assert st == 0 and ref["status"] == 0
-    if abs(iters - ref["iters"]) > 2:
-        lo, hi = _oracle_spread(o, b, ref, P=P)
-        assert lo - 2 <= iters <= hi + 2, (iters, ref["iters"], lo, hi)
+    assert _iters_ok(o, b, ref, iters, P, label), (label, iters, ref["iters"])
     if iters == ref["iters"]:
-        assert np.linalg.norm(x - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+        err = np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])
     else:  # compare at a fixed iteration count to separate round-off from stopping (SURVEY §8c)
         k = min(iters, ref["iters"])
         xk, ik, _, sk = S.pcg(_dev(b), rtol=1e-300, maxit=k)
         rk = o.pcg(b, rtol=1e-300, maxit=k)
         assert ik == k == rk["iters"], (ik, sk, k, rk["iters"], rk["status"])
-        assert np.linalg.norm(xk.cpu().numpy() - rk["x"]) <= 1e-7 * np.linalg.norm(rk["x"])
+        err = np.linalg.norm(xk.cpu().numpy() - rk["x"]) / np.linalg.norm(rk["x"])
+    assert err <= x_tol, (label, err)
     if abs(cond - ref["cond"]) > 0.01 * ref["cond"]:
-        # Lanczos K is a Ritz lower bound of K(P^-1 A); when the RHS excites an extreme eigenvector
-        # only at rounding level the estimate is not unique (R22): accept the oracle's own spread
-        # under 1e-13 perturbations of b, or (small problems) interlacing with the true K
         ks = [o.pcg(b * (1 + 1e-13 * g.normal(600 + t, b.shape[0])), rtol=1e-8)["cond"] for t in range(4)]
         ok = min(ks) * 0.99 <= cond <= max(ks) * 1.01
         if not ok and S.N <= 3000:
             ev = np.sort(np.linalg.eigvals(o.dense_precond() @ o.dense_A()).real)
             ok = 0.95 * ev[-1] / ev[0] <= cond <= ev[-1] / ev[0] * (1 + 1e-8)
+        print(f"\n[K branch] {label}: GPU K {cond}, oracle {ref['cond']}, oracle spread {ks}, ok {ok}")
         assert ok, (cond, ref["cond"], ks)
     assert len(a) == iters
     assert np.allclose(a[:3], ref["alphas"][:3], rtol=1e-9)
+    return iters, cond
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_pcg_parity(name):
+    P, o, S = _pair(name)
+    _pcg_parity(S, o, P, o.rhs(), name)
 
 
 def test_pcg_host_matches_device():
@@ -286,15 +298,13 @@ def test_full_size_sampled_apply(k):
         mask |= P.part == s
     idx = np.repeat(mask, S.info["n_p"])
     err = np.linalg.norm(z[idx] - zr[idx]) / np.linalg.norm(zr[idx])
-    if err > 1e-10:
-        # DESIGN.md R30: the coarse correction amplifies last-bit differences of two correct assemblies
-        # by kappa(A0). Measure the oracle's own sensitivity to 1-ulp noise in Q and accept 10x it.
-        o2 = O.Oracle(P)
-        o2.set_perturb(2.2e-16, 1)
-        o2.setup_schwarz(sample=sample)
-        zp = o2.apply_sampled(r, sample)
-        sens = np.linalg.norm(zp[idx] - zr[idx]) / np.linalg.norm(zr[idx])
-        assert err <= 10 * sens, (err, sens)
+    info = S.get_info()
+    print(f"\ncfg{k} full-size sampled apply: rel err {err:.3e}; coarse solve relerr "
+          f"{info['coarse_solve_relerr']:.3e} with {info['coarse_refine']} refinement step(s)")
+    # north_star bound, strict: the coarse solve is refined to <= 3e-11 (R30)
+    assert err <= 1e-10, err
+    if info["coarse_mode"] == 2:
+        assert info["coarse_solve_relerr"] <= 3e-11
     # PCG at full size: converges, and the true residual (oracle SpMV) meets the tolerance
     b = o.rhs()
     x, iters, cond, st = S.pcg(_dev(b))
@@ -319,8 +329,8 @@ def test_nested_dissection_coarse_path(monkeypatch, name, leaf):
     S = _solver(P)
     info = S.get_info()
     assert info["coarse_mode"] == 2
-    # setup-time calibration of the ND solve (R30): one solve of A0 z = A0 v within 1e-9 after refinement
-    assert 0 < info["coarse_solve_relerr"] <= 1e-9 and 0 <= info["coarse_refine"] <= 2
+    # setup-time calibration of the ND solve (R30, Z30): one solve of A0 z = A0 v within 3e-11 after refinement
+    assert 0 < info["coarse_solve_relerr"] <= 3e-11 and 0 <= info["coarse_refine"] <= 2
     o = O.Oracle(P)
     o.setup_schwarz()
     for seed in range(3):
@@ -328,13 +338,7 @@ def test_nested_dissection_coarse_path(monkeypatch, name, leaf):
         z = S.apply(_dev(r)).cpu().numpy()
         zr = o.apply(r)
         assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr), seed
-    b = o.rhs()
-    ref = o.pcg(b, rtol=1e-8)
-    x, iters, cond, st = S.pcg(_dev(b), rtol=1e-8)
-    assert st == 0
-    if abs(iters - ref["iters"]) > 2:  # R22: the oracle's own spread under last-bit perturbations
-        lo, hi = _oracle_spread(o, b, ref, P=P)
-        assert lo - 2 <= iters <= hi + 2, (iters, ref["iters"], lo, hi)
+    _pcg_parity(S, o, P, o.rhs(), f"nd {name} leaf {leaf}")
 
 
 @pytest.mark.parametrize("name", ["cfg2s", "ex4_h256_H16_p3", "cfg4s"])
@@ -424,10 +428,7 @@ def test_local_kernel_variants(monkeypatch, name, env, kernel):
         z = S.apply(_dev(r)).cpu().numpy()
         zr = o.apply(r)
         assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr), seed
-    b = o.rhs()
-    ref = o.pcg(b, rtol=1e-8)
-    x, iters, cond, st = S.pcg(_dev(b))
-    assert st == 0 and _iters_ok(o, b, ref, iters, P), (iters, ref["iters"])
+    _pcg_parity(S, o, P, o.rhs(), f"local {name} {env}")
     S.close()
 
 
@@ -459,11 +460,50 @@ def test_spmv_kernel_variants(monkeypatch, name, env):
         yv = S.spmv(_dev(xv)).cpu().numpy()
         yr = o.spmv(xv)
         assert np.all(np.abs(yv - yr) <= tol * o.spmv_abs(xv) + 1e-300), seed
-    b = o.rhs()
-    ref = o.pcg(b, rtol=1e-8)
-    x, iters, cond, st = S.pcg(_dev(b))
-    assert st == 0 and _iters_ok(o, b, ref, iters, P), (iters, ref["iters"])
+    _pcg_parity(S, o, P, o.rhs(), f"spmv {name} {env}")
     S.close()
+
+
+@pytest.mark.parametrize("name", ["cfg4s", "cfg5s_p6q6"])
+def test_pupdate_split_is_bitwise_identical(monkeypatch, name):
+    """The separate direction-update pass (k_pupdate + SpMV gather of one vector, the default only when
+    the vectors exceed 12 MB, i.e. full-size config 3) computes p = z + beta p with the same expression
+    as the fused gather: PCG with and without the split gives the same iterations, K and x bit for bit."""
+    P = CASES[name]()
+    b = _dev(g.normal(12, P.N))
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("DGAS_SPMV_PSPLIT", v)
+        S = _solver(P)
+        x, it, c, st = S.pcg(b, rtol=1e-8)
+        a, bet = S.history()
+        out.append((x.cpu().numpy(), it, c, st, a))
+        S.close()
+    (x0, i0, c0, s0, a0), (x1, i1, c1, s1, a1) = out
+    assert s0 == s1 == 0 and i0 == i1 and c0 == c1
+    assert np.array_equal(x0, x1) and np.array_equal(a0, a1)
+
+
+def test_nd_two_contexts_smem_limit(monkeypatch):
+    """the ND kernels' dynamic shared-memory limit is a per-function attribute; a second
+    context with smaller fronts must not break the first one's launches (or its PCG graph)."""
+    monkeypatch.setenv("DGAS_COARSE_MODE", "nd")
+    P = CASES["cfg4s"]()
+    monkeypatch.setenv("DGAS_ND_LEAF", "64")
+    S1 = _solver(P)
+    r = _dev(g.normal(21, S1.N))
+    z1 = S1.apply(r).cpu().numpy()
+    b = _dev(g.normal(22, S1.N))
+    x1, it1, _, _ = S1.pcg(b)
+    monkeypatch.setenv("DGAS_ND_LEAF", "2")
+    S2 = _solver(P)
+    z2 = S2.apply(r).cpu().numpy()
+    assert np.linalg.norm(z2 - z1) <= 1e-10 * np.linalg.norm(z1)
+    assert np.array_equal(S1.apply(r).cpu().numpy(), z1)  # first context still works, same result
+    x1b, it1b, _, st = S1.pcg(b)
+    assert st == 0 and it1b == it1 and torch.equal(x1b, x1)
+    S2.close()
+    S1.close()
 
 
 @pytest.mark.parametrize("name", ["cfg4s", "cfg3s", "cfg2s"])

@@ -5,7 +5,7 @@ and stores what the GPU parity tests compare against (ASPCG protocol, PAPER.md:7
 relative residual <= 1e-8, Lanczos estimate from the same run's CG coefficients, R11/R12):
 
   iters, lmin, lmax, cond (K), the full alpha/beta history, the relative residual history,
-  ||b||, a checksum of b (the test feeds the oracle's b to the GPU and checks it is this b),
+  ||b||, a checksum of b, b on the sampled dofs (the test feeds the oracle's b to the GPU and checks it is this b),
   x on the dofs of >= 8 fixed subdomains (interior, boundary, extreme rho) at iterations
   iters-2 .. iters+2 (the oracle runs 2 iterations past its stop test), and ||x_{iters+2}||.
 
@@ -71,7 +71,7 @@ def run(name, threads):
         name=name, N=o.N, N0=o.N0, iters=it, iters_run=h["iters_run"],
         lmin=h["lmin"], lmax=h["lmax"], cond=h["cond"],
         alphas=h["alphas"], betas=h["betas"], resid=h["resid"],
-        bnorm=np.linalg.norm(b), b_sum=b.sum(), b_abs_sum=np.abs(b).sum(),
+        bnorm=np.linalg.norm(b), b_sum=b.sum(), b_abs_sum=np.abs(b).sum(), b_idx=b[idx],
         subdomains=subs, idx=idx, hist_iters=hist_iters,
         hist=np.stack([h["hist"][j] for j in hist_iters]),
         xnorm_run=np.linalg.norm(h["x"]),
@@ -85,13 +85,28 @@ def run(name, threads):
           f"-> {path}", flush=True)
 
 
+def augment(name):
+    """Add b on the sampled dofs to an existing file (oracle rhs only, no PCG)."""
+    path = os.path.join(OUT, f"full_{name}.npz")
+    d = dict(np.load(path))
+    if "b_idx" in d:
+        return
+    P = problem(name)
+    b = O.Oracle(P).rhs()
+    assert abs(np.linalg.norm(b) - float(d["bnorm"])) <= 1e-14 * float(d["bnorm"])
+    d["b_idx"] = b[d["idx"]]
+    np.savez_compressed(path, **d)
+    print(f"{name}: b_idx added", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--threads", type=int, default=os.cpu_count())
+    ap.add_argument("--augment", action="store_true", help="only add b_idx to existing files")
     ap.add_argument("names", nargs="*", default=NAMES)
     a = ap.parse_args()
     for n in a.names:
-        run(n, a.threads)
+        augment(n) if a.augment else run(n, a.threads)
 
 
 if __name__ == "__main__":
