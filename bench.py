@@ -91,50 +91,110 @@ def aggregate(ms, iters, world, device="cpu"):
     return float(mx[0]), float(sm[1])
 
 
-def cpu_baseline(name, P=None, max_sub=8):
-    """The oracle as it stands, on a bounded sample of the same workload (see `sample`)."""
-    import numpy as np
+def host_info():
+    model = ""
+    try:
+        for l in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=20).stdout.splitlines():
+            if l.startswith("Model name"):
+                model = l.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
 
-    import dgas_gen
-    import oracle
+
+def l2_policy(P):
+    """Deterministic from the problem (both arms print the same config): the operators of one PCG
+    iteration (A and the local factors, >= ~12 n_p-blocks per cell) against the B200's 126 MB L2."""
+    est = 12 * P.N * P.n_p * 8
+    if est > 126e6:
+        return f"inputs larger than L2 (operators ~{est / 1e9:.2f} GB > 126 MB L2; no flush needed)"
+    return f"L2-resident (operators ~{est / 1e6:.1f} MB fit the 126 MB L2; L2 flushed before every timed solve)"
+
+
+def problem_config(name, P):
+    return {"workload": name, "N": P.N, "N0": P.N0, "p": P.p, "q": P.q, "n_cells": P.n_cells,
+            "n_subdomains": P.n_sub, "n_coarse": P.n_coarse, "rtol": 1e-8, "maxit": 5000, "x0": "zero",
+            "l2_policy": l2_policy(P)}
+
+
+class OracleSample:
+    """The oracle (oracle/, test infrastructure) as it stands, timed on a bounded sample of one PCG
+    iteration of the workload: the full SpMV, the full restriction + coarse solve (A0 factored in
+    full, untimed setup), the local solves + prolongation of `ns` spread subdomains scaled to all
+    n_sub, and the iteration's vector ops (3 axpys, 2 dots). Threads: OpenMP over subdomains."""
+
+    def __init__(self, name, P, ns):
+        import numpy as np
+
+        import dgas_gen
+        import oracle
+        self.oracle = oracle
+        self.P = P
+        self.sub = sorted(set(np.linspace(0, P.n_sub - 1, min(ns, P.n_sub)).astype(int).tolist()))
+        t0 = time.time()
+        self.o = oracle.Oracle(P)
+        self.o.setup_schwarz(sample=self.sub)
+        self.t_setup = time.time() - t0
+        self.x = dgas_gen.normal(1, self.o.N)
+
+    def iteration_seconds(self, threads, reps=2):
+        import numpy as np
+        self.oracle.set_threads(threads)
+        o, x, sub = self.o, self.x, self.sub
+
+        def best(f):
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter(); f(); ts.append(time.perf_counter() - t0)
+            return min(ts)
+        t_spmv = best(lambda: o.spmv(x))
+        t_coarse = best(lambda: o.apply_sampled(x, []))           # restriction + coarse solve
+        t_cs = best(lambda: o.apply_sampled(x, sub))              # + local solves, prolongation (sample)
+        v = x.copy()
+
+        def vec():
+            v[:] += 0.5 * x; v[:] -= 0.25 * x; float(v @ x); v[:] = x + 0.1 * v; float(v @ v)
+        t_vec = best(vec)
+        return t_spmv + t_coarse + max(0.0, t_cs - t_coarse) * self.P.n_sub / len(self.sub) + t_vec
+
+    def sample_text(self, name):
+        return (f"{name}: one oracle PCG iteration = SpMV over all {self.P.n_cells} cells + restriction and "
+                f"{'band' if self.P.N0 > 8192 else 'dense'}-Cholesky coarse solve of all N0 = {self.P.N0} + "
+                f"dense-Cholesky local solves and prolongation of {len(self.sub)}/{self.P.n_sub} spread "
+                f"subdomains scaled to all + vector ops (setup {self.t_setup:.0f}s untimed)")
+
+
+def cpu_baseline(name, P=None):
+    """Reported baseline (never the target): all host cores (OpenMP) and one core."""
     P = _problem(name) if P is None else P
-    t0 = time.time()
-    o = oracle.Oracle(P)
-    t_asm = time.time() - t0
-    sub = list(range(min(max_sub, P.n_sub)))
-    o.setup_schwarz(use_coarse=False, sample=sub)
-    x = dgas_gen.normal(1, o.N)
-    t0 = time.perf_counter(); o.spmv(x); t_spmv = time.perf_counter() - t0
-    t0 = time.perf_counter(); o.apply_sampled(x, sub); t_loc = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    v = x.copy()
-    for _ in range(3):  # the 3 axpys + 2 dots of one Hestenes–Stiefel iteration, in numpy
-        v += 0.5 * x; float(v @ x)
-    t_vec = time.perf_counter() - t0
-    t_iter = t_spmv + t_loc * P.n_sub / len(sub) + t_vec
-    return {"value": 1.0 / t_iter, "unit": "PCG it/s", "cores": 1, "kind": "oracle",
-            "sample": (f"{name}: oracle SpMV over all {P.n_cells} cells + dense-Cholesky local solves of "
-                       f"{len(sub)}/{P.n_sub} subdomains scaled to all + vector ops, per PCG iteration; "
-                       f"coarse solve excluded (oracle setup of A0 for this size not in the sample); "
-                       f"oracle assembly {t_asm:.1f}s not timed"),
-            "seconds_per_iter": t_iter}
+    nproc = os.cpu_count() or 1
+    smp = OracleSample(name, P, ns=max(8, min(64, 2 * nproc)))
+    t_all = smp.iteration_seconds(nproc)
+    t_one = smp.iteration_seconds(1)
+    return {"value": 1.0 / t_all, "unit": "PCG it/s", "cores": nproc, "kind": "oracle",
+            "sample": smp.sample_text(name), "host": host_info(),
+            "single_core": {"value": 1.0 / t_one, "unit": "PCG it/s", "cores": 1}}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands on the host cores (this tier's reference arm)."""
     if rank != 0:
         return
     name = args.config
-    per = []
     P = _problem(name)
-    for _ in range(max(1, args.steps)):
-        per.append(cpu_baseline(name, P)["seconds_per_iter"])
+    nproc = os.cpu_count() or 1
+    smp = OracleSample(name, P, ns=max(8, min(64, 2 * nproc)))
+    for _ in range(args.warmup):
+        smp.iteration_seconds(nproc, reps=1)
+    per = [smp.iteration_seconds(nproc, reps=1) for _ in range(max(1, args.steps))]
     v = 1.0 / (sum(per) / len(per))
-    cb = cpu_baseline(name, P)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "PCG it/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": name},
-            "cpu_baseline": {**{k: cb[k] for k in ("unit", "cores", "kind", "sample")}, "value": v},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(per) / len(per),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": problem_config(name, P),
+            "cpu_baseline": {"value": v, "unit": "PCG it/s", "cores": nproc, "kind": "oracle",
+                             "sample": smp.sample_text(name), "host": host_info()},
             "e2e": {"value": v, "unit": "PCG it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -144,7 +204,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))  # the largest BASELINE config
     ap.add_argument("--impl", default="dgas", choices=["dgas", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20)
@@ -186,19 +246,27 @@ def main():
     iters_total = 0
     iters_list = []
     conds = []
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # L2-resident workloads (config 1, 2, small config-5 pairs): flush L2 before every timed step by
+    # writing a buffer twice its size (outside the step's events); larger workloads need no flush
+    flush = None
+    if l2_policy(P).startswith("L2-resident"):
+        flush = torch.empty(2 * torch.cuda.get_device_properties(local).L2_cache_size // 4, dtype=torch.float32,
+                            device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with Clocks(local) as clk:
         barrier()
-        e0.record()
-        for _ in range(args.steps):
+        for k in range(args.steps):
             x.zero_()
+            if flush is not None:
+                flush.fill_(float(k))
+            ev[k][0].record()
             _, it, cond, st = S.pcg(b, x)
+            ev[k][1].record()
             iters_total += it
             iters_list.append(it)
             conds.append(cond)
-        e1.record()
         barrier()
-    ms = e0.elapsed_time(e1)
+    ms = sum(a.elapsed_time(c) for a, c in ev)
     ms, iters_all = aggregate(ms, iters_total, world, device="cuda")
     value = iters_all / (ms / 1e3)
     iters_per_solve = iters_total / args.steps
@@ -245,6 +313,18 @@ def main():
     }
     kern = {nm: {"ms": kt[nm], "alg_bytes": alg[nm], "GBps": alg[nm] / (kt[nm] * 1e-3) / 1e9,
                  "frac": alg[nm] / (kt[nm] * 1e-3) / 1e9 / hbm_peak} for nm in kt}
+    # SURVEY §8(d) algorithmic minimum: A as its symmetric half (diagonal blocks' lower triangles, every
+    # coupled pair once) next to the full block-CSR the kernel streams
+    nnzb, nh = info["nnz_blocks"], info["n_cells"]
+    a_sym = 8 * (nh * npp * (npp + 1) // 2 + (nnzb - nh) // 2 * npp * npp)
+    kern["spmv"]["alg_bytes_sym_half"] = a_sym + 2 * N * 8
+    kern["spmv"]["frac_sym_half"] = (a_sym + 2 * N * 8) / (kt["spmv"] * 1e-3) / 1e9 / hbm_peak
+    # B_env of one PCG iteration: A symmetric half, local envelope factor once, coarse
+    # factor (x refinement passes), Q twice, ~10 N vector entries; t_env = B_env / peak
+    refine = info["coarse_refine"]
+    b_env = (a_sym + info["bytes_U"] + dinv_tri + info["bytes_coarse"] * (1 + refine) + 2 * info["bytes_G"]
+             + 10 * N * 8)
+    t_iter_ms = ms / max(1, iters_total)
     dom = "local" if kt["local"] >= kt["spmv"] else "spmv"
     traffic = None
     try:
@@ -258,16 +338,19 @@ def main():
         "metric": METRIC, "value": value, "unit": "PCG it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "N": N, "N0": N0, "p": S.p, "q": S.q, "n_cells": info["n_cells"],
-                   "n_subdomains": info["n_subdomains"], "n_coarse": info["n_coarse"], "rtol": 1e-8,
-                   "iters_per_solve": iters_per_solve, "lanczos_cond": conds[-1] if conds else None,
-                   "l2_policy": (f"inputs larger than L2: operator bytes "
-                                 f"{(info['bytes_A'] + info['bytes_U'] + info['bytes_coarse']) / 1e9:.2f} GB "
-                                 f"> 126 MB L2"),
-                   "parallelism": "replicas" if world > 1 else "single-gpu", "setup_s": t_setup,
-                   "coarse_solver": ["dense-inverse", "band", "nested-dissection"][info["coarse_mode"]],
-                   "local_kernel": {1: "envelope", 2: "panel"}.get(info["local_kernel"]),
-                   "local_ctas_per_sm": info["local_ctas_per_sm"]},
+        "config": problem_config(args.config, P),
+        "run": {"iters_per_solve": iters_per_solve, "lanczos_cond": conds[-1] if conds else None,
+                "parallelism": "replicas" if world > 1 else "single-gpu", "setup_s": t_setup,
+                "coarse_solver": ["dense-inverse", "band", "nested-dissection"][info["coarse_mode"]],
+                "coarse_refine_steps": refine, "coarse_solve_relerr": info["coarse_solve_relerr"],
+                "local_kernel": {1: "envelope", 2: "panel"}.get(info["local_kernel"]),
+                "local_ctas_per_sm": info["local_ctas_per_sm"],
+                "operator_bytes": info["bytes_A"] + info["bytes_U"] + info["bytes_coarse"] + info["bytes_G"],
+                "l2_bytes": torch.cuda.get_device_properties(local).L2_cache_size},
+        "algorithmic_roofline_per_iter": {
+            "B_env_bytes": b_env, "t_env_ms": b_env / (hbm_peak * 1e9) * 1e3, "t_measured_ms": t_iter_ms,
+            "t_env_over_t_measured": b_env / (hbm_peak * 1e9) * 1e3 / t_iter_ms,
+            "note": "SURVEY §8(d) B_env (A symmetric half, envelope factor read once) at the measured HBM peak"},
         "dof_iters_per_s": value * N / max(world, 1) * world,
         "ms_per_apply": kt["apply_total"],
         "spmv_apply_hbm_gbs": spmv_apply_gbs,

@@ -91,8 +91,9 @@ typedef struct {
   int32_t coarse_mode;           /* 0 dense explicit inverse, 1 band, 2 nested dissection */
   int32_t launches_per_iter;     /* kernel launches of one PCG iteration (graph body) */
   int32_t launches_per_solve;    /* fixed launches of one dgas_pcg besides the iterations */
-  int32_t coarse_refine;         /* iterative-refinement steps of the ND coarse solve (R30 calibration) */
-  double coarse_solve_relerr;    /* measured ||z - v|| / ||v|| of one coarse solve of A0 z = A0 v (ND only) */
+  int32_t coarse_refine;         /* iterative-refinement steps of the coarse solve (dense or ND; R30 calibration) */
+  double coarse_solve_relerr;    /* measured ||z - v|| / ||v|| of one coarse solve of A0 z = A0 v (dense or ND;
+                                    refinement steps are added while it exceeds 3e-11) */
   int32_t unroll;                /* PCG iterations per execution of the graph's WHILE body; the last body of a
                                     solve launches its remaining copies as immediate-return kernels */
   int32_t local_kernel;          /* 1: envelope kernel (all subdomains resident); 2: panel kernel (few CTAs
@@ -148,7 +149,8 @@ int dgas_history(dgas_ctx ctx, double* alphas, double* betas, int cap);
 
 /* Diagnostics (host outputs, caller order): the A block coupling caller cells (i, j) (n_p x n_p,
  * zero if not coupled; returns 1 if stored), the basis coefficients of cell i (n_p x n_p, over the
- * bbox-Legendre products of R6), the dense A0 (N0 x N0, only when coarse_dense). */
+ * bbox-Legendre products of R6), the assembled A0 = Q^T A Q densely (N0 x N0, row-major; any coarse
+ * mode; caller allocates N0*N0 doubles). */
 int dgas_debug_block(dgas_ctx ctx, int32_t i, int32_t j, double* out);
 int dgas_debug_basis(dgas_ctx ctx, int32_t i, double* out);
 int dgas_debug_A0(dgas_ctx ctx, double* out);

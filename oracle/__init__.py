@@ -50,8 +50,10 @@ def lib():
         L.or_apply.argtypes = [_P, _P, _P]
         L.or_apply_ld.argtypes = [_P, _P, _P]
         L.or_apply_sampled.argtypes = [_P, ctypes.c_int, _P, _P, _P]
+        L.or_apply_sampled_ld.argtypes = [_P, ctypes.c_int, _P, _P, _P]
         L.or_set_refine.argtypes = [_P, ctypes.c_int]
         L.or_set_perturb.argtypes = [_P, ctypes.c_double, ctypes.c_uint64]
+        L.or_perturb_A.argtypes = [_P, ctypes.c_double, ctypes.c_uint64]
         L.or_get_G.argtypes = [_P, _P]
         L.or_get_A0.argtypes = [_P, _P]
         L.or_coarse_basis.argtypes = [_P, ctypes.c_int, _P, _P]
@@ -201,11 +203,16 @@ class Oracle:
         """Relative perturbation of G before A0 is formed (sensitivity probe, R30)."""
         lib().or_set_perturb(self.h, eps, seed)
 
-    def apply_sampled(self, r, sample):
+    def perturb_A(self, eps, seed=1):
+        """A <- A (1 + eps u), symmetric (sensitivity probe, R22/R30); before setup_schwarz."""
+        lib().or_perturb_A(self.h, eps, seed)
+
+    def apply_sampled(self, r, sample, long_double=False):
         r = np.ascontiguousarray(r, dtype=np.float64)
         s = np.ascontiguousarray(sample, np.int32)
         z = np.zeros(self.N)
-        st = lib().or_apply_sampled(self.h, s.shape[0], _ptr(s), _ptr(r), _ptr(z))
+        f = lib().or_apply_sampled_ld if long_double else lib().or_apply_sampled
+        st = f(self.h, s.shape[0], _ptr(s), _ptr(r), _ptr(z))
         if st:
             raise OracleError(st, "sampled apply failed")
         return z

@@ -847,27 +847,29 @@ int apply_t(Ctx* c, const Factors<T>& F, const double* r, double* z, const std::
         for (int a = 0; a < np; ++a) s += (T)c->G[o][a * nq + b] * (T)r[(int64_t)c->ov_fine[o] * np + a];
         r0[(int64_t)c->ov_coarse[o] * nq + b] += s;
       }
-    if (F.band < 0) chol_solve((int)N0, F.L0, r0);
+    if (c->F.band < 0) chol_solve((int)N0, F.L0, r0);
     else {
-      if constexpr (std::is_same<T, double>::value) {
-        std::vector<double> b0(r0.begin(), r0.end());
-        band_solve(N0, F.band, F.L0, r0);
-        for (int it = 0; it < c->refine; ++it) {  // DESIGN.md R30: residual in long double, one more solve
-          const int bw = F.band;
-          const int64_t ld = bw + 1;
-          std::vector<double> res(N0);
-          for (int64_t i = 0; i < N0; ++i) {
-            long double s = b0[i];
-            for (int64_t j = std::max<int64_t>(0, i - bw); j <= std::min<int64_t>(N0 - 1, i + bw); ++j) {
-              double a = j <= i ? c->A0band[i * ld + (j - i + bw)] : c->A0band[j * ld + (i - j + bw)];
-              s -= (long double)a * r0[j];
-            }
-            res[i] = (double)s;
+      // band path (N0 > dense_max): the fp64 band factor, plus c->refine refinement steps with a
+      // long-double residual (R30). The long-double apply (T = long double) uses the same
+      // refined fp64 band solve for its coarse part (no long-double band factor is kept).
+      const int bw = c->F.band;
+      const int64_t ld = bw + 1;
+      std::vector<double> b0(r0.begin(), r0.end()), x0(b0);
+      band_solve(N0, bw, c->F.L0, x0);
+      for (int it = 0; it < c->refine; ++it) {
+        std::vector<double> res(N0);
+        for (int64_t i = 0; i < N0; ++i) {
+          long double s = b0[i];
+          for (int64_t j = std::max<int64_t>(0, i - bw); j <= std::min<int64_t>(N0 - 1, i + bw); ++j) {
+            double a = j <= i ? c->A0band[i * ld + (j - i + bw)] : c->A0band[j * ld + (i - j + bw)];
+            s -= (long double)a * x0[j];
           }
-          band_solve(N0, F.band, F.L0, res);
-          for (int64_t i = 0; i < N0; ++i) r0[i] += res[i];
+          res[i] = (double)s;
         }
-      } else return -2;
+        band_solve(N0, bw, c->F.L0, res);
+        for (int64_t i = 0; i < N0; ++i) x0[i] += res[i];
+      }
+      for (int64_t i = 0; i < N0; ++i) r0[i] = (T)x0[i];
     }
     for (size_t o = 0; o < c->G.size(); ++o) {  // z += Q z0
       int f = c->ov_fine[o];
@@ -891,11 +893,39 @@ int or_apply_ld(void* h, const double* r, double* z) { return apply_t(((Ctx*)h),
 // apply restricted to the dofs of the listed subdomains (others left 0): sampled full-size parity
 void or_set_refine(void* h, int steps) { ((Ctx*)h)->refine = steps; }
 void or_set_perturb(void* h, double eps, uint64_t seed) { ((Ctx*)h)->perturb = eps; ((Ctx*)h)->perturb_seed = seed; }
+// Sensitivity probe (R22/R30): A <- A (1 + eps u), u uniform in [-1, 1] from a hash of the unordered entry,
+// so A stays symmetric. Models two correct assemblies of A that differ by ~kappa(Gram) eps (the basis is a
+// CholQR2 of a Gram matrix). Call before setup_schwarz; the SpMV and every factor then use the result.
+void or_perturb_A(void* h, double eps, uint64_t seed) {
+  Ctx* c = (Ctx*)h;
+  const int np = c->np;
+  for (int i = 0; i < c->nc; ++i)
+    for (auto& kv : c->A[i]) {
+      const int j = kv.first;
+      for (int a = 0; a < np; ++a)
+        for (int b = 0; b < np; ++b) {
+          uint64_t k0 = (uint64_t)std::min(i, j), k1 = (uint64_t)std::max(i, j);
+          int aa = i < j ? a : i > j ? b : std::min(a, b), bb = i < j ? b : i > j ? a : std::max(a, b);
+          uint64_t z = seed * 0x9e3779b97f4a7c15ULL ^ (k0 * 1000003ULL + k1) * 0xbf58476d1ce4e5b9ULL ^
+                       (uint64_t)(aa * 64 + bb) * 0x94d049bb133111ebULL;
+          z ^= z >> 31; z *= 0xbf58476d1ce4e5b9ULL; z ^= z >> 27; z *= 0x94d049bb133111ebULL; z ^= z >> 31;
+          const double u = (double)(z >> 11) * (1.0 / 9007199254740992.0) * 2 - 1;
+          kv.second[a * np + b] *= 1 + eps * u;
+        }
+    }
+}
 int or_apply_sampled(void* h, int n_sample, const int* sample, const double* r, double* z) {
   Ctx* c = (Ctx*)h;
   std::vector<char> only(c->nsub, 0);
   for (int k = 0; k < n_sample; ++k) only[sample[k]] = 1;
   return apply_t(c, c->F, r, z, &only);
+}
+// the same in long double (setup_schwarz with long_double_too; Z30 / DESIGN.md R30 reference)
+int or_apply_sampled_ld(void* h, int n_sample, const int* sample, const double* r, double* z) {
+  Ctx* c = (Ctx*)h;
+  std::vector<char> only(c->nsub, 0);
+  for (int k = 0; k < n_sample; ++k) only[sample[k]] = 1;
+  return apply_t(c, c->FL, r, z, &only);
 }
 
 // G blocks (n_ov x np x nq) and dense A0 (N0 x N0, only if dense) for diagnostics

@@ -119,6 +119,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     if (st2) return st2;
     if ((st2 = nd_calibrate(ctx))) return st2;
   }
+
   if (const char* e = std::getenv("DGAS_UNROLL")) ctx->unroll = std::max(1, std::min(8, std::atoi(e)));
   {
     // chunked restriction: pieces of each coarse element in chunks of <= 8 warp steps (32/n_p pieces
@@ -171,6 +172,11 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     ctx->prolong_grid = per * nsm;
   }
   ctx->n_coarse_ctas = ctx->coarse_dense ? (int)std::min<int64_t>(592, std::max<int64_t>(1, ctx->N0 / 32)) : 1;
+  if (ctx->coarse_mode == 0) {  // calibrated refinement of the dense coarse solve (R30, Z30)
+    if (const char* e = std::getenv("DGAS_ND_TOL")) ctx->nd_tol = std::atof(e);
+    int st2 = dense_calibrate(ctx);
+    if (st2) return st2;
+  }
   {
     // TMA ring of the local-solve CTAs: unit = CC columns of a row-block (about the average row-block
     // for n_p = 15), S slots; 128-thread CTAs target ~55 KB (3-4 CTAs/SM), 256-thread ~110 KB.
@@ -598,8 +604,8 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->alg_bytes_spmv = info->bytes_A + (2 * N) * 8 + (int64_t)ctx->nnzb * 4;
   const int64_t dinv_tri = (int64_t)ctx->nc * (np * (np + 1) / 2) * 8;
   // refinement steps of the ND coarse solve re-read the factors and read the A0 pair blocks once more
-  const int refine = ctx->coarse_mode == 2 ? ctx->nd.refine : 0;
-  const int64_t a0b = (int64_t)(ctx->nd.h_prow.empty() ? 0 : ctx->nd.h_prow.back()) * nq * nq * 8;
+  const int refine = ctx->coarse_mode == 2 ? ctx->nd.refine : ctx->coarse_mode == 0 ? ctx->dense_refine : 0;
+  const int64_t a0b = ctx->n_pairs * nq * nq * 8;
   const int64_t coarse_alg = info->bytes_coarse * (1 + refine) + refine * a0b;
   info->alg_bytes_apply = info->bytes_U + dinv_tri + coarse_alg + 2 * info->bytes_G + 3 * N * 8;
   info->alg_bytes_iter = info->bytes_A + info->bytes_U + dinv_tri + coarse_alg + 2 * info->bytes_G + 16 * N * 8;
@@ -607,12 +613,12 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->last_cond = ctx->last_cond; info->last_lmin = ctx->last_lmin; info->last_lmax = ctx->last_lmax;
   info->last_relres = ctx->last_relres;
   info->coarse_mode = ctx->coarse_mode;
-  info->coarse_refine = ctx->coarse_mode == 2 ? ctx->nd.refine : 0;
+  info->coarse_refine = refine;
   info->unroll = ctx->unroll;
   info->local_kernel = ctx->local_kernel;
   info->local_ctas_per_sm = ctx->local_kernel == 2 ? ctx->panel_cps : 0;
-  info->coarse_solve_relerr = ctx->coarse_mode == 2 ? ctx->nd.calib_err : 0.0;
-  int coarse_launches = 1;
+  info->coarse_solve_relerr = ctx->coarse_mode == 2 ? ctx->nd.calib_err : ctx->coarse_mode == 0 ? ctx->dense_err : 0.0;
+  int coarse_launches = 1 + 3 * (ctx->coarse_mode == 0 ? ctx->dense_refine : 0);
   if (ctx->coarse_mode == 2) {
     coarse_launches = 0;
     for (int L = 0; L < ctx->nd.nlev; ++L) {
@@ -654,26 +660,17 @@ extern "C" int dgas_debug_basis(dgas_ctx ctx, int32_t i, double* out) {
 
 extern "C" int dgas_debug_A0(dgas_ctx ctx, double* out) {
   if (!ctx || !out) return DGAS_E_INVALID_ARG;
-  if (!ctx->coarse_dense && ctx->coarse_mode != 1) return DGAS_E_INVALID_ARG;
-  // the tile storage holds the Cholesky factor after setup: return L L^T (lower tiles) densely
-  const int nT = ctx->nT, bt = ctx->bt;
-  std::vector<double> t((size_t)nT * (bt + 1) * CT * CT);
-  DGAS_CUDA(cudaMemcpy(t.data(), ctx->d_A0t, t.size() * sizeof(double), cudaMemcpyDeviceToHost));
-  const int64_t N0 = ctx->N0, NP = (int64_t)nT * CT;
-  std::vector<double> L((size_t)NP * NP, 0.0);
-  for (int I = 0; I < nT; ++I)
-    for (int K = std::max(0, I - bt); K <= I; ++K)
-      for (int a = 0; a < CT; ++a)
-        for (int b = 0; b < CT; ++b) {
-          int64_t r = (int64_t)I * CT + a, c = (int64_t)K * CT + b;
-          if (c <= r) L[r * NP + c] = t[((size_t)I * (bt + 1) + (K - I + bt)) * CT * CT + a * CT + b];
-        }
-  for (int64_t r = 0; r < N0; ++r)
-    for (int64_t c = 0; c < N0; ++c) {
-      double s = 0;
-      for (int64_t k = 0; k <= std::min(r, c); ++k) s += L[r * NP + k] * L[c * NP + k];
-      out[r * N0 + c] = s;
-    }
+  // A0 = Q^T A Q as assembled (eq:A0): the coupled-pair blocks, before any scaling or factorisation
+  const int64_t N0 = ctx->N0, nq = ctx->nq, np_ = ctx->n_pairs;
+  std::vector<int> pair((size_t)2 * np_);
+  std::vector<double> blk((size_t)np_ * nq * nq);
+  DGAS_CUDA(cudaMemcpy(pair.data(), ctx->d_pair, pair.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  DGAS_CUDA(cudaMemcpy(blk.data(), ctx->d_A0b, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  std::fill(out, out + N0 * N0, 0.0);
+  for (int64_t k = 0; k < np_; ++k)
+    for (int a = 0; a < nq; ++a)
+      for (int c = 0; c < nq; ++c)
+        out[((int64_t)pair[2 * k] * nq + a) * N0 + (int64_t)pair[2 * k + 1] * nq + c] = blk[((size_t)k * nq + a) * nq + c];
   return DGAS_OK;
 }
 

@@ -293,6 +293,23 @@ __global__ void __launch_bounds__(256) k_lauum(int nT, int bt, int64_t N0, int64
   }
 }
 
+// dense path: factor the symmetrically scaled D^-1/2 A0 D^-1/2 (D = diag A0; config-4-like rho
+// jumps put kappa(A0) at 8e8 and kappa of the scaled matrix at 9e6) and fold the scaling back into X
+__global__ void k_scale_tiles(int64_t N0, int nT, int bt, const double* __restrict__ dsc, double* A0t) {
+  const int I = blockIdx.x, K = I - bt + (int)blockIdx.y;
+  if (K < 0) return;
+  double* t = A0t + ((size_t)I * (bt + 1) + (K - I + bt)) * CT * CT;
+  for (int e = threadIdx.x; e < CT * CT; e += blockDim.x) {
+    const int64_t r = (int64_t)I * CT + e / CT, c = (int64_t)K * CT + e % CT;
+    if (r < N0 && c < N0) t[e] *= dsc[r] * dsc[c];
+  }
+}
+__global__ void k_scale_X(int64_t N0, int64_t ldX, const double* __restrict__ dsc, double* X) {
+  const int64_t r = blockIdx.x;
+  const double dr = dsc[r];
+  for (int64_t c = threadIdx.x; c < N0; c += blockDim.x) X[r * ldX + c] *= dr * dsc[c];
+}
+
 // ------------------------------------------------------------------ launcher
 int coarse_setup_run(dgas_ctx ctx) {
   cudaStream_t s = ctx->stream;
@@ -321,6 +338,10 @@ int coarse_setup_run(dgas_ctx ctx) {
   }
   k_pad<<<1, CT, 0, s>>>(ctx->N0, ctx->nT, ctx->bt, ctx->d_A0t);
   const int nT = ctx->nT, bt = ctx->bt;
+  if (ctx->coarse_dense) {
+    launch_a0_diag(ctx, ctx->d_prow, ctx->d_dsc0, s);
+    k_scale_tiles<<<dim3(nT, bt + 1), 256, 0, s>>>(ctx->N0, nT, bt, ctx->d_dsc0, ctx->d_A0t);
+  }
   for (int K = 0; K < nT; ++K) {
     k_potrf<<<1, 256, 0, s>>>(K, bt, ctx->d_A0t, ctx->d_Dinv0, ctx->d_err);
     int nb = std::min(bt, nT - 1 - K);
@@ -333,6 +354,7 @@ int coarse_setup_run(dgas_ctx ctx) {
   if (ctx->coarse_dense) {
     for (int I = 0; I < nT; ++I) k_trtri_row<<<I + 1, 256, 0, s>>>(I, bt, ctx->d_A0t, ctx->d_Dinv0, ctx->d_W);
     k_lauum<<<dim3(nT, nT), 256, 0, s>>>(nT, bt, ctx->N0, ctx->ldX, ctx->d_W, ctx->d_X);
+    k_scale_X<<<(unsigned)ctx->N0, 256, 0, s>>>(ctx->N0, ctx->ldX, ctx->d_dsc0, ctx->d_X);
     DGAS_CUDA(cudaGetLastError());
   }
   int herr[8];

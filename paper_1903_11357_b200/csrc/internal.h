@@ -79,6 +79,12 @@ struct dgas_ctx_s {
   int nd_grid = 1 << 30;     // max CTAs per ND solve level (grid-stride over work items; DGAS_ND_GRID)
   int nd_l2 = 1;             // ND solve operator loads evict-last in L2 (DGAS_ND_L2)
   double nd_tol = 3e-11;     // coarse-solve relative error above which refinement steps are added (Z30; DGAS_ND_TOL)
+  // dense coarse path: symmetric diagonal scaling and calibrated refinement (as the ND path, R30)
+  int* d_prow = nullptr;     // coarse pair rows (pairs sorted by (J1, J2)), every coarse mode
+  double* d_dsc0 = nullptr;  // diag(A0)^-1/2
+  double *d_rb0 = nullptr, *d_zb0 = nullptr;  // refinement residual / correction (N0)
+  int dense_refine = 0;
+  double dense_err = 0, dense_err0 = 0;
   NdPlan nd;
   double* d_A0b = nullptr;   // A0 blocks per coarse pair (n_pairs x nq x nq)
   int max_sub_cells = 0, max_urow = 0, max_deg = 0;
@@ -288,6 +294,12 @@ int nd_setup_run(dgas_ctx ctx);
 void nd_solve_launch(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s);
 int nd_set_smem(dgas_ctx ctx);
 int nd_calibrate(dgas_ctx ctx);
+int dense_calibrate(dgas_ctx ctx);
+void launch_a0_diag(dgas_ctx ctx, const int* prow, double* dsc, cudaStream_t s);
+void launch_a0_resid(dgas_ctx ctx, const int* prow, const double* b, const double* z, double* res, const PcgState* st,
+                     int mode, cudaStream_t s);
+void launch_axpy_add(int64_t n, const double* a, double* y, const PcgState* st, int mode, cudaStream_t s);
+void launch_coarse_dense(dgas_ctx ctx, int mode, const PcgState* st, const double* r0, double* z0, cudaStream_t s);
 void nd_free(dgas_ctx ctx);
 int apply_set_smem(dgas_ctx ctx, size_t smem);
 size_t apply_smem_bytes(dgas_ctx ctx);

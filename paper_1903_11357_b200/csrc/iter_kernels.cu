@@ -1121,11 +1121,23 @@ __global__ void k_zfill(int mode, int copy, int64_t n, const double* r_in, doubl
     z[i] = copy ? r[i] : 0.0;
 }
 
+// dense / band coarse solve z0 = A0^-1 r0, plus the calibrated refinement steps of the dense path
+// (R30: z0 += X (r0 - A0 z0), residual from the A0 pair blocks)
+void launch_coarse_dense(dgas_ctx ctx, int mode, const PcgState* st, const double* r0, double* z0, cudaStream_t s) {
+  k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt, ctx->d_X,
+                                                ctx->d_A0t, ctx->d_Dinv0, r0, z0, st);
+  if (!ctx->coarse_dense) return;
+  for (int it = 0; it < ctx->dense_refine; ++it) {
+    launch_a0_resid(ctx, ctx->d_prow, r0, z0, ctx->d_rb0, st, mode, s);
+    k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(mode, 1, ctx->N0, ctx->ldX, ctx->nT, ctx->bt, ctx->d_X, ctx->d_A0t,
+                                                  ctx->d_Dinv0, ctx->d_rb0, ctx->d_zb0, st);
+    launch_axpy_add(ctx->N0, ctx->d_zb0, z0, st, mode, s);
+  }
+}
+
 static void launch_coarse_part(dgas_ctx ctx, int mode, PcgState* st, cudaStream_t s) {
   if (ctx->coarse_mode == 2) nd_solve_launch(ctx, mode, st, s);
-  else
-    k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(mode, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt,
-                                                  ctx->d_X, ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, st);
+  else launch_coarse_dense(ctx, mode, st, ctx->d_r0, ctx->d_z0, s);
 }
 
 // T_HH = T_h (the paper's regime): every subdomain is one cell, A_i^-1 = D^T D with
@@ -1208,8 +1220,7 @@ void launch_local_only(dgas_ctx ctx, const double* r, double* z, cudaStream_t s)
 
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s) {
   if (ctx->coarse_mode == 2) { nd_solve_launch(ctx, 0, nullptr, s); return; }
-  k_coarse<<<ctx->n_coarse_ctas, CO_T, 0, s>>>(0, ctx->coarse_dense, ctx->N0, ctx->ldX, ctx->nT, ctx->bt, ctx->d_X,
-                                                ctx->d_A0t, ctx->d_Dinv0, ctx->d_r0, ctx->d_z0, nullptr);
+  launch_coarse_dense(ctx, 0, nullptr, ctx->d_r0, ctx->d_z0, s);
 }
 
 void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s,

@@ -364,6 +364,18 @@ __global__ void k_axpy_add(int64_t n, const double* a, double* y, const PcgState
 
 static void nd_solve_once(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s, const double* rin, double* zout);
 
+void launch_a0_diag(dgas_ctx ctx, const int* prow, double* dsc, cudaStream_t s) {
+  k_nd_diag<<<(unsigned)((ctx->N0 + 255) / 256), 256, 0, s>>>(ctx->ncoarse, ctx->nq, prow, ctx->d_pair, ctx->d_A0b, dsc);
+}
+void launch_a0_resid(dgas_ctx ctx, const int* prow, const double* b, const double* z, double* res, const PcgState* st,
+                     int mode, cudaStream_t s) {
+  const int nb = (ctx->ncoarse + ND_T / 32 - 1) / (ND_T / 32);
+  k_a0_resid<<<nb, ND_T, 0, s>>>(ctx->ncoarse, ctx->nq, prow, ctx->d_pair, ctx->d_A0b, b, z, res, st, mode);
+}
+void launch_axpy_add(int64_t n, const double* a, double* y, const PcgState* st, int mode, cudaStream_t s) {
+  k_axpy_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, a, y, st, mode);
+}
+
 void nd_solve_launch(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s) {
   nd_solve_once(ctx, mode, st, s, ctx->d_r0, ctx->d_z0);
   for (int it = 0; it < ctx->nd.refine; ++it) {  // iterative refinement (R30)
@@ -414,9 +426,9 @@ __global__ void k_nd_testvec(int64_t n, double* v) {
 // configs 3 and 5 (4e-12, 1.2e-11) need none. A persistent dependency-driven single-launch solve and
 // a 4-rows-per-warp GEMV were tried for this and measured slower (beside the local solves only one
 // 256-thread CTA per SM fits, and both designs hold fewer loads in flight than this one).
-int nd_calibrate(dgas_ctx ctx) {
-  NdPlan& P = ctx->nd;
-  if (P.refine_env >= 0) return 0;
+// shared by both coarse paths: solve A0 z = A0 v (r0 = -A0 v, expect z = -v) with `refine` steps
+static int coarse_calibrate_impl(dgas_ctx ctx, const int* prow, int* refine_out, double* err_out, double* err0_out,
+                                 int* refine_ctl, void (*solve)(dgas_ctx, cudaStream_t)) {
   cudaStream_t s = ctx->stream;
   const int64_t n = ctx->N0;
   double *dv = nullptr, *dzero = nullptr;
@@ -424,15 +436,12 @@ int nd_calibrate(dgas_ctx ctx) {
   DGAS_CUDA(cudaMalloc((void**)&dzero, n * 8));
   DGAS_CUDA(cudaMemsetAsync(dzero, 0, n * 8, s));
   k_nd_testvec<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, dv);
-  const int nb = (ctx->ncoarse + ND_T / 32 - 1) / (ND_T / 32);
   std::vector<double> hv(n), hz(n);
   DGAS_CUDA(cudaMemcpyAsync(hv.data(), dv, n * 8, cudaMemcpyDeviceToHost, s));
   auto measure = [&](int refine) -> double {
-    P.refine = refine;
-    // r0 = 0 - A0 v, so the solve should return z0 = -v
-    k_a0_resid<<<nb, ND_T, 0, s>>>(ctx->ncoarse, ctx->nq, P.d_prow, ctx->d_pair, ctx->d_A0b, dzero, dv, ctx->d_r0,
-                                   nullptr, 0);
-    nd_solve_launch(ctx, 0, nullptr, s);
+    *refine_ctl = refine;
+    launch_a0_resid(ctx, prow, dzero, dv, ctx->d_r0, nullptr, 0, s);
+    solve(ctx, s);
     if (cudaMemcpyAsync(hz.data(), ctx->d_z0, n * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
     if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
     double e = 0, vv = 0;
@@ -440,7 +449,7 @@ int nd_calibrate(dgas_ctx ctx) {
     return std::sqrt(e / vv);
   };
   double err = measure(0);
-  P.calib_err0 = err;
+  *err0_out = err;
   int best = 0;
   for (int r = 1; r <= 2 && err > ctx->nd_tol; ++r) {
     const double e = measure(r);
@@ -448,16 +457,39 @@ int nd_calibrate(dgas_ctx ctx) {
     err = e;
     best = r;
   }
-  P.refine = best;
-  P.calib_err = err;
-  if (std::getenv("DGAS_VERBOSE"))
-    fprintf(stderr, "dgas: ND coarse solve relerr %.3e unrefined, %.3e with %d refinement step(s)\n", P.calib_err0, err,
-            best);
+  *refine_ctl = best;
+  *refine_out = best;
+  *err_out = err;
   cudaFree(dv);
   cudaFree(dzero);
   DGAS_CUDA(cudaMemsetAsync(ctx->d_z0, 0, n * 8, s));
   DGAS_CUDA(cudaGetLastError());
   return err >= 0 ? 0 : DGAS_E_CUDA;
+}
+
+static void nd_solve_plain(dgas_ctx ctx, cudaStream_t s) { nd_solve_launch(ctx, 0, nullptr, s); }
+static void dense_solve_plain(dgas_ctx ctx, cudaStream_t s) { launch_coarse_dense(ctx, 0, nullptr, ctx->d_r0, ctx->d_z0, s); }
+
+int nd_calibrate(dgas_ctx ctx) {
+  NdPlan& P = ctx->nd;
+  if (P.refine_env >= 0) return 0;
+  int r = 0;
+  int st = coarse_calibrate_impl(ctx, P.d_prow, &r, &P.calib_err, &P.calib_err0, &P.refine, nd_solve_plain);
+  if (std::getenv("DGAS_VERBOSE"))
+    fprintf(stderr, "dgas: ND coarse solve relerr %.3e unrefined, %.3e with %d refinement step(s)\n", P.calib_err0,
+            P.calib_err, P.refine);
+  return st;
+}
+
+int dense_calibrate(dgas_ctx ctx) {
+  int r = 0;
+  int st = coarse_calibrate_impl(ctx, ctx->d_prow, &r, &ctx->dense_err, &ctx->dense_err0, &ctx->dense_refine,
+                                 dense_solve_plain);
+  if (const char* e = std::getenv("DGAS_DENSE_REFINE")) ctx->dense_refine = std::max(0, std::atoi(e));
+  if (std::getenv("DGAS_VERBOSE"))
+    fprintf(stderr, "dgas: dense coarse solve relerr %.3e unrefined, %.3e with %d refinement step(s)\n",
+            ctx->dense_err0, ctx->dense_err, ctx->dense_refine);
+  return st;
 }
 
 int nd_set_smem(dgas_ctx ctx) {

@@ -531,6 +531,16 @@ extern "C" int dgas_setup(dgas_ctx* out, const dgas_mesh* mesh, int p, const int
   if ((st = dev_upload(ctx, &ctx->d_contrib_ptr, cptr_h))) return bail(st, ctx->detail);
   if ((st = dev_upload(ctx, &ctx->d_contrib, contrib))) return bail(st, ctx->detail);
   if ((st = dev_alloc(ctx, &ctx->d_A0b, (size_t)std::max<int64_t>(1, ctx->n_pairs) * nq * nq))) return bail(st, ctx->detail);
+  {
+    // pair rows of A0 (pairs are sorted by (J1, J2)): residuals of the refinement steps, diagonal scaling
+    std::vector<int> prow(ctx->ncoarse + 1, 0);
+    for (size_t k = 0; k < pair_h.size() / 2; ++k) prow[pair_h[2 * k] + 1]++;
+    for (int J = 0; J < ctx->ncoarse; ++J) prow[J + 1] += prow[J];
+    if ((st = dev_upload(ctx, &ctx->d_prow, prow))) return bail(st, ctx->detail);
+    if ((st = dev_alloc(ctx, &ctx->d_dsc0, (size_t)ctx->N0 + 1))) return bail(st, ctx->detail);
+    if ((st = dev_alloc(ctx, &ctx->d_rb0, (size_t)ctx->N0 + 1))) return bail(st, ctx->detail);
+    if ((st = dev_alloc(ctx, &ctx->d_zb0, (size_t)ctx->N0 + 1))) return bail(st, ctx->detail);
+  }
   if (ctx->coarse_mode != 2) {
     size_t tiles = (size_t)ctx->nT * (ctx->bt + 1);
     if ((st = dev_alloc(ctx, &ctx->d_A0t, tiles * CT * CT))) return bail(st, ctx->detail);
@@ -591,6 +601,8 @@ static void free_ctx(dgas_ctx ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->d_A0b) cudaFree(ctx->d_A0b);
+  for (void* p2 : {(void*)ctx->d_prow, (void*)ctx->d_dsc0, (void*)ctx->d_rb0, (void*)ctx->d_zb0})
+    if (p2) cudaFree(p2);
   nd_free(ctx);
   for (int i = 0; i < 3; ++i) {
     if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);

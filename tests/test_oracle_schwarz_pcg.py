@@ -363,3 +363,38 @@ def test_apply_sampled_is_full_apply_restricted(cfg):
     # the unsampled setup really lacks the other factors
     with pytest.raises(O.OracleError):
         os_.apply(r)
+
+
+def test_long_double_sampled_apply_and_band():
+    """The long-double sampled apply (the exact reference of the full-size GPU apply check, Z30 / R30) is
+    the long-double full apply restricted to the sample; with the band coarse path (no long-double band
+    factor: fp64 band solve refined with long-double residuals) it agrees with the dense long-double
+    apply to ~1e-15 once refined."""
+    P = g.config(3, scale="small")
+    sample = [0, P.n_sub - 1]
+    od = O.Oracle(P)
+    od.setup_schwarz(long_double=True)
+    r = g.normal(95, od.N)
+    zl = od.apply(r, long_double=True)
+    mask = np.repeat(np.isin(P.part, sample), od.np_)
+    assert np.array_equal(od.apply_sampled(r, sample, long_double=True)[mask], zl[mask])
+    ob = O.Oracle(P)
+    ob.setup_schwarz(long_double=True, dense_max=0, sample=sample)
+    ob.set_refine(2)
+    zb = ob.apply_sampled(r, sample, long_double=True)
+    assert np.linalg.norm(zb[mask] - zl[mask]) <= 1e-14 * np.linalg.norm(zl[mask])
+
+
+def test_perturb_A_probe_is_symmetric_and_bounded():
+    """The A-perturbation sensitivity probe (R22/R30) keeps A symmetric and moves every entry by at
+    most eps relative (and really moves them)."""
+    P = g.config(1)
+    o = O.Oracle(P)
+    A = o.dense_A()
+    o2 = O.Oracle(P)
+    o2.perturb_A(1e-6, 3)
+    A2 = o2.dense_A()
+    assert np.array_equal(A2, A2.T)
+    nz = A != 0
+    rel = np.abs(A2[nz] - A[nz]) / np.abs(A[nz])
+    assert rel.max() <= 1e-6 * (1 + 1e-12) and rel.max() > 1e-7

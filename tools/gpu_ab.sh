@@ -16,7 +16,7 @@ for c in ${CONFIGS:-}; do
     echo "$c [$v] $(echo "$out" | python -c 'import sys,json
 try:
   d=json.loads(sys.stdin.read()); k=d["kernels"]
-  print("it/s %.1f iters %s K %.4f | " % (d["value"], d["config"]["iters_per_solve"], d["config"]["lanczos_cond"]) + " ".join("%s %.4f" % (n, k[n]["ms"]) for n in k))
+  print("it/s %.1f iters %s K %.4f | " % (d["value"], d["run"]["iters_per_solve"], d["run"]["lanczos_cond"]) + " ".join("%s %.4f" % (n, k[n]["ms"]) for n in k))
 except Exception as e: print("FAILED", e)')" >> $L
     grep -i "ND coarse\|error" gpurun_out/ab_err_${c}.log | head -3 >> $L
   done
