@@ -394,7 +394,8 @@ def test_perturb_A_probe_is_symmetric_and_bounded():
     o2 = O.Oracle(P)
     o2.perturb_A(1e-6, 3)
     A2 = o2.dense_A()
-    assert np.array_equal(A2, A2.T)
+    # same factor on (i,j) and (j,i): the asymmetry of assembly rounding is only scaled, never added to
+    assert np.abs(A2 - A2.T).max() <= np.abs(A - A.T).max() * (1 + 2e-6)
     nz = A != 0
     rel = np.abs(A2[nz] - A[nz]) / np.abs(A[nz])
     assert rel.max() <= 1e-6 * (1 + 1e-12) and rel.max() > 1e-7
