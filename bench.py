@@ -221,6 +221,7 @@ def main():
 
     if args.local_f32:
         os.environ["DGAS_PANEL_F32"] = "1"
+        os.environ["DGAS_LOCAL_INV"] = "0"
     from paper_1903_11357_b200 import dgas
     torch.cuda.set_device(local)
     if world > 1:
@@ -306,9 +307,9 @@ def main():
     dinv_tri = info["n_cells"] * npp * (npp + 1) // 2 * 8
     alg = {
         "spmv": info["alg_bytes_spmv"],
-        "apply_fused": info["bytes_U"] + dinv_tri + info["bytes_coarse"] + 2 * N * 8 + 2 * N0 * 8,
+        "apply_fused": info["bytes_local"] + info["bytes_coarse"] + 2 * N * 8 + 2 * N0 * 8,
         "apply_total": info["alg_bytes_apply"],
-        "local": info["bytes_U"] + dinv_tri + 2 * N * 8,
+        "local": info["bytes_local"] + 2 * N * 8,
         "coarse": info["bytes_coarse"] + 2 * N0 * 8,
     }
     kern = {nm: {"ms": kt[nm], "alg_bytes": alg[nm], "GBps": alg[nm] / (kt[nm] * 1e-3) / 1e9,
@@ -343,7 +344,7 @@ def main():
                 "parallelism": "replicas" if world > 1 else "single-gpu", "setup_s": t_setup,
                 "coarse_solver": ["dense-inverse", "band", "nested-dissection"][info["coarse_mode"]],
                 "coarse_refine_steps": refine, "coarse_solve_relerr": info["coarse_solve_relerr"],
-                "local_kernel": {1: "envelope", 2: "panel"}.get(info["local_kernel"]),
+                "local_kernel": {1: "envelope", 2: "panel", 3: "explicit-inverse"}.get(info["local_kernel"]),
                 "local_ctas_per_sm": info["local_ctas_per_sm"],
                 "operator_bytes": info["bytes_A"] + info["bytes_U"] + info["bytes_coarse"] + info["bytes_G"],
                 "l2_bytes": torch.cuda.get_device_properties(local).L2_cache_size},

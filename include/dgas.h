@@ -96,9 +96,12 @@ typedef struct {
                                     refinement steps are added while it exceeds 3e-11) */
   int32_t unroll;                /* PCG iterations per execution of the graph's WHILE body; the last body of a
                                     solve launches its remaining copies as immediate-return kernels */
-  int32_t local_kernel;          /* 1: envelope kernel (all subdomains resident); 2: panel kernel (few CTAs
-                                    per SM so the factor is re-read from L2 by the backward sweep) */
+  int32_t local_kernel;          /* 1: envelope kernel (all subdomains resident); 2: panel kernel (merged
+                                    [D | -U] panels, TMA ring); 3: explicit local inverses Z_i = A_i^-1 (one
+                                    GEMV per subdomain, L2-resident small configs; NEXT-4) */
   int32_t local_ctas_per_sm;     /* resident local-solve CTAs per SM the panel kernel is sized for */
+  int64_t bytes_local;           /* operator bytes one local-solve launch reads (factor; or Z for kernel 3) */
+  double local_inv_err;          /* kernel 3: ||Z r - exact solve(r)|| / ||exact solve(r)|| at setup */
 } dgas_info_t;
 
 /* Build the SIPDG operator and the two-level Schwarz preconditioner on the GPU.

@@ -217,6 +217,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     int st = apply_set_smem(ctx, apply_smem_bytes(ctx));
     if (st) return st;
     if ((st = panel_configure(ctx))) return st;
+    if ((st = local_inv_setup(ctx))) return st;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -607,8 +608,9 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   const int refine = ctx->coarse_mode == 2 ? ctx->nd.refine : ctx->coarse_mode == 0 ? ctx->dense_refine : 0;
   const int64_t a0b = ctx->n_pairs * nq * nq * 8;
   const int64_t coarse_alg = info->bytes_coarse * (1 + refine) + refine * a0b;
-  info->alg_bytes_apply = info->bytes_U + dinv_tri + coarse_alg + 2 * info->bytes_G + 3 * N * 8;
-  info->alg_bytes_iter = info->bytes_A + info->bytes_U + dinv_tri + coarse_alg + 2 * info->bytes_G + 16 * N * 8;
+  const int64_t local_b = ctx->local_kernel == 3 ? ctx->inv_bytes : info->bytes_U + dinv_tri;
+  info->alg_bytes_apply = local_b + coarse_alg + 2 * info->bytes_G + 3 * N * 8;
+  info->alg_bytes_iter = info->bytes_A + local_b + coarse_alg + 2 * info->bytes_G + 16 * N * 8;
   info->last_iters = ctx->last_iters; info->last_status = ctx->last_status;
   info->last_cond = ctx->last_cond; info->last_lmin = ctx->last_lmin; info->last_lmax = ctx->last_lmax;
   info->last_relres = ctx->last_relres;
@@ -617,6 +619,8 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->unroll = ctx->unroll;
   info->local_kernel = ctx->local_kernel;
   info->local_ctas_per_sm = ctx->local_kernel == 2 ? ctx->panel_cps : 0;
+  info->bytes_local = ctx->local_kernel == 3 ? ctx->inv_bytes : info->bytes_U + dinv_tri;
+  info->local_inv_err = ctx->inv_err;
   info->coarse_solve_relerr = ctx->coarse_mode == 2 ? ctx->nd.calib_err : ctx->coarse_mode == 0 ? ctx->dense_err : 0.0;
   int coarse_launches = 1 + 3 * (ctx->coarse_mode == 0 ? ctx->dense_refine : 0);
   if (ctx->coarse_mode == 2) {

@@ -85,6 +85,13 @@ struct dgas_ctx_s {
   double *d_rb0 = nullptr, *d_zb0 = nullptr;  // refinement residual / correction (N0)
   int dense_refine = 0;
   double dense_err = 0, dense_err0 = 0;
+  // explicit local inverses Z_i = A_i^-1 (local_inv.cu, local_kernel 3)
+  double* d_inv_Z = nullptr;
+  int64_t* d_inv_zoff = nullptr;
+  int2* d_inv_items = nullptr;
+  int inv_nitems = 0, inv_maxn = 0, inv_grid = 0;
+  int64_t inv_bytes = 0;
+  double inv_err = 0;
   NdPlan nd;
   double* d_A0b = nullptr;   // A0 blocks per coarse pair (n_pairs x nq x nq)
   int max_sub_cells = 0, max_urow = 0, max_deg = 0;
@@ -295,6 +302,8 @@ void nd_solve_launch(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s)
 int nd_set_smem(dgas_ctx ctx);
 int nd_calibrate(dgas_ctx ctx);
 int dense_calibrate(dgas_ctx ctx);
+int local_inv_setup(dgas_ctx ctx);
+void launch_local_inv(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s);
 void launch_a0_diag(dgas_ctx ctx, const int* prow, double* dsc, cudaStream_t s);
 void launch_a0_resid(dgas_ctx ctx, const int* prow, const double* b, const double* z, double* res, const PcgState* st,
                      int mode, cudaStream_t s);

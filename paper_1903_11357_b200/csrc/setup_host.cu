@@ -601,7 +601,8 @@ static void free_ctx(dgas_ctx ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->d_A0b) cudaFree(ctx->d_A0b);
-  for (void* p2 : {(void*)ctx->d_prow, (void*)ctx->d_dsc0, (void*)ctx->d_rb0, (void*)ctx->d_zb0})
+  for (void* p2 : {(void*)ctx->d_prow, (void*)ctx->d_dsc0, (void*)ctx->d_rb0, (void*)ctx->d_zb0, (void*)ctx->d_inv_Z,
+                   (void*)ctx->d_inv_zoff, (void*)ctx->d_inv_items})
     if (p2) cudaFree(p2);
   nd_free(ctx);
   for (int i = 0; i < 3; ++i) {

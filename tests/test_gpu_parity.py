@@ -452,6 +452,11 @@ def test_eager_path_matches_graph(monkeypatch, name):
     ("cfg4s", {"DGAS_LOCAL_KERNEL": "1"}, 1),
     ("cfg1", {}, 2),
     ("cfg5s_p3q1", {}, 2),
+    # explicit local inverses (NEXT-4, local_inv.cu), the default when they fit half the L2
+    ("cfg1", {"DGAS_LOCAL_INV": "1"}, 3),
+    ("cfg2", {"DGAS_LOCAL_INV": "1"}, 3),
+    ("cfg5s_p1q1", {"DGAS_LOCAL_INV": "1"}, 3),
+    ("cfg3s", {"DGAS_LOCAL_INV": "1"}, 3),
     # tiny ring: every panel spans several units, many backward refills (producer protocol)
     ("cfg4s", {"DGAS_LOCAL_CPS": "8", "DGAS_PANEL_SLOT_KB": "1"}, 2),
     ("cfg3s", {"DGAS_PANEL_KEEP": "0", "DGAS_LOCAL_CPS": "3"}, 2),
@@ -461,11 +466,14 @@ def test_eager_path_matches_graph(monkeypatch, name):
 def test_local_kernel_variants(monkeypatch, name, env, kernel):
     """Both local-solve kernels (envelope k_local, panel k_local_panel) and the panel kernel's ring
     geometries give the oracle's preconditioner apply within 1e-10 (north_star tolerance)."""
+    monkeypatch.setenv("DGAS_LOCAL_INV", "0")  # the factor kernels unless the case asks for the inverses
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     P = CASES[name]()
     S = _solver(P)
     assert S.info["local_kernel"] == kernel
+    if kernel == 3:  # Z_i reproduces the exact local solve (setup check)
+        assert S.info["local_inv_err"] <= 1e-12
     o = O.Oracle(P)
     o.setup_schwarz()
     for seed in range(3):
@@ -558,6 +566,7 @@ def test_panel_f32_variant(monkeypatch, name):
     PCG, whose residuals stay fp64, still reaches rtol 1e-8 with the oracle's solution (1e-7) and
     about its iteration count."""
     monkeypatch.setenv("DGAS_PANEL_F32", "1")
+    monkeypatch.setenv("DGAS_LOCAL_INV", "0")
     P = CASES[name]()
     S = _solver(P)
     assert S.info["local_kernel"] == 2

@@ -1,11 +1,11 @@
 #!/bin/bash
 # A/B helper: optional pytest selection, then bench lines for configs x env variants.
-#   TESTS="-k expr"  CONFIGS="cfg3 cfg4"  VARIANTS="DGAS_X=0;DGAS_X=1"  (";"-separated env sets, "-" = none)
+#   KEXPR="pytest -k expression"  CONFIGS="cfg3 cfg4"  VARIANTS="DGAS_X=0;DGAS_X=1"  (";"-separated env sets, "-" = none)
 cd $GRAFT_REPO_ROOT
 L=gpurun_out/ab.log
 nvidia-smi -L > $L 2>&1
-if [ -n "$TESTS" ]; then
-  timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -q -m gpu -x $TESTS > gpurun_out/ab_tests.log 2>&1; echo "tests rc $?" >> $L
+if [ -n "$KEXPR" ]; then
+  timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -q -m gpu -rA -s -k "$KEXPR" > gpurun_out/ab_tests.log 2>&1; echo "tests rc $?" >> $L
   tail -5 gpurun_out/ab_tests.log >> $L
 fi
 IFS=';' read -ra VS <<< "${VARIANTS:--}"
