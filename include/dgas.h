@@ -164,6 +164,37 @@ int dgas_debug_A0(dgas_ctx ctx, double* out);
  * by bench.py to time kernels with CUDA events on the launching stream. */
 int dgas_bench_kernels(dgas_ctx ctx, int which, int reps, void* stream);
 
+/* ---- Subdomain-sharded multi-GPU solve (PAPER.md:123 any decomposition,
+ * PAPER.md:741 "massively parallel"). One process per GPU, each with a full (replicated) context from
+ * dgas_setup. dgas_shard gives rank `rank` of `nranks` a contiguous range of subdomains (balanced by cell
+ * count); per iteration the rank computes only its own rows, subdomains and cells. The collectives are
+ * the CALLER's (sum over ranks; all-gather for the halo), between these calls, on the same stream:
+ *   begin -> allreduce(red0) -> precond -> allreduce(red1) -> direction(first=1) -> allgather(hsend)
+ *   loop: spmv -> allreduce(red2) -> update -> allreduce(red0) -> [stop if red0[N0] <= rtol^2 red0_begin[N0+1]]
+ *         -> precond -> allreduce(red1) -> direction(first=0) -> allgather(hsend)
+ *   finish -> allreduce(x)
+ * Buffers are caller-owned device arrays of doubles: red0 [N0 + 2] = [Q^T r | r.r | b.b] (begin fills all
+ * three parts, update the first two), red1 [1] = r.z, red2 [1] = p.q, hsend [cap] = this rank's border
+ * values of p, hall [nranks * cap] = every rank's hsend (all-gathered, rank-major). Asynchronous on
+ * `stream` except dgas_shard and dgas_shard_finish. info[6] out: own dof range [info0, info1) in internal
+ * order, cap, N, N0, own subdomain count. Errors: DGAS_E_INVALID_ARG (ranks > subdomains, bad rank, no
+ * byte-ring SpMV); dgas_shard_finish returns DGAS_E_BREAKDOWN if p.Ap <= 0 or r.z <= 0 was seen. */
+int dgas_shard(dgas_ctx ctx, int32_t rank, int32_t nranks, int64_t* info);
+/* b: caller order, length N, the full right-hand side on every rank. x = 0, r = b. */
+int dgas_shard_begin(dgas_ctx ctx, const double* b, double* red0, void* stream);
+/* z0 = A0^-1 r0 with r0 = summed red0[0..N0) (replicated coarse solve), z = own local solves + Q z0 on own
+ * cells; red1 = own part of r.z. */
+int dgas_shard_precond(dgas_ctx ctx, const double* red0, double* red1, void* stream);
+/* beta = summed r.z / previous (first: p = z), p = z + beta p on own dofs; hsend = p on own border cells. */
+int dgas_shard_direction(dgas_ctx ctx, const double* red1, double* hsend, int32_t first, void* stream);
+/* p on other ranks' border cells from hall; q = A p on own rows (eq:Ah); red2 = own part of p.q. */
+int dgas_shard_spmv(dgas_ctx ctx, const double* hall, double* red2, void* stream);
+/* alpha = summed r.z / summed p.q; x += alpha p, r -= alpha q (own); red0[0..N0] = own [Q^T r | r.r]. */
+int dgas_shard_update(dgas_ctx ctx, const double* red2, double* red0, void* stream);
+/* x: caller order, length N: own dofs of the iterate, zero elsewhere (sum over ranks = the solution).
+ * lanczos[3] (device) = (lmin, lmax, K) from the first `iters` CG coefficients. */
+int dgas_shard_finish(dgas_ctx ctx, int32_t iters, double* x, double* lanczos, void* stream);
+
 /* Frees every device buffer of the context. */
 int dgas_destroy(dgas_ctx ctx);
 

@@ -31,6 +31,7 @@ static int panel_configure(dgas_ctx ctx) {
   // are latency-bound, 0.78-0.90 ms)
   int cps = (ctx->nsub + nsm - 1) / nsm;
   if (cps > 3) cps = 7;
+  if (const char* e = std::getenv("DGAS_LOCAL_CPS")) cps = std::max(1, std::min(8, std::atoi(e)));  // tests, sweeps
   ctx->panel_cps = cps;
   size_t reserve = 8 * 1024;
   if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;

@@ -62,6 +62,15 @@ struct NdPlan {
   double* d_dsc = nullptr;             // diag(A0)^-1/2 (symmetric scaling of the fronts)
 };
 
+// Subdomain-sharded multi-GPU solve (shard.cu): this rank's view of the replicated context
+struct ShardPlan {
+  int active = 0, rank = 0, nranks = 1, cap = 1, nsend_own = 0, send_off = 0;
+  std::vector<int> s_begin, c_begin;  // [nranks+1] subdomain / cell ranges (internal numbering)
+  int *d_send_ptr = nullptr, *d_send = nullptr;  // border cells of every rank (CSR by rank)
+  double* d_partials = nullptr;
+  void* d_state = nullptr;
+};
+
 struct dgas_ctx_s {
   // sizes
   int p = 0, q = 0, np = 0, nq = 0, nc = 0, nsub = 0, ncoarse = 0, nface = 0, nov = 0;
@@ -92,6 +101,8 @@ struct dgas_ctx_s {
   int inv_nitems = 0, inv_maxn = 0, inv_grid = 0;
   int64_t inv_bytes = 0;
   double inv_err = 0;
+  std::vector<int> inv_item_ptr;  // [nsub+1] first work item of each subdomain
+  ShardPlan sh;
   NdPlan nd;
   double* d_A0b = nullptr;   // A0 blocks per coarse pair (n_pairs x nq x nq)
   int max_sub_cells = 0, max_urow = 0, max_deg = 0;
@@ -304,6 +315,14 @@ int nd_calibrate(dgas_ctx ctx);
 int dense_calibrate(dgas_ctx ctx);
 int local_inv_setup(dgas_ctx ctx);
 void launch_local_inv(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s);
+void launch_local_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
+void launch_local_inv_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
+void launch_local_panel_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
+void launch_spmv_range(dgas_ctx ctx, int c_begin, int c_end, const double* x, double* y, cudaStream_t s);
+void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);
+void launch_lanczos(dgas_ctx ctx, cudaStream_t s);
+int dgas_post_setup(dgas_ctx ctx);
+void shard_free(dgas_ctx ctx);
 void launch_a0_diag(dgas_ctx ctx, const int* prow, double* dsc, cudaStream_t s);
 void launch_a0_resid(dgas_ctx ctx, const int* prow, const double* b, const double* z, double* res, const PcgState* st,
                      int mode, cudaStream_t s);

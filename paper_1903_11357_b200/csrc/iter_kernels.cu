@@ -1194,6 +1194,28 @@ static void launch_local(dgas_ctx ctx, int mode, PcgState* st, const double* r, 
                          st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows, ctx->local_reuse)));
 }
 
+// local solves of subdomains [sb, se) only (sharded solve, shard.cu; mode 0): the single-GPU kernels
+// index subdomains through sub_ptr[blockIdx] (absolute cell numbers), so a shifted sub_ptr and a grid
+// of se - sb CTAs run exactly the solves of that range
+void launch_local_range(dgas_ctx ctx, int sb, int se, const double* r, double* z, cudaStream_t s) {
+  if (se <= sb) return;
+  if (ctx->max_sub_cells == 1) {
+    const int c0 = ctx->sub_ptr_h[sb], n = ctx->sub_ptr_h[se] - c0;
+    unsigned grid = 1;
+    DISPATCH_P(ctx->p, (grid = (n + 8 * ProlongCfg<NP_>::CPW - 1) / (8 * ProlongCfg<NP_>::CPW)));
+    DISPATCH_P(ctx->p, (k_bjacobi<NP_><<<grid, 256, 0, s>>>(0, n, ctx->d_Dinv + (size_t)c0 * NP_ * NP_,
+                                                            r + (size_t)c0 * NP_, ctx->d_rbuf, z + (size_t)c0 * NP_,
+                                                            nullptr)));
+    return;
+  }
+  if (ctx->local_kernel == 2) { launch_local_panel_range(ctx, sb, se, r, z, s); return; }
+  if (ctx->local_kernel == 3) { launch_local_inv_range(ctx, sb, se, r, z, s); return; }
+  const size_t smem = apply_smem_bytes(ctx);
+  DISPATCH_P(ctx->p, (k_local<NP_><<<se - sb, LocalCfg<NP_>::T + 32, smem, s>>>(
+                         0, ctx->d_sub_ptr + sb, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
+                         nullptr, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows, ctx->local_reuse)));
+}
+
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
   static const bool no_fork = std::getenv("DGAS_NO_FORK") != nullptr;
   if (ctx->precond != 0) {

@@ -92,6 +92,14 @@ void launch_local_inv(dgas_ctx ctx, int mode, const PcgState* st, const double* 
                                                              ctx->d_rbuf, z, st);
 }
 
+// the work items of subdomains [sb, se) only (sharded solve, mode 0)
+void launch_local_inv_range(dgas_ctx ctx, int sb, int se, const double* r, double* z, cudaStream_t s) {
+  const int i0 = ctx->inv_item_ptr[sb], n = ctx->inv_item_ptr[se] - i0;
+  if (n <= 0) return;
+  k_local_inv<<<std::min(n, ctx->inv_grid), INV_T, (size_t)ctx->inv_maxn * 8, s>>>(
+      0, ctx->np, ctx->d_inv_items + i0, n, ctx->d_sub_ptr, ctx->d_inv_zoff, ctx->d_inv_Z, r, ctx->d_rbuf, z, nullptr);
+}
+
 // Build Z_i after the local-solve kernel is configured; switch local_kernel to 3 when accepted.
 int local_inv_setup(dgas_ctx ctx) {
   if (ctx->max_sub_cells <= 1) return 0;  // one-cell subdomains: k_bjacobi already is the inverse
@@ -116,8 +124,11 @@ int local_inv_setup(dgas_ctx ctx) {
   if (!want) return 0;
   if ((size_t)maxn * 8 > 96 * 1024) return 0;  // r_i staged in shared memory
   std::vector<int2> items;
-  for (int s = 0; s < nsub; ++s)
+  ctx->inv_item_ptr.assign(nsub + 1, 0);
+  for (int s = 0; s < nsub; ++s) {
     for (int r0 = 0; r0 < (sp[s + 1] - sp[s]) * np; r0 += INV_ROWS) items.push_back(make_int2(s, r0));
+    ctx->inv_item_ptr[s + 1] = (int)items.size();
+  }
   int st;
   if ((st = dev_upload(ctx, &ctx->d_inv_zoff, zoff)) || (st = dev_upload(ctx, &ctx->d_inv_items, items))) return st;
   if ((st = dev_alloc(ctx, &ctx->d_inv_Z, (size_t)std::max<int64_t>(1, zoff[nsub])))) return st;

@@ -401,3 +401,20 @@ void launch_local_panel(dgas_ctx ctx, int mode, PcgState* st, const double* r, d
   }
 #undef PANEL_LAUNCH
 }
+
+// subdomains [sb, se) only (sharded solve, mode 0): shifted sub_ptr / sub_units, grid se - sb
+void launch_local_panel_range(dgas_ctx ctx, int sb, int se, const double* r, double* z, cudaStream_t s) {
+  if (se <= sb) return;
+  const size_t smem = panel_smem_bytes(ctx);
+#define PANEL_LAUNCH_R(NAR, TS)                                                                                    \
+  DISPATCH_P15(ctx->p, (k_local_panel<NP_, NAR, TS><<<se - sb, PanelCfg<NP_, NAR>::T + 32, smem, s>>>(             \
+                           0, ctx->d_sub_ptr + sb, ctx->d_first, ctx->d_pus, ctx->d_sub_units + sb, ctx->d_p_off,   \
+                           reinterpret_cast<const TS*>(ctx->d_P), r, ctx->d_rbuf, z, nullptr, ctx->panel_slots,    \
+                           ctx->panel_slot_bytes, ctx->panel_cc, ctx->max_sub_cells, ctx->panel_keep)))
+  if (ctx->panel_f32) {
+    if (panel_narrow(ctx)) { PANEL_LAUNCH_R(true, float); } else { PANEL_LAUNCH_R(false, float); }
+  } else {
+    if (panel_narrow(ctx)) { PANEL_LAUNCH_R(true, double); } else { PANEL_LAUNCH_R(false, double); }
+  }
+#undef PANEL_LAUNCH_R
+}

@@ -605,6 +605,7 @@ static void free_ctx(dgas_ctx ctx) {
                    (void*)ctx->d_inv_zoff, (void*)ctx->d_inv_items})
     if (p2) cudaFree(p2);
   nd_free(ctx);
+  shard_free(ctx);
   for (int i = 0; i < 3; ++i) {
     if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
     if (ctx->ev_fork[i]) cudaEventDestroy(ctx->ev_fork[i]);

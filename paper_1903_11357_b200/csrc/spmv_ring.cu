@@ -316,3 +316,16 @@ void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgSta
                            mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr, ctx->d_a_off, ctx->d_A, x, y, ctx->d_z,
                            ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha, ctx->sr_ring_bytes, ctx->sr_G)));
 }
+
+// y = A x on the rows of cells [cb, ce) only (sharded solve, shard.cu; mode 0): the kernel addresses its
+// cell range relative to its nbr_ptr / a_off / y pointers, and gathers x through absolute cell ids
+void launch_spmv_range(dgas_ctx ctx, int cb, int ce, const double* x, double* y, cudaStream_t s) {
+  const int n = ce - cb;
+  if (n <= 0) return;
+  const int grid = std::min(ctx->sr_grid, n), chunk = (n + grid - 1) / grid;
+  const size_t smem = spmv_ring_smem(ctx);  // sized for the full problem's (larger) chunk
+  DISPATCH_PSR(ctx->p, (k_spmv_ring<NP_><<<grid, (SR_NW + 1) * 32, smem, s>>>(
+                           0, n, chunk, ctx->d_nbr_ptr + cb, ctx->d_nbr, ctx->d_a_off + cb, ctx->d_A, x,
+                           y + (size_t)cb * NP_, ctx->d_z, ctx->d_pbuf, nullptr, ctx->d_partials, ctx->d_alpha,
+                           ctx->sr_ring_bytes, ctx->sr_G)));
+}

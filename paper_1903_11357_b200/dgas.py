@@ -19,7 +19,9 @@ E_INVALID_ARG, E_MESH, E_NOT_SPD, E_BREAKDOWN, E_CUDA, E_NOMEM = -1, -2, -3, -4,
 
 EXPORTS = ["dgas_setup", "dgas_rhs", "dgas_spmv", "dgas_apply", "dgas_pcg", "dgas_pcg_host", "dgas_info",
            "dgas_history", "dgas_debug_block", "dgas_debug_basis", "dgas_debug_A0", "dgas_bench_kernels",
-           "dgas_destroy", "dgas_strerror", "dgas_error_detail", "dgas_set_precond"]
+           "dgas_destroy", "dgas_strerror", "dgas_error_detail", "dgas_set_precond", "dgas_shard",
+           "dgas_shard_begin", "dgas_shard_precond", "dgas_shard_direction", "dgas_shard_spmv", "dgas_shard_update",
+           "dgas_shard_finish"]
 PRECOND = {"two_level": 0, "one_level": 1, "coarse": 2, "none": 3}   # DGAS_PRECOND_* (include/dgas.h)
 
 
@@ -77,6 +79,13 @@ def load():
     L.dgas_bench_kernels.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P]
     L.dgas_set_precond.argtypes = [_P, ctypes.c_int]
     L.dgas_destroy.argtypes = [_P]
+    L.dgas_shard.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P]
+    L.dgas_shard_begin.argtypes = [_P, _P, _P, _P]
+    L.dgas_shard_precond.argtypes = [_P, _P, _P, _P]
+    L.dgas_shard_direction.argtypes = [_P, _P, _P, ctypes.c_int32, _P]
+    L.dgas_shard_spmv.argtypes = [_P, _P, _P, _P]
+    L.dgas_shard_update.argtypes = [_P, _P, _P, _P]
+    L.dgas_shard_finish.argtypes = [_P, ctypes.c_int32, _P, _P, _P]
     L.dgas_strerror.restype = ctypes.c_char_p
     L.dgas_strerror.argtypes = [ctypes.c_int]
     L.dgas_error_detail.restype = ctypes.c_char_p
@@ -232,3 +241,102 @@ class Solver:
         out = np.zeros((self.N0, self.N0))
         self._check(load().dgas_debug_A0(self.ctx, out.ctypes.data))
         return out
+
+
+class ShardBackend:
+    """Marshalling of the dgas_shard_* entry points (include/dgas.h) for one rank of a Solver."""
+
+    def __init__(self, solver, rank, nranks):
+        import torch
+        self.S = solver
+        info = np.zeros(6, np.int64)
+        solver._check(load().dgas_shard(solver.ctx, rank, nranks, info.ctypes.data))
+        self.dof_begin, self.dof_end, self.cap, self.N, self.N0, self.n_sub_own = (int(v) for v in info)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def zeros(self, n):
+        import torch
+        return torch.zeros(n, dtype=torch.float64, device=self.device)
+
+    def begin(self, b, red0):
+        self.S._check(load().dgas_shard_begin(self.S.ctx, _dptr(b), _dptr(red0), _stream()))
+
+    def precond(self, red0, red1):
+        self.S._check(load().dgas_shard_precond(self.S.ctx, _dptr(red0), _dptr(red1), _stream()))
+
+    def direction(self, red1, hsend, first):
+        self.S._check(load().dgas_shard_direction(self.S.ctx, _dptr(red1), _dptr(hsend), int(first), _stream()))
+
+    def spmv(self, hall, red2):
+        self.S._check(load().dgas_shard_spmv(self.S.ctx, _dptr(hall), _dptr(red2), _stream()))
+
+    def update(self, red2, red0):
+        self.S._check(load().dgas_shard_update(self.S.ctx, _dptr(red2), _dptr(red0), _stream()))
+
+    def finish(self, iters, x, lanczos):
+        return self.S._check(load().dgas_shard_finish(self.S.ctx, int(iters), _dptr(x), _dptr(lanczos), _stream()))
+
+
+class ShardedSolver:
+    """Subdomain-sharded ASPCG over torch.distributed ranks (include/dgas.h "Sharded").
+
+    Every rank owns a contiguous range of subdomains of its (replicated) Solver; the arithmetic runs in the
+    dgas_shard_* kernels, the collectives are torch.distributed calls between them (NCCL on GPUs, gloo in
+    the tests). `backend` defaults to the rank's ShardBackend; the tests substitute a CPU mock with the same
+    buffer semantics to check this driver's collective schedule."""
+
+    def __init__(self, solver=None, group=None, backend=None):
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.B = backend if backend is not None else ShardBackend(solver, self.rank, self.nranks)
+
+    def _sum(self, t):
+        import torch.distributed as dist
+        if self.nranks > 1:
+            dist.all_reduce(t, group=self.group)
+
+    def _gather(self, hall, hsend):
+        import torch.distributed as dist
+        if self.nranks > 1:
+            dist.all_gather(list(hall.view(self.nranks, -1).unbind(0)), hsend, group=self.group)
+        else:
+            hall.copy_(hsend)
+
+    def pcg(self, b, rtol=1e-8, maxit=5000):
+        """Solve A x = b (b: the full right-hand side, caller order, on every rank). Returns
+        (x, iters, cond, status) with x the full solution on every rank (PAPER.md:741 protocol, R11/R12)."""
+        B, N0 = self.B, self.B.N0
+        red0, red1, red2 = B.zeros(N0 + 2), B.zeros(1), B.zeros(1)
+        hsend, hall = B.zeros(B.cap), B.zeros(self.nranks * B.cap)
+        B.begin(b, red0)
+        self._sum(red0)
+        bb = float(red0[N0 + 1])
+        stop2 = rtol * rtol * bb
+        it, status = 0, 1  # DGAS_NOT_CONVERGED until the stop test holds
+        if bb > 0:
+            B.precond(red0, red1)
+            self._sum(red1)
+            B.direction(red1, hsend, True)
+            self._gather(hall, hsend)
+            while it < maxit:
+                B.spmv(hall, red2)
+                self._sum(red2)
+                B.update(red2, red0)
+                self._sum(red0)
+                it += 1
+                if float(red0[N0]) <= stop2:  # ||r||^2 <= rtol^2 ||b||^2 after the update (R11)
+                    status = 0
+                    break
+                B.precond(red0, red1)
+                self._sum(red1)
+                B.direction(red1, hsend, False)
+                self._gather(hall, hsend)
+        else:
+            status = 0
+        x, lz = B.zeros(B.N), B.zeros(3)
+        st = B.finish(it, x, lz)
+        self._sum(x)
+        cond = float(lz[2]) if it > 0 else 1.0
+        return x, it, cond, st if st < 0 else status

@@ -1,0 +1,55 @@
+"""Shared parity helpers of the -m gpu tests (R22/R30 rounding-spread of the oracle itself)."""
+import numpy as np
+
+import dgas_gen as g
+import oracle as O
+
+_EPS = 2.220446049250313e-16
+
+
+def _kappa_gram(o, cells):
+    """max condition number of the cells' raw-basis Gram matrices, kappa(G) = cond(C)^2 with
+    C = (Cholesky factor)^-1 from the oracle: the relative rounding level of two correct assemblies
+    (basis coefficients, A entries) is ~ kappa(G) * eps."""
+    return max(np.linalg.cond(o.basis(int(c))[0]) ** 2 for c in cells)
+
+
+def _oracle_spread(o, b, ref, rtol=1e-8, P=None):
+    """Iteration counts of the oracle itself under last-bit perturbations: 1e-13 relative noise on b
+    and (P given) 1-ulp noise on G and kappa(Gram)-eps noise on A, i.e. two correct assemblies of the
+    operators (R22/R30). When the residual plateaus near rtol the stopping iteration is not unique under rounding
+    (R22); measured on cfg4s (rho jumps 1e8): b probes 208-209, G probes 206-208, GPU 205-209 with an
+    apply that agrees to 1.4e-13."""
+    its = [ref["iters"]]
+    for s in range(3):
+        its.append(o.pcg(b * (1 + 1e-13 * g.normal(500 + s, b.shape[0])), rtol=rtol)["iters"])
+    if P is not None:
+        for seed in (1, 2, 3):
+            o2 = O.Oracle(P)
+            o2.set_perturb(2.2e-16, seed)
+            o2.setup_schwarz()
+            its.append(o2.pcg(b, rtol=rtol)["iters"])
+        # two correct assemblies of A differ by ~kappa(Gram) eps (basis = CholQR2 of the cell Gram; the
+        # GPU's A blocks agree with the oracle's to this bound, test_basis_and_blocks): perturb A so
+        rng = np.random.default_rng(5)
+        kap = _kappa_gram(o, rng.choice(P.n_cells, size=min(64, P.n_cells), replace=False))
+        for seed in (1, 2, 3):
+            o2 = O.Oracle(P)
+            o2.perturb_A(kap * _EPS, seed)
+            o2.setup_schwarz()
+            its.append(o2.pcg(b, rtol=rtol)["iters"])
+    return min(its), max(its)
+
+
+def _iters_ok(o, b, ref, iters, P, label=""):
+    """north_star: within 2 of the oracle. Else (R22: the stopping iteration is not unique under
+    rounding when the residual plateaus near rtol) inside the oracle's OWN spread [lo, hi] under
+    last-bit perturbations of b and G -- one allowance or the other, never both stacked. The spread
+    branch is logged so the test output shows how often it fires."""
+    if abs(iters - ref["iters"]) <= 2:
+        return True
+    lo, hi = _oracle_spread(o, b, ref, P=P)
+    print(f"\n[spread branch] {label}: GPU iters {iters}, oracle {ref['iters']}, oracle spread [{lo}, {hi}]")
+    return lo <= iters <= hi
+
+
