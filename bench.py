@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--impl", default="dgas", choices=["dgas", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas of the single-GPU solve instead of the sharded solve")
     ap.add_argument("--local-f32", action="store_true",
                     help="NEXT-4 variant outside the fp64 contract: fp32-stored local factors (never the headline)")
     args = ap.parse_args()
@@ -223,10 +225,12 @@ def main():
         os.environ["DGAS_PANEL_F32"] = "1"
         os.environ["DGAS_LOCAL_INV"] = "0"
     from paper_1903_11357_b200 import dgas
+    # DGAS_BENCH_DEVICE / DGAS_DIST_BACKEND: test hooks (several ranks on one GPU over gloo)
+    local = int(os.environ.get("DGAS_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("DGAS_DIST_BACKEND", "nccl"))
     P = _problem(args.config)
     t0 = time.time()
     S = dgas.Solver(P)
@@ -235,6 +239,16 @@ def main():
     info = S.info
     b = S.rhs(P.f_kind)
     x = torch.zeros_like(b)
+    # N > 1: the subdomain-sharded solve over NCCL: one problem, total work fixed
+    sharded = world > 1 and not args.replicas
+    SS = dgas.ShardedSolver(S) if sharded else None
+
+    def solve(bb, xx):
+        if sharded:
+            xs, it_, c_, st_ = SS.pcg(bb)
+            xx.copy_(xs)
+            return xx, it_, c_, st_
+        return S.pcg(bb, xx)
 
     def barrier():
         if world > 1:
@@ -242,7 +256,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        x.zero_(); S.pcg(b, x)
+        x.zero_(); solve(b, x)
     barrier()
     iters_total = 0
     iters_list = []
@@ -261,7 +275,7 @@ def main():
             if flush is not None:
                 flush.fill_(float(k))
             ev[k][0].record()
-            _, it, cond, st = S.pcg(b, x)
+            _, it, cond, st = solve(b, x)
             ev[k][1].record()
             iters_total += it
             iters_list.append(it)
@@ -269,25 +283,36 @@ def main():
         barrier()
     ms = sum(a.elapsed_time(c) for a, c in ev)
     ms, iters_all = aggregate(ms, iters_total, world, device="cuda")
+    if sharded:
+        iters_all = iters_total  # one shared solve: the ranks' iterations are the same iterations
     value = iters_all / (ms / 1e3)
     iters_per_solve = iters_total / args.steps
 
     # ---- e2e through the public C ABI with host buffers (pinned), copies inside the timed region
     bh = b.cpu().pin_memory()
     xh = torch.zeros(S.N, dtype=torch.float64).pin_memory()
-    S.pcg_host(bh, xh)
+    if sharded:  # host b in, solve, host x out (every rank holds b and receives x)
+        def host_solve():
+            bd = bh.to("cuda", non_blocking=True)
+            xd, it_, _, _ = SS.pcg(bd)
+            xh.copy_(xd)
+            return it_
+    else:
+        def host_solve():
+            return S.pcg_host(bh, xh)[0]
+    host_solve()
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record()
     e2e_iters = 0
     for _ in range(args.steps):
         xh.zero_()
-        it, _, _ = S.pcg_host(bh, xh)
-        e2e_iters += it
+        e2e_iters += host_solve()
     e3.record()
     barrier()
     e2e_ms = e2.elapsed_time(e3)
-    e2e_value = e2e_iters * world / (e2e_ms / 1e3)
+    e2e_ms, _ = aggregate(e2e_ms, 0, world, device="cuda")
+    e2e_value = e2e_iters * (1 if sharded else world) / (e2e_ms / 1e3)
 
     # ---- per-kernel timing (CUDA events on the launching stream) for the roofline
     peaks = _peaks()
@@ -337,11 +362,13 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": "PCG it/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": problem_config(args.config, P),
         "run": {"iters_per_solve": iters_per_solve, "lanczos_cond": conds[-1] if conds else None,
-                "parallelism": "replicas" if world > 1 else "single-gpu", "setup_s": t_setup,
+                "parallelism": (f"sharded-subdomains-{world}x-nccl" if sharded else "replicas") if world > 1
+                else "single-gpu", "setup_s": t_setup,
                 "coarse_solver": ["dense-inverse", "band", "nested-dissection"][info["coarse_mode"]],
                 "coarse_refine_steps": refine, "coarse_solve_relerr": info["coarse_solve_relerr"],
                 "local_kernel": {1: "envelope", 2: "panel", 3: "explicit-inverse"}.get(info["local_kernel"]),
@@ -363,9 +390,10 @@ def main():
         "e2e": {"value": e2e_value, "unit": "PCG it/s", "h2d_bytes_per_step": 2 * N * 8,
                 "d2h_bytes_per_step": N * 8},
         # the last WHILE body of a solve also launches its remaining unrolled copies (immediate return)
-        "gpu_launches": int(info["launches_per_iter"] * sum(-(-it // info["unroll"]) * info["unroll"]
-                                                            for it in iters_list)
-                            + info["launches_per_solve"] * args.steps),
+        "gpu_launches": (int((info["launches_per_iter"] + 12) * sum(iters_list) + 16 * args.steps) if sharded else
+                         int(info["launches_per_iter"] * sum(-(-it // info["unroll"]) * info["unroll"]
+                                                             for it in iters_list)
+                             + info["launches_per_solve"] * args.steps)),
         "clocks": clk.summary(),
     }
     if args.local_f32:
