@@ -218,6 +218,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     int st = apply_set_smem(ctx, apply_smem_bytes(ctx));
     if (st) return st;
     if ((st = panel_configure(ctx))) return st;
+    if (ctx->local_kernel == 2 && (st = local_warp_setup(ctx))) return st;
     if ((st = local_inv_setup(ctx))) return st;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);

@@ -102,6 +102,12 @@ struct dgas_ctx_s {
   int64_t inv_bytes = 0;
   double inv_err = 0;
   std::vector<int> inv_item_ptr;  // [nsub+1] first work item of each subdomain
+  // warp-per-subdomain local solve (local_panel.cu k_local_warp, local_kernel 4)
+  int *d_lw_pus = nullptr, *d_lw_units = nullptr;
+  unsigned* d_lw_cnt = nullptr;
+  int lw_S = 0, lw_cc = 0, lw_warps = 2, lw_grid = 0, lw_keep = 1;
+  uint32_t lw_slot = 0;
+  size_t lw_smem = 0;
   ShardPlan sh;
   NdPlan nd;
   double* d_A0b = nullptr;   // A0 blocks per coarse pair (n_pairs x nq x nq)
@@ -318,6 +324,8 @@ void launch_local_inv(dgas_ctx ctx, int mode, const PcgState* st, const double* 
 void launch_local_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
 void launch_local_inv_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
 void launch_local_panel_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
+int local_warp_setup(dgas_ctx ctx);
+void launch_local_warp(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s);
 void launch_spmv_range(dgas_ctx ctx, int c_begin, int c_end, const double* x, double* y, cudaStream_t s);
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);
 void launch_lanczos(dgas_ctx ctx, cudaStream_t s);

@@ -418,3 +418,302 @@ void launch_local_panel_range(dgas_ctx ctx, int sb, int se, const double* r, dou
   }
 #undef PANEL_LAUNCH_R
 }
+
+// ====================================================================================================
+// k_local_warp — the same merged-panel solve (P_k = [D_k | -U_k], units of CCW columns), one WARP per
+// subdomain. The CTA kernel above spends most issue slots on per-step CTA barriers, mbarrier polling
+// and idle row/column slots (ncu, config 3: 72% issue-busy, 356 M warp instructions per launch), so it
+// needs 7-8 CTAs per SM to stream at ~60% of HBM peak, and with every subdomain in flight the factor
+// is read twice from HBM (backward sweep after the whole forward sweep; 1.65-1.85x the algorithmic
+// bytes). Here a warp owns a subdomain end to end: lane (a, h) = (row, column slice) in the forward
+// step (row sums by shuffles), lane = column in the backward step (u_k in registers), __syncwarp only,
+// and the warp's lane 0 issues its own cp.async.bulk refills into a private ring (no empty barriers:
+// producer and consumer are the same warp). Short steps let 1-2 warps per SM keep HBM busy, so few
+// subdomains are in flight at a time and the forward copies (evict-last) are still in L2 when the
+// backward sweep re-reads them: HBM reads the factor about once. Subdomains are taken dynamically
+// (atomic counter; the last warp out resets it).
+//   forward  L y = r   : y_k = D_k r_k - U_k y_old           (lanes: rows x column slices)
+//   backward L^T z = y : v = P_k^T u_k, z_k = v[0..NP), y_old -= U_k^T u_k (lanes: columns)
+// ====================================================================================================
+template <int NP>
+struct WarpCfg {
+  static constexpr int LPR = 32 / NP;       // column slices per row (lanes a + NP h)
+  static constexpr int LANES = NP * LPR;    // active lanes in the forward step
+  static constexpr int RN = (NP + LPR - 1) / LPR;  // D columns (r_k entries) per lane
+};
+
+// per-warp smem: full[S] (256 B) | us[mc+1] | fk[mc] | po[mc] | Y[mc NP] | ring[S slot]
+struct WarpLayout {
+  size_t off_us, off_fk, off_po, off_Y, off_ring, stride;
+  __host__ __device__ WarpLayout(int mc, int np, int S, uint32_t slot) {
+    off_us = 256;
+    off_fk = off_us + (((size_t)(mc + 1) * 4 + 15) & ~(size_t)15);
+    off_po = off_fk + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_Y = off_po + (((size_t)mc * 8 + 15) & ~(size_t)15);
+    off_ring = (off_Y + (size_t)mc * np * 8 + 127) & ~(size_t)127;
+    stride = (off_ring + (size_t)S * slot + 127) & ~(size_t)127;
+  }
+};
+
+template <int NP>
+__global__ void __launch_bounds__(128) k_local_warp(
+    int mode, int nsub, const int* __restrict__ sub_ptr, const int* __restrict__ first, const int* __restrict__ pus,
+    const int* __restrict__ sub_units, const int64_t* __restrict__ p_off, const double* __restrict__ P,
+    const double* r_in, double* const* rbuf, double* z, const PcgState* st, unsigned* cnt, int S, uint32_t slot_bytes,
+    int CC, int max_cells, int keep_fwd) {
+  using C = WarpCfg<NP>;
+  constexpr int LPR = C::LPR, RN = C::RN;
+  constexpr int DPK = panel_dpk<double>(NP), AL = panel_al<double>();
+  extern __shared__ __align__(128) unsigned char smw[];
+  const double* r = r_in;
+  if (mode >= 1) {
+    if (st->done) return;
+    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+  }
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const WarpLayout L(max_cells, NP, S, slot_bytes);
+  unsigned char* base = smw + (size_t)wl * L.stride;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base);
+  int* us = reinterpret_cast<int*>(base + L.off_us);
+  int* fk = reinterpret_cast<int*>(base + L.off_fk);
+  int64_t* po = reinterpret_cast<int64_t*>(base + L.off_po);
+  double* Y = reinterpret_cast<double*>(base + L.off_Y);
+  unsigned char* ring = base + L.off_ring;
+  if (lane == 0) {
+    for (int t = 0; t < S; ++t) mbar_init(&full[t], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const int SM1 = S - 1, CC0 = CC - panel_e<double>(NP);
+  const uint64_t pol_first = l2_evict_first(), pol_keep = keep_fwd ? l2_evict_last() : pol_first;
+  uint32_t ph = 0;  // parity of the next completion per slot (S <= 32)
+  const int a = lane % NP, h = lane / NP;
+  const bool fwd_lane = lane < C::LANES;
+  for (;;) {
+    int sub = 0;
+    if (lane == 0) sub = (int)atomicAdd(cnt, 1u);
+    sub = __shfl_sync(0xffffffffu, sub, 0);
+    if (sub >= nsub) break;
+    const int s0 = sub_ptr[sub], m = sub_ptr[sub + 1] - s0;
+    for (int k = lane; k < m; k += 32) {
+      us[k] = pus[s0 + k];
+      fk[k] = first[s0 + k];
+      po[k] = p_off[s0 + k];
+    }
+    if (lane == 0) us[m] = sub_units[sub];
+    __syncwarp();
+    const int U = us[m];
+    // unit u of cell k -> (offset, bytes) in the cell's panel
+    auto issue = [&](int u, int k, uint64_t pol) {
+      const int WU = (k - fk[k]) * NP, t = u - us[k];
+      int64_t off, n;
+      if (t == 0) { off = 0; n = DPK + (int64_t)min(WU, CC0) * NP; }
+      else { const int j0 = CC0 + (t - 1) * CC; off = DPK + (int64_t)j0 * NP; n = (int64_t)(min(WU, j0 + CC) - j0) * NP; }
+      const uint32_t nbytes = (uint32_t)((n + AL - 1) / AL * AL * 8);
+      bulk_load(ring + (size_t)(u & SM1) * slot_bytes, P + po[k] + off, nbytes, &full[u & SM1], pol);
+    };
+    int kf = 0;  // lane 0: cell of the next forward unit to issue
+    if (lane == 0) {
+      for (int u = 0; u < min(S, U); ++u) {
+        while (us[kf + 1] <= u) ++kf;
+        issue(u, kf, u < U - S ? pol_keep : pol_first);
+      }
+    }
+    const double* rs = r + (size_t)s0 * NP;
+    double rk[RN];
+#pragma unroll
+    for (int t = 0; t < RN; ++t) rk[t] = h + LPR * t < NP && fwd_lane ? rs[h + LPR * t] : 0.0;
+    // ---------------- forward sweep
+    for (int k = 0; k < m; ++k) {
+      const int u0 = us[k], u1 = us[k + 1], f = fk[k], WU = (k - f) * NP;
+      const double* yb = Y + f * NP;
+      double v0 = 0, v1 = 0;
+      for (int u = u0; u < u1; ++u) {
+        const int sl = u & SM1, t = u - u0;
+        mbar_wait(&full[sl], (ph >> sl) & 1);
+        ph ^= 1u << sl;
+        const double* Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+        if (fwd_lane) {
+          int j0, j1;
+          const double* Pu;
+          if (t == 0) {
+#pragma unroll
+            for (int tt = 0; tt < RN; ++tt) {
+              const int c = h + LPR * tt;
+              if (c < NP && c <= a) v1 += Ps[panel_dcol(NP, c) + a - c] * rk[tt];
+            }
+            j0 = 0; j1 = min(WU, CC0); Pu = Ps + DPK + a;
+          } else {
+            j0 = CC0 + (t - 1) * CC; j1 = min(WU, j0 + CC); Pu = Ps - j0 * NP + a;
+          }
+          int j = j0 + h;
+          double v2 = 0, v3 = 0;
+          for (; j + 3 * LPR < j1; j += 4 * LPR) {  // 8 independent loads in flight per lane
+            const double p0 = Pu[j * NP], p1 = Pu[(j + LPR) * NP], p2 = Pu[(j + 2 * LPR) * NP],
+                         p3 = Pu[(j + 3 * LPR) * NP];
+            const double y0 = yb[j], y1 = yb[j + LPR], y2 = yb[j + 2 * LPR], y3 = yb[j + 3 * LPR];
+            v0 += p0 * y0; v1 += p1 * y1; v2 += p2 * y2; v3 += p3 * y3;
+          }
+          for (; j < j1; j += LPR) v0 += Pu[j * NP] * yb[j];
+          v0 += v2; v1 += v3;
+        }
+        __syncwarp();
+        if (lane == 0 && u + S < U) {  // the slot is consumed: refill it with unit u + S
+          while (us[kf + 1] <= u + S) ++kf;
+          issue(u + S, kf, u + S < U - S ? pol_keep : pol_first);
+        }
+      }
+      double v = v0 + v1, tot = v;
+#pragma unroll
+      for (int h2 = 1; h2 < LPR; ++h2) tot += __shfl_sync(0xffffffffu, v, (a + NP * h2) & 31);
+      if (h == 0 && lane < NP) Y[k * NP + a] = tot;
+      // prefetch r_{k+1}
+#pragma unroll
+      for (int t = 0; t < RN; ++t)
+        rk[t] = k + 1 < m && h + LPR * t < NP && fwd_lane ? rs[(k + 1) * NP + h + LPR * t] : 0.0;
+      __syncwarp();
+    }
+    // ---------------- backward sweep: units in reverse; the last S units are still in the ring
+    int kb = m - 1;  // lane 0: cell of the next backward refill
+    double* zs = z + (size_t)s0 * NP;
+    for (int k = m - 1; k >= 0; --k) {
+      const int u0 = us[k], u1 = us[k + 1], f = fk[k], WU = (k - f) * NP;
+      double uk[NP];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) uk[i] = Y[k * NP + i];
+      double* yb = Y + f * NP;
+      for (int u = u1 - 1; u >= u0; --u) {
+        const int sl = u & SM1, t = u - u0;
+        if (u < U - S) {
+          mbar_wait(&full[sl], (ph >> sl) & 1);
+          ph ^= 1u << sl;
+        }
+        const double* Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+        const int xoff = t == 0 ? NP : 0;
+        const int j0 = t == 0 ? 0 : CC0 + (t - 1) * CC, j1 = t == 0 ? min(WU, CC0) : min(WU, j0 + CC);
+        const double* Pu = t == 0 ? Ps + DPK : Ps - j0 * NP;
+        const int nx = xoff + j1 - j0;
+        if (t == 0 && lane < NP) {  // z_k = D_k^T u_k: D column x holds rows x..NP-1
+          const int x = lane;
+          const double* col = Ps + panel_dcol(NP, x) - x;
+          double w = 0;
+#pragma unroll
+          for (int i = 0; i < NP; ++i)
+            if (i >= x) w += col[i] * uk[i];
+          zs[k * NP + x] = w;
+        }
+        // U columns: y_old -= U_k^T u_k (full columns, no predicates)
+        for (int x = lane; x < nx - xoff; x += 32) {
+          const double* col = Pu + (j0 + x) * NP;
+          double w0 = 0, w1 = 0;
+#pragma unroll
+          for (int i = 0; i + 1 < NP; i += 2) {
+            w0 += col[i] * uk[i];
+            w1 += col[i + 1] * uk[i + 1];
+          }
+          if (NP & 1) w0 += col[NP - 1] * uk[NP - 1];
+          yb[j0 + x] += w0 + w1;
+        }
+        __syncwarp();
+        if (lane == 0 && u - S >= 0) {  // slot consumed: load unit u - S (needed S units later)
+          while (us[kb] > u - S) --kb;
+          issue(u - S, kb, pol_first);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // last warp out resets the subdomain counter for the next launch
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(cnt + 1, 1u) == gridDim.x * (blockDim.x >> 5) - 1) {
+      cnt[0] = 0;
+      cnt[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// host: the warp kernel's own unit tables (its CCW differs from the CTA kernel's CC), ring sizing
+int local_warp_setup(dgas_ctx ctx) {
+  if (!panel_supported(ctx->p) || ctx->max_sub_cells <= 1 || ctx->panel_f32) return 0;
+  int dev = 0, nsm = 148, smem_sm = 233472, optin = 232448;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // default on for the large configs (>= 4 subdomains per SM; measured B200 PCG it/s, tools/gpu_ab.sh:
+  // config 3 1082 -> 1133 with 4 x 4 warps/SM, config 4 1821 -> 1923 with 4 x 2); the CTA kernel stays
+  // for fewer subdomains (config 5: 256 subdomains, latency-bound chains, CTA kernel 1.8-2.3x faster)
+  int want = ctx->nsub >= 4 * nsm;
+  if (const char* e = std::getenv("DGAS_LOCAL_WARP")) want = std::atoi(e) != 0;
+  if (!want) return 0;
+  int W = 4, cps = ctx->np <= 10 ? 4 : 2;
+  if (const char* e = std::getenv("DGAS_LW_WARPS")) W = std::max(1, std::min(4, std::atoi(e)));
+  if (const char* e = std::getenv("DGAS_LW_CPS")) cps = std::max(1, std::min(16, std::atoi(e)));
+  size_t reserve = 8 * 1024;
+  if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;
+  size_t per_cta = std::min((size_t)optin, ((size_t)smem_sm - reserve) / cps - 1024);
+  const size_t per_warp = per_cta / W;
+  const int np = ctx->np, mc = ctx->max_sub_cells;
+  const size_t fixed = WarpLayout(mc, np, 0, 0).off_ring + 128;
+  if (per_warp <= fixed + 4096) return 0;
+  const size_t B = per_warp - fixed;
+  size_t target = 8 * 1024;
+  if (const char* e = std::getenv("DGAS_LW_SLOT_KB")) target = (size_t)std::atoi(e) * 1024;
+  int S = 2;
+  while (S < 32 && B / (2 * S) >= target) S *= 2;
+  const int cc_min = panel_min_cc(np, 0), maxW = ctx->max_urow + np;
+  const int cc_max = std::max(cc_min, (maxW + 1) / 2 * 2);
+  int CC = (int)std::min<size_t>(cc_max, (B / S) / (8 * np)) / 2 * 2;
+  if (CC < cc_min) return 0;
+  const uint32_t sb = (uint32_t)(((((int64_t)CC * np + 1) / 2 * 2) * 8 + 127) / 128 * 128);
+  while (S < 32 && (size_t)2 * S * sb <= B) S *= 2;
+  // unit tables for CCW = CC
+  const std::vector<int>& sp = ctx->sub_ptr_h;
+  const int CC0 = CC - panel_e<double>(np);
+  std::vector<int> pus(ctx->nc), sub_units(ctx->nsub);
+  int maxU = 0;
+  for (int s = 0; s < ctx->nsub; ++s) {
+    int acc = 0;
+    for (int c = sp[s]; c < sp[s + 1]; ++c) {
+      const int k = c - sp[s], WU = (k - ctx->first_h[c]) * np;
+      pus[c] = acc;
+      acc += panel_units(WU, CC, CC0);
+    }
+    sub_units[s] = acc;
+    maxU = std::max(maxU, acc);
+  }
+  int st;
+  if ((st = dev_upload(ctx, &ctx->d_lw_pus, pus)) || (st = dev_upload(ctx, &ctx->d_lw_units, sub_units))) return st;
+  if ((st = dev_alloc(ctx, &ctx->d_lw_cnt, 4))) return st;
+  ctx->lw_S = S;
+  ctx->lw_slot = sb;
+  ctx->lw_cc = CC;
+  ctx->lw_warps = W;
+  ctx->lw_grid = cps * nsm;
+  ctx->lw_keep = 1;
+  if (const char* e = std::getenv("DGAS_LW_KEEP")) ctx->lw_keep = std::atoi(e) != 0;
+  ctx->lw_smem = WarpLayout(mc, np, S, sb).stride * W;
+  cudaError_t e = cudaSuccess;
+  DISPATCH_P15(ctx->p, ({
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, k_local_warp<NP_>);
+    if (e == cudaSuccess && (size_t)optin < ctx->lw_smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_local_warp<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  }));
+  if (e != cudaSuccess) { ctx->detail = std::string("warp local smem: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
+  if (std::getenv("DGAS_VERBOSE"))
+    fprintf(stderr, "dgas: warp local solve: %d warps x %d CTAs/SM, ring %d x %u B (CC %d), smem/CTA %zu\n", W, cps, S,
+            sb, CC, ctx->lw_smem);
+  ctx->local_kernel = 4;
+  return 0;
+}
+
+void launch_local_warp(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s) {
+  DISPATCH_P15(ctx->p, (k_local_warp<NP_><<<ctx->lw_grid, 32 * ctx->lw_warps, ctx->lw_smem, s>>>(
+                           mode, ctx->nsub, ctx->d_sub_ptr, ctx->d_first, ctx->d_lw_pus, ctx->d_lw_units, ctx->d_p_off,
+                           reinterpret_cast<const double*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->d_lw_cnt, ctx->lw_S,
+                           ctx->lw_slot, ctx->lw_cc, ctx->max_sub_cells, ctx->lw_keep)));
+}

