@@ -102,6 +102,9 @@ typedef struct {
   int32_t local_ctas_per_sm;     /* resident local-solve CTAs per SM the panel kernel is sized for */
   int64_t bytes_local;           /* operator bytes one local-solve launch reads (factor; or Z for kernel 3) */
   double local_inv_err;          /* kernel 3: ||Z r - exact solve(r)|| / ||exact solve(r)|| at setup */
+  int64_t dedup_A_bytes;         /* bytes of A actually stored when bitwise-identical row-blocks are shared
+                                    (exact de-duplication, NEXT-4; 0: not de-duplicated) */
+  int64_t dedup_local_bytes;     /* the same for the local factors (merged panels) */
 } dgas_info_t;
 
 /* Build the SIPDG operator and the two-level Schwarz preconditioner on the GPU.

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 
 #include "internal.h"
 
@@ -276,6 +277,35 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     }
   }
   DGAS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (std::getenv("DGAS_DEDUP_STATS")) {  // diagnostic: bitwise-identical row-blocks / local factors
+    std::vector<double> A((size_t)ctx->a_off_h[ctx->nc]);
+    DGAS_CUDA(cudaMemcpy(A.data(), ctx->d_A, A.size() * 8, cudaMemcpyDeviceToHost));
+    auto fnv = [](const double* p, int64_t n) {
+      uint64_t h = 1469598103934665603ULL;
+      const unsigned char* b = reinterpret_cast<const unsigned char*>(p);
+      for (int64_t i = 0; i < n * 8; ++i) { h ^= b[i]; h *= 1099511628211ULL; }
+      return h ^ (uint64_t)n;
+    };
+    std::map<uint64_t, int> rows;
+    for (int c = 0; c < ctx->nc; ++c) rows[fnv(A.data() + ctx->a_off_h[c], ctx->a_off_h[c + 1] - ctx->a_off_h[c])]++;
+    std::map<uint64_t, int> subs;
+    if (ctx->local_kernel == 2 || ctx->local_kernel == 4) {
+      std::vector<int64_t> po(ctx->nc + 1);
+      DGAS_CUDA(cudaMemcpy(po.data(), ctx->d_p_off, (ctx->nc + 1) * 8, cudaMemcpyDeviceToHost));
+      std::vector<double> Pp((size_t)ctx->p_total);
+      DGAS_CUDA(cudaMemcpy(Pp.data(), ctx->d_P, Pp.size() * 8, cudaMemcpyDeviceToHost));
+      for (int s2 = 0; s2 < ctx->nsub; ++s2) {
+        const int64_t a0 = po[ctx->sub_ptr_h[s2]], a1 = po[ctx->sub_ptr_h[s2 + 1]];
+        subs[fnv(Pp.data() + a0, a1 - a0)]++;
+      }
+    }
+    fprintf(stderr, "dgas: dedup stats: %d cells, %zu distinct row-blocks; %d subdomains, %zu distinct local factors\n",
+            ctx->nc, rows.size(), ctx->nsub, subs.size());
+  }
+  {
+    int st3 = dedup_setup(ctx);  // exact de-duplication of bitwise-identical operator data (dedup.cu)
+    if (st3) return st3;
+  }
   return 0;
 }
 
@@ -604,7 +634,7 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->bytes_coarse = ctx->coarse_mode == 2 ? ctx->nd.bytes : ctx->coarse_dense ? ctx->N0 * ctx->ldX * 8
                                          : (int64_t)ctx->nT * (ctx->bt + 1) * CT * CT * 8 + (int64_t)ctx->nT * CT * CT * 8;
   // algorithmic bytes: every operator entry read once, vectors once each
-  info->alg_bytes_spmv = info->bytes_A + (2 * N) * 8 + (int64_t)ctx->nnzb * 4;
+  info->alg_bytes_spmv = info->bytes_A + (2 * N) * 8 + (int64_t)ctx->nnzb * 4;  // full-storage bytes (reference)
   const int64_t dinv_tri = (int64_t)ctx->nc * (np * (np + 1) / 2) * 8;
   // refinement steps of the ND coarse solve re-read the factors and read the A0 pair blocks once more
   const int refine = ctx->coarse_mode == 2 ? ctx->nd.refine : ctx->coarse_mode == 0 ? ctx->dense_refine : 0;
@@ -623,6 +653,8 @@ extern "C" int dgas_info(dgas_ctx ctx, dgas_info_t* info) {
   info->local_ctas_per_sm = ctx->local_kernel == 2 ? ctx->panel_cps : 0;
   info->bytes_local = ctx->local_kernel == 3 ? ctx->inv_bytes : info->bytes_U + dinv_tri;
   info->local_inv_err = ctx->inv_err;
+  info->dedup_A_bytes = ctx->d_a_dd ? ctx->a_bytes_stored : 0;
+  info->dedup_local_bytes = ctx->p_bytes_stored;
   info->coarse_solve_relerr = ctx->coarse_mode == 2 ? ctx->nd.calib_err : ctx->coarse_mode == 0 ? ctx->dense_err : 0.0;
   int coarse_launches = 1 + 3 * (ctx->coarse_mode == 0 ? ctx->dense_refine : 0);
   if (ctx->coarse_mode == 2) {
@@ -649,7 +681,7 @@ extern "C" int dgas_debug_block(dgas_ctx ctx, int32_t i, int32_t j, double* out)
   int deg = hi - lo, sl = -1;
   for (int k = lo; k < hi; ++k) if (ctx->nbr_h[k] == cj) sl = k - lo;
   if (sl < 0) return 0;
-  const int64_t off = ctx->a_off_h[ci];
+  const int64_t off = ctx->d_a_dd ? ctx->a_dd_h[ci] : ctx->a_off_h[ci];
   std::vector<double> row((size_t)np * deg * np);
   DGAS_CUDA(cudaMemcpy(row.data(), ctx->d_A + off, row.size() * sizeof(double), cudaMemcpyDeviceToHost));
   for (int a = 0; a < np; ++a)

@@ -109,6 +109,13 @@ struct dgas_ctx_s {
   uint32_t lw_slot = 0;
   size_t lw_smem = 0;
   ShardPlan sh;
+  // exact de-duplication of bitwise-identical operator data (dedup.cu; NEXT-4 Cartesian de-duplication)
+  int64_t* d_a_dd = nullptr;          // [nc] compact-store offset of each cell's row-block (nullptr: off)
+  int dd_grid = 0;                     // persistent CTAs of k_spmv_dd
+  std::vector<int64_t> a_dd_h;
+  int64_t a_unique = 0, a_bytes_stored = 0;  // distinct row-blocks, bytes of the compact A
+  int p_unique = 0;                   // distinct subdomain factors (panel store)
+  int64_t p_bytes_stored = 0;
   NdPlan nd;
   double* d_A0b = nullptr;   // A0 blocks per coarse pair (n_pairs x nq x nq)
   int max_sub_cells = 0, max_urow = 0, max_deg = 0;
@@ -325,6 +332,7 @@ void launch_local_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* 
 void launch_local_inv_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
 void launch_local_panel_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
 int local_warp_setup(dgas_ctx ctx);
+int dedup_setup(dgas_ctx ctx);
 void launch_local_warp(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s);
 void launch_spmv_range(dgas_ctx ctx, int c_begin, int c_end, const double* x, double* y, cudaStream_t s);
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);

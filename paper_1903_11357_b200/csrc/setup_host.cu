@@ -603,7 +603,7 @@ static void free_ctx(dgas_ctx ctx) {
   if (ctx->d_A0b) cudaFree(ctx->d_A0b);
   for (void* p2 : {(void*)ctx->d_prow, (void*)ctx->d_dsc0, (void*)ctx->d_rb0, (void*)ctx->d_zb0, (void*)ctx->d_inv_Z,
                    (void*)ctx->d_inv_zoff, (void*)ctx->d_inv_items, (void*)ctx->d_lw_pus, (void*)ctx->d_lw_units,
-                   (void*)ctx->d_lw_cnt})
+                   (void*)ctx->d_lw_cnt, (void*)ctx->d_a_dd})
     if (p2) cudaFree(p2);
   nd_free(ctx);
   shard_free(ctx);

@@ -41,7 +41,8 @@ template <int NP>
 __global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
     int mode, int nc, int chunk, const int* __restrict__ nbr_ptr, const int* __restrict__ nbr,
     const int64_t* __restrict__ a_off, const double* __restrict__ A, const double* x, double* y, const double* z,
-    double* const* pbuf, PcgState* st, double* partials, double* alpha_hist, uint32_t ring_bytes, int G) {
+    double* const* pbuf, PcgState* st, double* partials, double* alpha_hist, uint32_t ring_bytes, int G,
+    const int64_t* __restrict__ a_dd) {
   constexpr int LPR = SrCfg<NP>::LPR, E = SrCfg<NP>::E, XS = SrCfg<NP>::XS;
   constexpr int NTT = (SR_NW + 1) * 32;
   extern __shared__ __align__(128) double sm[];
@@ -99,7 +100,8 @@ __global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
         }
         vst[gi % SR_NB] = V;
         pst[gi % SR_NB] = Pp;
-        bulk_load(ring + Pp, A + o0, len, &full[gi % SR_NB], pol);
+        // de-duplicated storage (G = 1): the cell's row-block lives at a_dd[cell] in the compact store
+        bulk_load(ring + Pp, A + (a_dd ? a_dd[c0 + gi] : o0), len, &full[gi % SR_NB], pol);
         V += len;
         Pp += len;
       }
@@ -229,6 +231,126 @@ __global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// k_spmv_dd — the same q = A p (+ PCG fusion: p = z + beta p_old, p.q, alpha) when A is stored
+// de-duplicated (dedup.cu: config 3 has 1225 distinct row-blocks, 4.8 MB, L2-resident): no TMA ring
+// (one bulk copy per cell was the bottleneck, 0.40 ms), each warp reads its cell's row-block straight
+// from the compact store through the L2 (__ldg), lanes (row a, column slice h) as in k_spmv_ring, the
+// neighbour values gathered one cell ahead. Persistent CTAs of 8 warps over contiguous cell ranges.
+template <int NP>
+__global__ void __launch_bounds__(SR_NW * 32) k_spmv_dd(
+    int mode, int nc, int chunk, const int* __restrict__ nbr_ptr, const int* __restrict__ nbr,
+    const int64_t* __restrict__ a_dd, const double* __restrict__ A, const double* x, double* y, const double* z,
+    double* const* pbuf, PcgState* st, double* partials, double* alpha_hist) {
+  constexpr int LPR = SrCfg<NP>::LPR, E = SrCfg<NP>::E, XS = SrCfg<NP>::XS;
+  constexpr int NTT = SR_NW * 32;
+  __shared__ double red[NTT / 32];
+  __shared__ double wdot[NTT / 32];
+  __shared__ double xs_all[SR_NW * XS];
+  int it = 0;
+  double beta = 0;
+  const double* pold = nullptr;
+  double* pnew = nullptr;
+  const bool pcg = mode == 1 || mode == 3;
+  if (pcg) {
+    if (st->done) return;
+    it = st->it;
+    beta = it > 0 ? st->beta : 0.0;
+    pold = pbuf[it & 1];
+    pnew = pbuf[(it + 1) & 1];
+    if (mode == 3) x = pnew;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c0 = min(nc, blockIdx.x * chunk), c1 = min(nc, c0 + chunk), n = c1 - c0;
+  double* xs = xs_all + w * XS;
+  auto colval = [&](int64_t id) -> double {
+    return mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
+  };
+  double mydot = 0;
+  const int a = lane % NP, h = lane / NP;
+  double vN[E];
+  auto load = [&](int i, double* v) {  // gathered neighbour values of cell i (index load + value load)
+    if (i >= n) {
+#pragma unroll
+      for (int t = 0; t < E; ++t) v[t] = 0.0;
+      return;
+    }
+    const int lo = nbr_ptr[c0 + i], W = (nbr_ptr[c0 + i + 1] - lo) * NP;
+#pragma unroll
+    for (int t = 0; t < E; ++t) {
+      const int e = lane + 32 * t;
+      v[t] = e < W ? colval((int64_t)__ldg(nbr + lo + e / NP) * NP + e % NP) : 0.0;
+    }
+  };
+  load(w, vN);
+  for (int i = w; i < n; i += SR_NW) {
+    const int c = c0 + i;
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < E; ++t) xs[lane + 32 * t] = vN[t];
+    __syncwarp();
+    load(i + SR_NW, vN);  // next cell's gather overlaps this cell's products
+    const int W = (nbr_ptr[c + 1] - nbr_ptr[c]) * NP;
+    const double* Ab = A + a_dd[c] + a;
+    double pn = 0;
+    if (pcg && h == 0 && lane < NP) {
+      const size_t id = (size_t)c * NP + a;
+      pn = mode == 3 ? x[id] : it > 0 ? z[id] + beta * pold[id] : z[id];
+    }
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    if (h < LPR) {
+      int col = h;
+      for (; col + 3 * LPR < W; col += 4 * LPR) {
+        s0 += __ldg(Ab + col * NP) * xs[col];
+        s1 += __ldg(Ab + (col + LPR) * NP) * xs[col + LPR];
+        s2 += __ldg(Ab + (col + 2 * LPR) * NP) * xs[col + 2 * LPR];
+        s3 += __ldg(Ab + (col + 3 * LPR) * NP) * xs[col + 3 * LPR];
+      }
+      for (; col < W; col += LPR) s0 += __ldg(Ab + col * NP) * xs[col];
+    }
+    const double v = (s0 + s1) + (s2 + s3);
+    double tot = v;
+#pragma unroll
+    for (int h2 = 1; h2 < LPR; ++h2) tot += __shfl_sync(0xffffffffu, v, (a + NP * h2) & 31);
+    if (h == 0 && lane < NP) {
+      const size_t id = (size_t)c * NP + a;
+      y[id] = tot;
+      if (pcg) {
+        if (mode == 1) pnew[id] = pn;
+        mydot += pn * tot;
+      }
+    }
+  }
+  if (!pcg) return;
+  mydot = warp_sum(mydot);
+  if (lane == 0) wdot[w] = mydot;
+  __syncthreads();
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    double t0 = 0;
+    for (int k = 0; k < NTT / 32; ++k) t0 += wdot[k];
+    partials[blockIdx.x] = t0;
+    __threadfence();
+    am_last = atomicAdd(&st->cnt[0], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double sacc = 0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += NTT) sacc += __ldcg(partials + k);
+  sacc = warp_sum(sacc);
+  if (lane == 0) red[w] = sacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double pq = 0;
+    for (int k = 0; k < NTT / 32; ++k) pq += red[k];
+    st->cnt[0] = 0;
+    st->pq = pq;
+    if (!(pq > 0) || !isfinite(pq)) { st->done = 1; st->status = DGAS_E_BREAKDOWN; }
+    else { st->alpha = st->gamma / pq; alpha_hist[it] = st->alpha; }
+  }
+}
+
 #define DISPATCH_PSR(P, ...)                                \
   switch (P) {                                              \
     case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
@@ -310,11 +432,18 @@ void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgSta
     k_pupdate<<<nsm * 8, 256, 0, s>>>(ctx->N, ctx->d_z, ctx->d_pbuf, st);
     mode = 3;
   }
+  if (ctx->d_a_dd) {
+    const int grid = ctx->dd_grid, chunk = (ctx->nc + grid - 1) / grid;
+    DISPATCH_PSR(ctx->p, (k_spmv_dd<NP_><<<grid, SR_NW * 32, 0, s>>>(mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr,
+                                                                     ctx->d_a_dd, ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf,
+                                                                     st, ctx->d_partials, ctx->d_alpha)));
+    return;
+  }
   const int grid = ctx->sr_grid, chunk = sr_chunk(ctx);
   const size_t smem = spmv_ring_smem(ctx);
   DISPATCH_PSR(ctx->p, (k_spmv_ring<NP_><<<grid, (SR_NW + 1) * 32, smem, s>>>(
                            mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr, ctx->d_a_off, ctx->d_A, x, y, ctx->d_z,
-                           ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha, ctx->sr_ring_bytes, ctx->sr_G)));
+                           ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha, ctx->sr_ring_bytes, ctx->sr_G, ctx->d_a_dd)));
 }
 
 // y = A x on the rows of cells [cb, ce) only (sharded solve, shard.cu; mode 0): the kernel addresses its
@@ -322,10 +451,18 @@ void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgSta
 void launch_spmv_range(dgas_ctx ctx, int cb, int ce, const double* x, double* y, cudaStream_t s) {
   const int n = ce - cb;
   if (n <= 0) return;
+  if (ctx->d_a_dd) {
+    const int grid = std::min(ctx->dd_grid, n), chunk = (n + grid - 1) / grid;
+    DISPATCH_PSR(ctx->p, (k_spmv_dd<NP_><<<grid, SR_NW * 32, 0, s>>>(0, n, chunk, ctx->d_nbr_ptr + cb, ctx->d_nbr,
+                                                                     ctx->d_a_dd + cb, ctx->d_A, x, y + (size_t)cb * NP_,
+                                                                     ctx->d_z, ctx->d_pbuf, nullptr, ctx->d_partials,
+                                                                     ctx->d_alpha)));
+    return;
+  }
   const int grid = std::min(ctx->sr_grid, n), chunk = (n + grid - 1) / grid;
   const size_t smem = spmv_ring_smem(ctx);  // sized for the full problem's (larger) chunk
   DISPATCH_PSR(ctx->p, (k_spmv_ring<NP_><<<grid, (SR_NW + 1) * 32, smem, s>>>(
                            0, n, chunk, ctx->d_nbr_ptr + cb, ctx->d_nbr, ctx->d_a_off + cb, ctx->d_A, x,
                            y + (size_t)cb * NP_, ctx->d_z, ctx->d_pbuf, nullptr, ctx->d_partials, ctx->d_alpha,
-                           ctx->sr_ring_bytes, ctx->sr_G)));
+                           ctx->sr_ring_bytes, ctx->sr_G, ctx->d_a_dd ? ctx->d_a_dd + cb : nullptr)));
 }

@@ -49,7 +49,8 @@ class Info(ctypes.Structure):
                 ("launches_per_solve", ctypes.c_int32), ("coarse_refine", ctypes.c_int32),
                 ("coarse_solve_relerr", ctypes.c_double), ("unroll", ctypes.c_int32),
                 ("local_kernel", ctypes.c_int32), ("local_ctas_per_sm", ctypes.c_int32),
-                ("bytes_local", ctypes.c_int64), ("local_inv_err", ctypes.c_double)]
+                ("bytes_local", ctypes.c_int64), ("local_inv_err", ctypes.c_double),
+                ("dedup_A_bytes", ctypes.c_int64), ("dedup_local_bytes", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

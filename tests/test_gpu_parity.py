@@ -544,3 +544,29 @@ def test_panel_f32_variant(monkeypatch, name):
     xh = x.cpu().numpy()
     assert np.linalg.norm(xh - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
     S.close()
+
+
+def test_dedup_is_bitwise_identical(monkeypatch):
+    """Exact de-duplication (dedup.cu, NEXT-4): config-3-style Cartesian meshes produce bitwise-identical
+    row-blocks and local factors; storing each once changes no arithmetic. With the SpMV on the same CTA
+    chunking as the byte ring (DGAS_DD_CPS = its CTAs per SM), PCG gives the same iterations, K and x bit
+    for bit, with and without de-duplication."""
+    P = CASES["cfg3s"]()
+    out = []
+    for dd in ("0", "1"):
+        monkeypatch.setenv("DGAS_DEDUP", dd)
+        monkeypatch.setenv("DGAS_DD_CPS", "2")
+        S = _solver(P)
+        info = S.get_info()
+        if dd == "1":
+            assert 0 < info["dedup_A_bytes"] < info["bytes_A"] // 4
+        else:
+            assert info["dedup_A_bytes"] == 0
+        b = S.rhs(P.f_kind)
+        x, it, c, st = S.pcg(b, rtol=1e-8)
+        out.append((x.cpu().numpy(), it, c, st, S.spmv(b).cpu().numpy()))
+        S.close()
+    (x0, i0, c0, s0, y0), (x1, i1, c1, s1, y1) = out
+    assert s0 == s1 == 0 and i0 == i1 and c0 == c1
+    assert np.array_equal(y0, y1)
+    assert np.array_equal(x0, x1)
