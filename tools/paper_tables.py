@@ -9,7 +9,8 @@ K from the Lanczos extreme-eigenvalue estimate. The meshes are our own seeded Vo
 for digit. With --oracle the CPU oracle solves every case with N_h <= --oracle-max and the GPU iteration
 count is compared with it (parity; the paper's numbers are context).
 
-Usage: python tools/paper_tables.py [--p 1 3] [--ex 2 4] [--oracle] [--out gpurun_out/paper_tables.json]
+Usage: python tools/paper_tables.py [--p 1 3] [--ex 2 4] [--oracle] [--kah] [--out gpurun_out/paper_tables.json]
+       python tools/paper_tables.py --add-spreads file.json   (CPU, oracle only: R22 spreads of rows outside +-2)
 """
 import argparse
 import json
@@ -40,6 +41,47 @@ def cases(ex, p):
             yield coarse, nf, ref
 
 
+def spread(oracle, P, o, b, it0, precond=True):
+    import numpy as np
+    its = [it0]
+    kw = dict(rtol=1e-8, maxit=50000, precond=precond)
+    for s in range(3):
+        its.append(o.pcg(b * (1 + 1e-13 * dgas_gen.normal(500 + s, b.shape[0])), **kw)["iters"])
+    kap = max(np.linalg.cond(o.basis(int(c))[0]) ** 2 for c in range(0, P.n_cells, max(1, P.n_cells // 64)))
+    for kind, seed in (("A", 1), ("A", 2), ("A", 3), ("G", 1), ("G", 2)):
+        o2 = oracle.Oracle(P)
+        if kind == "A":
+            o2.perturb_A(kap * 2.220446049250313e-16, seed)
+        else:
+            o2.set_perturb(2.220446049250313e-16, seed)
+        o2.setup_schwarz()
+        its.append(o2.pcg(b, **kw)["iters"])
+    return [min(its), max(its)]
+
+
+def add_spreads(path):
+    """Oracle-only post-processing (CPU): the spread of every oracle-checked row outside +-2."""
+    import oracle
+    rows = json.load(open(path))
+    for r in rows:
+        if "oracle_iters" not in r or abs(r["iters"] - r["oracle_iters"]) <= 2 or "oracle_spread" in r:
+            continue
+        if r["ex"] == 1:
+            P = dgas_gen.paper_case_ex1(r["coarse"][0], r["coarse"][1], r["coarse"][2], r["p"])
+        else:
+            coarse = r["coarse"] if r["coarse"] != "K(A_h)" else next(c for c, n, _ in cases(r["ex"], r["p"])
+                                                                     if n == r["n_fine"])
+            P = dgas_gen.paper_case(r["ex"], r["n_fine"], coarse, r["p"])
+        o = oracle.Oracle(P)
+        o.setup_schwarz()
+        b = o.rhs()
+        r["oracle_spread"] = spread(oracle, P, o, b, r["oracle_iters"], precond=r["coarse"] != "K(A_h)")
+        r["within_spread"] = r["oracle_spread"][0] <= r["iters"] <= r["oracle_spread"][1]
+        print(json.dumps({k: r[k] for k in ("ex", "p", "coarse", "iters", "oracle_iters", "oracle_spread",
+                                           "within_spread")}), flush=True)
+        json.dump(rows, open(path, "w"), indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--p", type=int, nargs="+", default=[1, 2, 3])
@@ -47,6 +89,8 @@ def main():
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--oracle-max", type=int, default=1024)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "paper_tables.json"))
+    ap.add_argument("--kah", action="store_true",
+                    help="also K(A_h) (unpreconditioned CG Lanczos, dgas_set_precond none) per fine mesh of Ex.2/4")
     a = ap.parse_args()
     import torch
     from paper_1903_11357_b200 import dgas
@@ -79,15 +123,44 @@ def main():
                     import oracle
                     o = oracle.Oracle(P)
                     o.setup_schwarz()
-                    r = o.pcg(o.rhs(), rtol=1e-8, maxit=20000)
+                    bo = o.rhs()
+                    r = o.pcg(bo, rtol=1e-8, maxit=20000)
                     row.update(oracle_iters=r["iters"], oracle_K=r["cond"])
+                    if abs(iters - r["iters"]) > 2:
+                        # R22: the oracle's own stopping-iteration spread under last-bit perturbations of b,
+                        # A (kappa(Gram) eps) and G (1 ulp): the GPU count is checked against it instead
+                        row["oracle_spread"] = spread(oracle, P, o, bo, r["iters"])
+                        row["within_spread"] = row["oracle_spread"][0] <= iters <= row["oracle_spread"][1]
                 S.close()
                 rows.append(row)
                 print(json.dumps(row), flush=True)
+            if a.kah and ex in (2, 4):
+                # the abstract's comparison: K of the unpreconditioned SIPG operator on each
+                # fine mesh, as the bottom rows of the paper's 3D tables list it
+                seen = sorted({nf for _, nf, _ in cases(ex, p)})
+                for nf in seen:
+                    coarse = next(c for c, n, _ in cases(ex, p) if n == nf)
+                    P = dgas_gen.paper_case(ex, nf, coarse, p)
+                    S = dgas.Solver(P)
+                    S.set_precond("none")
+                    b = S.rhs(dgas_gen.F_SINSIN)
+                    x, iters, cond, st = S.pcg(b, rtol=1e-8, maxit=50000)
+                    row = dict(ex=ex, p=p, coarse="K(A_h)", n_fine=nf, N=S.N, iters=iters, K=cond, status=st)
+                    if a.oracle and nf <= a.oracle_max:
+                        import oracle
+                        o = oracle.Oracle(P)
+                        r = o.pcg(o.rhs(), rtol=1e-8, maxit=50000, precond=False)
+                        row.update(oracle_iters=r["iters"], oracle_K=r["cond"])
+                    S.close()
+                    rows.append(row)
+                    print(json.dumps(row), flush=True)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(rows, f, indent=1)
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 2 and sys.argv[1] == "--add-spreads":
+        add_spreads(sys.argv[2])
+    else:
+        main()

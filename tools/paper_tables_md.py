@@ -20,8 +20,9 @@ def main(path):
            "Meshes are our seeded Voronoi meshes (DESIGN.md R31-R33), not the paper's, so the paper's numbers",
            "are context (same trend and magnitude expected), while the oracle columns are parity: the CPU",
            "oracle on the same mesh. Cell format: GPU K (iterations) | paper K (iterations).", ""]
-    par_total = par_ok = 0
-    dev_it = dev_k = 0.0
+    par_total = par_ok = par_spread = 0
+    dev_k = 0.0
+    spread_cases = []
     for ex in (1, 2, 4):
         sel = [r for r in rows if r["ex"] == ex]
         if not sel:
@@ -53,25 +54,44 @@ def main(path):
                 grid = defaultdict(dict)
                 for r in rs:
                     grid[r["coarse"]][r["n_fine"]] = r
-                for coarse in sorted(grid, reverse=(ex == 2)):
+                keys = sorted([k for k in grid if k != "K(A_h)"], reverse=(ex == 2)) + (["K(A_h)"] if "K(A_h)" in grid else [])
+                for coarse in keys:
                     cells = []
                     for c in cols:
                         r = grid[coarse].get(c)
-                        cells.append("-" if r is None else
-                                     f"{fmt(r['K'], r['iters'])} \\| {fmt(r['paper_K'], r['paper_iters'])}")
+                        if r is None:
+                            cells.append("-")
+                        elif coarse == "K(A_h)":  # unpreconditioned CG; the paper lists it for 3D only
+                            cells.append(fmt(r["K"], r["iters"]))
+                        else:
+                            cells.append(f"{fmt(r['K'], r['iters'])} \\| {fmt(r['paper_K'], r['paper_iters'])}")
                     out.append(f"| {coarse} | " + " | ".join(cells) + " |")
             out.append("")
             for r in rs:
                 if "oracle_iters" in r:
                     par_total += 1
-                    par_ok += int(r["oracle_iters"] == r["iters"] and abs(r["oracle_K"] - r["K"]) <= 1e-3 * r["K"])
-                    dev_it = max(dev_it, abs(r["oracle_iters"] - r["iters"]) / r["oracle_iters"])
+                    within2 = abs(r["oracle_iters"] - r["iters"]) <= 2
+                    kok = abs(r["oracle_K"] - r["K"]) <= 1e-2 * r["oracle_K"]
+                    par_ok += int(within2 and kok)
+                    if not within2:
+                        spread_cases.append(r)
+                        par_spread += int(bool(r.get("within_spread")) and kok)
                     dev_k = max(dev_k, abs(r["oracle_K"] - r["K"]) / r["oracle_K"])
-    out.append(f"Oracle parity: {par_ok} of {par_total} cases with the oracle run have identical iteration counts "
-               f"and K within 0.1%. Largest deviation over all {par_total}: iterations {100 * dev_it:.1f}%, "
-               f"K {100 * dev_k:.2f}% (the long, K up to 4e7 runs of Ex.1, where the stopping iteration of CG "
-               f"in fp64 depends on rounding order, DESIGN.md R22).")
-    times = [(r["solve_ms"], r) for r in rows]
+    out.append(f"Oracle parity (north_star: iterations within 2, K within 1%): {par_ok} of {par_total} oracle-checked "
+               f"cases. The other {len(spread_cases)} are long, K up to 4e7 runs where the stopping iteration of fp64 CG "
+               f"is not unique under rounding (DESIGN.md R22); for them the oracle's OWN iteration counts under "
+               f"last-bit perturbations of b, A and G were computed, and the GPU count lies inside that spread in "
+               f"{par_spread} of {len(spread_cases)}. Largest K deviation over all {par_total}: {100 * dev_k:.3f}%.")
+    out.append("")
+    if spread_cases:
+        out.append("| case | p | GPU iters | oracle iters | oracle spread | GPU K | oracle K |")
+        out.append("|---|---|---|---|---|---|---|")
+        for r in spread_cases:
+            sp = r.get("oracle_spread")
+            out.append(f"| {r['coarse'] if r['ex'] != 1 else '/'.join(map(str, r['coarse']))} (ex{r['ex']}, N_h {r['n_fine']}) "
+                       f"| {r['p']} | {r['iters']} | {r['oracle_iters']} | {sp[0] if sp else '?'}..{sp[1] if sp else '?'} "
+                       f"| {r['K']:.6g} | {r['oracle_K']:.6g} |")
+    times = [(r["solve_ms"], r) for r in rows if "solve_ms" in r]
     out.append("")
     out.append("Solve times (GPU, one dgas_pcg incl. Lanczos): " +
                ", ".join(f"ex{r['ex']} p{r['p']} N_h={r['n_fine']}: {t:.1f} ms / {r['iters']} it"
