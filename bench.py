@@ -385,7 +385,12 @@ def main():
         "spmv_apply_pct_of_hbm_peak": 100 * spmv_apply_gbs / hbm_peak,
         "roofline": {"bound": "hbm", "achieved": kern[dom]["GBps"], "peak": hbm_peak, "unit": "GB/s",
                      "frac": kern[dom]["frac"], "traffic": traffic, "kernel": dom,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s",
+                     **({"note": (f"operators de-duplicated (exact, NEXT-4): A {info['dedup_A_bytes'] / 1e6:.1f} MB and "
+                                  f"local factors {info['dedup_local_bytes'] / 1e6:.1f} MB stored, L2-resident; "
+                                  f"'achieved' divides the SURVEY 8(d) algorithmic bytes (full envelope factor) by the "
+                                  f"launch time, 'traffic' is what ncu measured from DRAM")}
+                        if info.get("dedup_A_bytes") else {})},
         "kernels": kern,
         "e2e": {"value": e2e_value, "unit": "PCG it/s", "h2d_bytes_per_step": 2 * N * 8,
                 "d2h_bytes_per_step": N * 8},
