@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
     double rk[RN];  // narrow: r_k entries c = q + LPR t, prefetched one step ahead (overwritten after use)
     if constexpr (NARROW) {
 #pragma unroll
-      for (int t = 0; t < RN; ++t) rk[t] = q + LPR * t < NP ? rs[q + LPR * t] : 0.0;
+      for (int t = 0; t < RN; ++t) rk[t] = rs[min(q + LPR * t, NP - 1)];
     }
     for (int k = 0; k < m; ++k) {
       const int u0 = us_s[k], u1 = us_s[k + 1], fk = fk_s[k];
@@ -190,10 +190,11 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
               const int c = q + LPR * t;
               if (c < NP && c <= a) v1 += (double)Ps[panel_dcol(NP, c) + a - c] * rk[t];
             }
-            if constexpr (NARROW) {  // prefetch r_{k+1}
+            if constexpr (NARROW) {  // prefetch r_{k+1}: unconditional loads from valid addresses (the
+              // values are only used under c < NP), so the loads stay in flight until the next D step
+              const int kn = min(k + 1, m - 1);
 #pragma unroll
-              for (int t = 0; t < RN; ++t)
-                rk[t] = k + 1 < m && q + LPR * t < NP ? rs[(k + 1) * NP + q + LPR * t] : 0.0;
+              for (int t = 0; t < RN; ++t) rk[t] = rs[kn * NP + min(q + LPR * t, NP - 1)];
             }
             j0 = 0; j1 = min(WU, CC0); Pu = Ps + DPK + a;
           } else {
@@ -520,9 +521,9 @@ __global__ void __launch_bounds__(128) k_local_warp(
       }
     }
     const double* rs = r + (size_t)s0 * NP;
-    double rk[RN];
+    double rk[RN];  // r_k entries c = h + LPR t (used only where c < NP: loads need no predicate)
 #pragma unroll
-    for (int t = 0; t < RN; ++t) rk[t] = h + LPR * t < NP && fwd_lane ? rs[h + LPR * t] : 0.0;
+    for (int t = 0; t < RN; ++t) rk[t] = rs[min(h + LPR * t, NP - 1)];
     // ---------------- forward sweep
     for (int k = 0; k < m; ++k) {
       const int u0 = us[k], u1 = us[k + 1], f = fk[k], WU = (k - f) * NP;
@@ -567,10 +568,10 @@ __global__ void __launch_bounds__(128) k_local_warp(
 #pragma unroll
       for (int h2 = 1; h2 < LPR; ++h2) tot += __shfl_sync(0xffffffffu, v, (a + NP * h2) & 31);
       if (h == 0 && lane < NP) Y[k * NP + a] = tot;
-      // prefetch r_{k+1}
+      // prefetch r_{k+1} (unconditional, valid addresses: stays in flight until the next D step)
+      const int kn = min(k + 1, m - 1);
 #pragma unroll
-      for (int t = 0; t < RN; ++t)
-        rk[t] = k + 1 < m && h + LPR * t < NP && fwd_lane ? rs[(k + 1) * NP + h + LPR * t] : 0.0;
+      for (int t = 0; t < RN; ++t) rk[t] = rs[kn * NP + min(h + LPR * t, NP - 1)];
       __syncwarp();
     }
     // ---------------- backward sweep: units in reverse; the last S units are still in the ring

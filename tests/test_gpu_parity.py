@@ -570,3 +570,53 @@ def test_dedup_is_bitwise_identical(monkeypatch):
     assert s0 == s1 == 0 and i0 == i1 and c0 == c1
     assert np.array_equal(y0, y1)
     assert np.array_equal(x0, x1)
+
+
+def test_error_paths_mesh_breakdown_notconverged(monkeypatch):
+    """include/dgas.h error contract: DGAS_E_MESH for a clockwise cell, for a non-manifold
+    edge and for overlap pieces that do not cover their fine cell; DGAS_E_BREAKDOWN for a non-finite
+    right-hand side; DGAS_NOT_CONVERGED (positive, iterate kept) when maxit is reached with the
+    nested-dissection coarse path."""
+    import copy
+    from paper_1903_11357_b200 import dgas
+    P = g.config(1)
+    P1 = copy.deepcopy(P)
+    a, b_ = P1.cell_ptr[5], P1.cell_ptr[6]
+    P1.cell_vtx = P1.cell_vtx.copy()
+    P1.cell_vtx[a:b_] = P1.cell_vtx[a:b_][::-1]  # clockwise loop
+    with pytest.raises(dgas.DgasError) as e:
+        dgas.Solver(P1)
+    assert e.value.code == dgas.E_MESH
+    P2 = copy.deepcopy(P)  # a duplicated cell: its edges are shared by three cells
+    n0 = P2.cell_ptr[1]
+    P2.cell_vtx = np.concatenate([P2.cell_vtx, P2.cell_vtx[:n0]]).astype(np.int32)
+    P2.cell_ptr = np.concatenate([P2.cell_ptr, [P2.cell_ptr[-1] + n0]]).astype(np.int32)
+    P2.part = np.concatenate([P2.part, [0]]).astype(np.int32)
+    P2.kappa = np.concatenate([P2.kappa, [1.0]])
+    if P2.parent is not None:
+        P2.parent = np.concatenate([P2.parent, [0]]).astype(np.int32)
+    with pytest.raises(dgas.DgasError) as e:
+        dgas.Solver(P2)
+    assert e.value.code == dgas.E_MESH
+    P4 = g.config(4, scale="small")  # non-nested: shrink one overlap piece so the cell is not covered
+    P4.ov_xy = P4.ov_xy.copy()
+    k0, k1 = P4.ov_ptr[0], P4.ov_ptr[1]
+    cen = P4.ov_xy[k0:k1].mean(0)
+    P4.ov_xy[k0:k1] = cen + 0.5 * (P4.ov_xy[k0:k1] - cen)
+    with pytest.raises(dgas.DgasError) as e:
+        dgas.Solver(P4)
+    assert e.value.code == dgas.E_MESH
+    S = _solver(P)
+    bad = torch.ones(S.N, dtype=torch.float64, device="cuda")
+    bad[7] = float("nan")
+    with pytest.raises(dgas.DgasError) as e:
+        S.pcg(bad, rtol=1e-8)
+    assert e.value.code == dgas.E_BREAKDOWN
+    S.close()
+    monkeypatch.setenv("DGAS_COARSE_MODE", "nd")
+    monkeypatch.setenv("DGAS_ND_LEAF", "2")
+    S = _solver(CASES["cfg2s"]())
+    b = S.rhs(g.F_SINSIN)
+    x, it, cond, st = S.pcg(b, rtol=1e-14, maxit=5)
+    assert st == dgas.NOT_CONVERGED and it == 5 and torch.isfinite(x).all() and cond >= 1
+    S.close()
