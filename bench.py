@@ -107,8 +107,10 @@ def l2_policy(P):
     """Deterministic from the problem (both arms print the same config): the operators of one PCG
     iteration (A and the local factors, >= ~12 n_p-blocks per cell) against the B200's 126 MB L2."""
     est = 12 * P.N * P.n_p * 8
+    vec = 6 * P.N * 8  # x, b, r, z, p, q
     if est > 126e6:
-        return f"inputs larger than L2 (operators ~{est / 1e9:.2f} GB > 126 MB L2; no flush needed)"
+        return (f"inputs larger than L2 (per-iteration working set > 126 MB: six N-vectors {vec / 1e6:.0f} MB plus "
+                f"the operators; no flush needed)")
     return f"L2-resident (operators ~{est / 1e6:.1f} MB fit the 126 MB L2; L2 flushed before every timed solve)"
 
 
@@ -371,7 +373,8 @@ def main():
                 else "single-gpu", "setup_s": t_setup,
                 "coarse_solver": ["dense-inverse", "band", "nested-dissection"][info["coarse_mode"]],
                 "coarse_refine_steps": refine, "coarse_solve_relerr": info["coarse_solve_relerr"],
-                "local_kernel": {1: "envelope", 2: "panel", 3: "explicit-inverse"}.get(info["local_kernel"]),
+                "local_kernel": {1: "envelope", 2: "panel", 3: "explicit-inverse", 4: "warp-per-subdomain"}.get(
+                    info["local_kernel"]),
                 "local_ctas_per_sm": info["local_ctas_per_sm"],
                 "operator_bytes": info["bytes_A"] + info["bytes_U"] + info["bytes_coarse"] + info["bytes_G"],
                 "l2_bytes": torch.cuda.get_device_properties(local).L2_cache_size},

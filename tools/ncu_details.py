@@ -14,7 +14,8 @@ import sys
 KEEP = ["Memory Throughput", "DRAM Throughput", "Duration", "Compute (SM) Throughput", "L2 Hit Rate",
         "Issued Warp Per Scheduler", "No Eligible", "Block Size", "Grid Size", "Registers Per Thread",
         "Dynamic Shared Memory Per Block", "Theoretical Occupancy", "Achieved Occupancy"]
-ROLE = {"k_local": "local", "k_local_panel": "local", "k_spmv3": "spmv", "k_spmv_ring": "spmv"}
+ROLE = {"k_local": "local", "k_local_panel": "local", "k_local_warp": "local", "k_local_inv": "local",
+        "k_spmv3": "spmv", "k_spmv_ring": "spmv", "k_spmv_dd": "spmv"}
 
 
 def run(args):
