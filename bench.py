@@ -373,7 +373,7 @@ def main():
                 else "single-gpu", "setup_s": t_setup,
                 "coarse_solver": ["dense-inverse", "band", "nested-dissection"][info["coarse_mode"]],
                 "coarse_refine_steps": refine, "coarse_solve_relerr": info["coarse_solve_relerr"],
-                "local_kernel": {1: "envelope", 2: "panel", 3: "explicit-inverse", 4: "warp-per-subdomain"}.get(
+                "local_kernel": {1: "envelope", 2: "panel", 3: "explicit-inverse", 4: "warp-per-subdomain", 5: "multi-rhs-shared-factor"}.get(
                     info["local_kernel"]),
                 "local_ctas_per_sm": info["local_ctas_per_sm"],
                 "operator_bytes": info["bytes_A"] + info["bytes_U"] + info["bytes_coarse"] + info["bytes_G"],

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdgas.so")
-SOURCES = ["setup_host.cu", "setup_kernels.cu", "coarse_kernels.cu", "iter_kernels.cu", "abi.cu", "nd_host.cu", "nd_kernels.cu", "local_panel.cu", "spmv_ring.cu", "local_inv.cu", "shard.cu", "dedup.cu"]
+SOURCES = ["setup_host.cu", "setup_kernels.cu", "coarse_kernels.cu", "iter_kernels.cu", "abi.cu", "nd_host.cu", "nd_kernels.cu", "local_panel.cu", "spmv_ring.cu", "local_inv.cu", "shard.cu", "dedup.cu", "local_mrhs.cu"]
 HEADERS = ["internal.h", "dense_cta.cuh", "tma.cuh", os.path.join("..", "..", "include", "dgas.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xcompiler", "-fPIC",

@@ -29,6 +29,8 @@ int dedup_setup(dgas_ctx ctx) {
   if (!on || ctx->spmv_kernel != 4) return 0;
   const int nc = ctx->nc;
   cudaStream_t s = ctx->stream;
+  double maxfrac = 0.25;  // stored / total above which de-duplication is not worth it (tests: small meshes)
+  if (const char* e = std::getenv("DGAS_DEDUP_MAXFRAC")) maxfrac = std::atof(e);
   DGAS_CUDA(cudaStreamSynchronize(s));
   // ---------------- A row-blocks
   {
@@ -56,7 +58,7 @@ int dedup_setup(dgas_ctx ctx) {
       }
     }
     // worth it only with real repetition (the compact store then fits L2 and the copies are L2 hits)
-    if ((double)stored < 0.25 * (double)ao[nc]) {
+    if ((double)stored < maxfrac * (double)ao[nc]) {
       std::vector<double> Ac((size_t)stored);
       for (int r : reps) std::memcpy(Ac.data() + dd[r], A.data() + ao[r], (size_t)(ao[r + 1] - ao[r]) * 8);
       double* dA = nullptr;
@@ -72,6 +74,7 @@ int dedup_setup(dgas_ctx ctx) {
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       ctx->dd_grid = std::min(nc, 8 * nsm);  // k_spmv_dd: 8 x 256-thread CTAs per SM
       if (const char* e = std::getenv("DGAS_DD_CPS")) ctx->dd_grid = std::min(nc, std::max(1, std::atoi(e)) * nsm);
+      if ((st = spmv_cls_setup(ctx, dd))) return st;  // class-sorted SpMV (row-block in registers)
     }
   }
   // ---------------- local factors (merged panels), whole subdomains at a time
@@ -108,7 +111,7 @@ int dedup_setup(dgas_ctx ctx) {
     int64_t stored = 0;
     std::vector<int64_t> base(nsub, -1);
     for (int r : reps) { base[r] = stored; stored += po[sp[r + 1]] - po[sp[r]]; }
-    if ((double)stored < 0.25 * (double)ctx->p_total) {
+    if ((double)stored < maxfrac * (double)ctx->p_total) {
       std::vector<double> Pc((size_t)stored + 32);
       for (int r : reps) std::memcpy(Pc.data() + base[r], Pp.data() + po[sp[r]], (size_t)(po[sp[r + 1]] - po[sp[r]]) * 8);
       std::vector<int64_t> pn(nc + 1);
@@ -127,6 +130,7 @@ int dedup_setup(dgas_ctx ctx) {
       ctx->d_p_off = dpo;
       ctx->p_unique = (int)reps.size();
       ctx->p_bytes_stored = stored * 8;
+      if ((st = mrhs_setup(ctx, rep_of))) return st;  // batched solves over the shared factors
     }
   }
   if (std::getenv("DGAS_VERBOSE"))

@@ -60,6 +60,11 @@ struct NdPlan {
   int* d_prow = nullptr;
   double *d_rb = nullptr, *d_zb = nullptr;
   double* d_dsc = nullptr;             // diag(A0)^-1/2 (symmetric scaling of the fronts)
+  // solve v2 (k_nd_fwd2 / k_nd_bwd2): one descriptor per work item, flat gather / child-source tables
+  void *d_wf2 = nullptr, *d_wb2 = nullptr;  // NdItem[] per direction
+  int *d_gF = nullptr, *d_gU = nullptr;
+  int2* d_tsrc = nullptr;
+  int v2 = 0, pdl = 0;
 };
 
 // Subdomain-sharded multi-GPU solve (shard.cu): this rank's view of the replicated context
@@ -112,9 +117,20 @@ struct dgas_ctx_s {
   // exact de-duplication of bitwise-identical operator data (dedup.cu; NEXT-4 Cartesian de-duplication)
   int64_t* d_a_dd = nullptr;          // [nc] compact-store offset of each cell's row-block (nullptr: off)
   int dd_grid = 0;                     // persistent CTAs of k_spmv_dd
+  int4* d_cls_items = nullptr;         // k_spmv_cls work items (class, first cell, count, W)
+  int64_t* d_cls_off = nullptr;        // compact-store offset per row-block class
+  int* d_cls_cells = nullptr;          // cells grouped by class
+  int* d_cls_nb = nullptr;             // [nc][CLS_MAXDEG] neighbour cells of d_cls_cells[i]
+  int cls_nitems = 0, cls_grid = 0;
   std::vector<int64_t> a_dd_h;
   int64_t a_unique = 0, a_bytes_stored = 0;  // distinct row-blocks, bytes of the compact A
   int p_unique = 0;                   // distinct subdomain factors (panel store)
+  // multiple-right-hand-side local solve over subdomains sharing a factor (local_mrhs.cu, local_kernel 5)
+  int4* d_mr_batches = nullptr;       // (representative subdomain, first member, count, 0) per batch
+  int* d_mr_members = nullptr;        // member subdomains, grouped by batch
+  int mr_nbatch = 0, mr_B = 0, mr_BS = 1, mr_S = 4, mr_WC = 1, mr_grid = 0, mr_classes = 0;
+  uint32_t mr_slot = 0;
+  size_t mr_smem = 0;
   int64_t p_bytes_stored = 0;
   NdPlan nd;
   double* d_A0b = nullptr;   // A0 blocks per coarse pair (n_pairs x nq x nq)
@@ -333,6 +349,9 @@ void launch_local_inv_range(dgas_ctx ctx, int sub_begin, int sub_end, const doub
 void launch_local_panel_range(dgas_ctx ctx, int sub_begin, int sub_end, const double* r, double* z, cudaStream_t s);
 int local_warp_setup(dgas_ctx ctx);
 int dedup_setup(dgas_ctx ctx);
+int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of);
+int spmv_cls_setup(dgas_ctx ctx, const std::vector<int64_t>& dd);
+void launch_local_mrhs(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s);
 void launch_local_warp(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s);
 void launch_spmv_range(dgas_ctx ctx, int c_begin, int c_end, const double* x, double* y, cudaStream_t s);
 void launch_coarse_only(dgas_ctx ctx, cudaStream_t s);

@@ -1192,6 +1192,10 @@ static void launch_local(dgas_ctx ctx, int mode, PcgState* st, const double* r, 
     launch_local_warp(ctx, mode, st, r, z, s);
     return;
   }
+  if (ctx->local_kernel == 5) {
+    launch_local_mrhs(ctx, mode, st, r, z, s);
+    return;
+  }
   const size_t smem = apply_smem_bytes(ctx);
   DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
                          mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,

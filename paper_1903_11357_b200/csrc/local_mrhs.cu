@@ -1,0 +1,402 @@
+// local_mrhs.cu — the local solves z_i = A_i^-1 r_i (the exact local solvers of the
+// additive Schwarz operator) for subdomains that SHARE their factor, as one
+// multiple-right-hand-side triangular solve per batch of subdomains.
+//
+// After exact de-duplication (dedup.cu) the 4,096 subdomains of config 3 use 64 distinct factors (one
+// class of 3,844 interior subdomains). The per-subdomain kernels (k_local_warp, k_local_panel) run one
+// dependent 2 x 64-step chain per subdomain: ~1 us per step, latency-bound (ncu: 21% occupancy, issue
+// 0.51, L2 hit 96%). Here a CTA solves a batch of B subdomains of one class at once: every chain step
+// is a small dense product with B columns instead of one,
+//   forward  L y = r   : Y_k = P_k [R_k ; Y_{f_k..k-1}]          (NP x (NP + WU)) x (.. x B)
+//   backward L^T z = y : V = P_k^T U_k, Z_k = V[0..NP), Y_{f_k..k-1} += V[NP..)    (U_k = Y_k)
+// with P_k = [D_k | -U_k] the merged panel of cell k (local_panel.cu layout), so the chain runs 2m
+// steps per BATCH instead of per subdomain and every factor element loaded is used B times.
+//   * Y (m NP rows x B columns, fp64) lives in shared memory, row stride BS odd (conflict-free column
+//     access); r is loaded into it, y overwrites r in place, z goes straight to global memory.
+//   * One panel per step streamed by cp.async.bulk into an S-slot ring (thread 0 issues, S steps ahead;
+//     the CTA barrier that ends a step releases its slot). The factors are L2-resident (20.5 MB on
+//     config 3) and stay so (evict-last).
+//   * Forward step: lanes = (column b of the batch, half), warps x halves = 16 column slices of the
+//     step's panel; each thread accumulates all NP rows for its b over its slice, halves combine by a
+//     shuffle, the 8 warps' partials by a shared-memory sum in fixed order (deterministic).
+//   * Backward step: the same slices own panel columns; u_k (NP values per b) in registers.
+// The batches (class, members) and the batch size are chosen on the host (mrhs_setup) so that all
+// batches run in one wave; DGAS_MRHS=0 disables the kernel, DGAS_MR_B / DGAS_MR_S force B / slots.
+#include <algorithm>
+#include <map>
+
+#include "internal.h"
+#include "tma.cuh"
+
+#define MR_T 256
+#define MR_NW (MR_T / 32)
+
+// panel layout helpers (same definitions as local_panel.cu)
+template <int NP> __host__ __device__ constexpr int mr_dpk() { return (NP * (NP + 1) / 2 + 1) / 2 * 2; }
+__host__ __device__ constexpr int mr_dcol(int np, int c) { return c * np - c * (c - 1) / 2; }
+
+// dynamic smem: full[16] | fk[mc] | fm[mc] | slt[mc] | po[mc] | mb[32] | red[NW][NP][BMAX] | W[WC NP][BS] | ring
+// W is a WINDOW of WC cells (row = (cell mod WC) NP + component, column b): the forward step k needs
+// cells f_k..k, the backward step k cells fm_k..k (fm_k = min_{j >= k} f_j), both at most maxbw + 1 cells;
+// r_{k+PD} / the y rows entering the backward window are prefetched PD steps ahead by cp.async into the
+// slots of cells that are done, so WC = maxbw + PD + 1. y goes to global memory (the z array serves as
+// the temporary: y_k is stored at z_k's place and read back by the backward sweep before z_k overwrites
+// it), so shared memory no longer grows with the subdomain size and B = 32 fits several CTAs per SM.
+#define MR_PD 6
+struct MrLayout {
+  size_t off_fk, off_fm, off_slt, off_po, off_mb, off_red, off_W, off_ring, total;
+  __host__ __device__ MrLayout(int mc, int np, int bmax, int bs, int wc, int S, uint32_t slot) {
+    off_fk = 128;
+    off_fm = off_fk + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_slt = off_fm + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_po = off_slt + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_mb = off_po + (size_t)mc * 8;
+    off_red = off_mb + 32 * 8;
+    off_W = off_red + (size_t)MR_NW * np * bmax * 8;
+    off_ring = (off_W + (size_t)wc * np * bs * 8 + 127) & ~(size_t)127;
+    total = off_ring + (size_t)S * slot;
+  }
+};
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NP>
+__global__ void __launch_bounds__(MR_T) k_local_mrhs(int mode, int nbatch, const int4* __restrict__ batches,
+                                                     const int* __restrict__ members, const int* __restrict__ sub_ptr,
+                                                     const int* __restrict__ first, const int64_t* __restrict__ p_off,
+                                                     const double* __restrict__ P, const double* r_in,
+                                                     double* const* rbuf, double* z, const PcgState* st, int S,
+                                                     uint32_t slot_bytes, int bmax, int BS, int WC, int max_cells) {
+  constexpr int DPK = mr_dpk<NP>();
+  extern __shared__ __align__(128) unsigned char sm[];
+  const double* r = r_in;
+  if (mode >= 1) {
+    if (st->done) return;
+    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+  }
+  const MrLayout L(max_cells, NP, bmax, BS, WC, S, slot_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  int* fk = reinterpret_cast<int*>(sm + L.off_fk);
+  int* fm = reinterpret_cast<int*>(sm + L.off_fm);
+  int* slt = reinterpret_cast<int*>(sm + L.off_slt);
+  int64_t* po = reinterpret_cast<int64_t*>(sm + L.off_po);
+  int64_t* mb = reinterpret_cast<int64_t*>(sm + L.off_mb);
+  double* red = reinterpret_cast<double*>(sm + L.off_red);
+  double* W = reinterpret_cast<double*>(sm + L.off_W);
+  unsigned char* ring = sm + L.off_ring;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int WR = WC * NP;  // window rows
+  if (tid == 0) {
+    for (int t = 0; t < S; ++t) mbar_init(&full[t], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = l2_evict_last();  // every batch of a class re-reads its factor: keep it in L2
+  const int SM1 = S - 1;
+  uint32_t gt = 0;  // steps this CTA has consumed: slot (g & SM1), parity (g / S) & 1
+  for (int bi = blockIdx.x; bi < nbatch; bi += gridDim.x) {
+    const int4 bt = batches[bi];
+    const int rep = bt.x, moff = bt.y, B = bt.z;
+    const int s0 = sub_ptr[rep], m = sub_ptr[rep + 1] - s0, T2 = 2 * m;
+    for (int k = tid; k < m; k += MR_T) {
+      fk[k] = first[s0 + k];
+      po[k] = p_off[s0 + k];
+      slt[k] = k % WC;
+    }
+    if (tid < B) mb[tid] = (int64_t)sub_ptr[members[moff + tid]] * NP;
+    __syncthreads();
+    if (tid == 0) {  // fm_k = min_{j >= k} f_j (the backward window's low end, monotone)
+      int mn = 1 << 30;
+      for (int k = m - 1; k >= 0; --k) { mn = min(mn, fk[k]); fm[k] = mn; }
+    }
+    // step t: forward cell t (t < m), backward cell 2m-1-t
+    auto issue = [&](int t) {
+      const int k = t < m ? t : T2 - 1 - t;
+      const int n = DPK + (k - fk[k]) * NP * NP;  // D triangle + (k - f_k) NP columns of NP rows
+      const uint32_t g = gt + (uint32_t)t;
+      bulk_load(ring + (size_t)(g & SM1) * slot_bytes, P + po[k], (uint32_t)(((n + 1) & ~1) * 8), &full[g & SM1], pol);
+    };
+    if (tid == 0)
+      for (int t = 0; t < min(S, T2); ++t) issue(t);
+    // cp.async of NP rows x B columns of cell c from global (src: r or the y temporaries in z) into its slot
+    auto fetch = [&](const double* src, int c) {
+      double* dst = W + (size_t)slt[c] * NP * BS;
+      for (int e = tid; e < NP * B; e += MR_T) {
+        const int bb = e / NP, i = e - bb * NP;
+        cp_async8(dst + (size_t)i * BS + bb, src + mb[bb] + (int64_t)c * NP + i);
+      }
+    };
+    __syncthreads();  // slt / mb visible to fetch
+    for (int c = 0; c < MR_PD; ++c) {
+      if (c < m) fetch(r, c);
+      cp_async_commit();
+    }
+    cp_async_wait<MR_PD - 1>();
+    __syncthreads();
+    const int H = B <= 16 ? 2 : 1;  // halves of a warp on different panel columns when B <= 16
+    const int b = H == 2 ? (lane & 15) : lane, half = H == 2 ? (lane >> 4) : 0;
+    const int NSL = MR_NW * H, sl = w * H + half;
+    const bool act = b < B;
+    // ------------------------------------------------ forward sweep
+    for (int k = 0; k < m; ++k) {
+      const uint32_t g = gt + (uint32_t)k;
+      mbar_wait(&full[g & SM1], (g / S) & 1);
+      const double* Ps = reinterpret_cast<const double*>(ring + (size_t)(g & SM1) * slot_bytes);
+      const int f = fk[k], K = NP + (k - f) * NP, rk = slt[k] * NP, rf = slt[f] * NP;
+      double acc[NP];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) acc[i] = 0.0;
+      if (act) {
+        for (int q = sl; q < K; q += NSL) {
+          if (q < NP) {  // D column q (rows q..NP-1) times r_k[q]
+            const double rv = W[(size_t)(rk + q) * BS + b];
+            const double* col = Ps + mr_dcol(NP, q) - q;
+#pragma unroll
+            for (int i = 0; i < NP; ++i)
+              if (i >= q) acc[i] += col[i] * rv;
+          } else {  // -U column j times y_old[j] (window rows wrap at WR)
+            const int j = q - NP;
+            int row = rf + j;
+            row -= row >= WR ? WR : 0;
+            const double yv = W[(size_t)row * BS + b];
+            const double* col = Ps + DPK + j * NP;
+            if constexpr (NP % 2 == 0) {
+              const double2* c2 = reinterpret_cast<const double2*>(col);
+#pragma unroll
+              for (int i = 0; i < NP / 2; ++i) {
+                const double2 pv = c2[i];
+                acc[2 * i] += pv.x * yv;
+                acc[2 * i + 1] += pv.y * yv;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < NP; ++i) acc[i] += col[i] * yv;
+            }
+          }
+        }
+      }
+      if (H == 2) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+      }
+      if (act) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i)
+          if (H == 1 || (half == 0) == (i < NP / 2)) red[(w * NP + i) * bmax + b] = acc[i];
+      }
+      __syncthreads();  // partials written; the step's ring slot is consumed
+      if (tid == 0 && k + S < T2) issue(k + S);
+      if (k + MR_PD < m) fetch(r, k + MR_PD);  // slot of cell k + PD - WC < f_k: free
+      cp_async_commit();
+      for (int o = tid; o < NP * B; o += MR_T) {
+        const int bb = o / NP, i = o - bb * NP;
+        double s = 0;
+#pragma unroll
+        for (int ww = 0; ww < MR_NW; ++ww) s += red[(ww * NP + i) * bmax + bb];
+        W[(size_t)(rk + i) * BS + bb] = s;
+        z[mb[bb] + (int64_t)k * NP + i] = s;  // y_k, read back by the backward sweep
+      }
+      cp_async_wait<MR_PD - 1>();  // r_{k+1} landed
+      __syncthreads();
+    }
+    // ------------------------------------------------ backward sweep
+    // the window holds y of cells max(0, m - WC) .. m-1; cells below are fetched PD steps ahead
+    int lo = max(0, m - WC);
+    for (int kk = m - 1; kk >= max(0, m - MR_PD); --kk) {
+      if (fm[kk] < lo) {
+        for (int c = fm[kk]; c < lo; ++c) fetch(z, c);
+        lo = fm[kk];
+      }
+      cp_async_commit();
+    }
+    cp_async_wait<MR_PD - 1>();
+    __syncthreads();
+    for (int k = m - 1; k >= 0; --k) {
+      const int t = T2 - 1 - k;
+      const uint32_t g = gt + (uint32_t)t;
+      mbar_wait(&full[g & SM1], (g / S) & 1);
+      const double* Ps = reinterpret_cast<const double*>(ring + (size_t)(g & SM1) * slot_bytes);
+      const int f = fk[k], K = NP + (k - f) * NP, rk = slt[k] * NP, rf = slt[f] * NP;
+      if (act) {
+        double uk[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) uk[i] = W[(size_t)(rk + i) * BS + b];
+        for (int q = sl; q < K; q += NSL) {
+          if (q < NP) {  // z_k[q] = (D_k^T u_k)[q]
+            const double* col = Ps + mr_dcol(NP, q) - q;
+            double v = 0;
+#pragma unroll
+            for (int i = 0; i < NP; ++i)
+              if (i >= q) v += col[i] * uk[i];
+            z[mb[b] + (int64_t)k * NP + q] = v;
+          } else {  // y_old[j] += (-U_k^T u_k)[j]
+            const int j = q - NP;
+            int row = rf + j;
+            row -= row >= WR ? WR : 0;
+            const double* col = Ps + DPK + j * NP;
+            double v0 = 0, v1 = 0;
+            if constexpr (NP % 2 == 0) {
+              const double2* c2 = reinterpret_cast<const double2*>(col);
+#pragma unroll
+              for (int i = 0; i < NP / 2; ++i) {
+                const double2 pv = c2[i];
+                v0 += pv.x * uk[2 * i];
+                v1 += pv.y * uk[2 * i + 1];
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i + 1 < NP; i += 2) {
+                v0 += col[i] * uk[i];
+                v1 += col[i + 1] * uk[i + 1];
+              }
+              v0 += col[NP - 1] * uk[NP - 1];
+            }
+            W[(size_t)row * BS + b] += v0 + v1;
+          }
+        }
+      }
+      // y rows of the cells the step k - PD needs (slots of cells > k, done)
+      const int k2 = k - MR_PD;
+      if (k2 >= 0 && fm[k2] < lo) {
+        for (int c = fm[k2]; c < lo; ++c) fetch(z, c);
+        lo = fm[k2];
+      }
+      cp_async_commit();
+      cp_async_wait<MR_PD - 1>();
+      __syncthreads();
+      if (tid == 0 && t + S < T2) issue(t + S);
+    }
+    gt += (uint32_t)T2;
+  }
+}
+
+#define DISPATCH_MR(P, ...)                                 \
+  switch (P) {                                              \
+    case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
+    case 2: { constexpr int NP_ = 6; __VA_ARGS__; } break;  \
+    case 3: { constexpr int NP_ = 10; __VA_ARGS__; } break; \
+    case 4: { constexpr int NP_ = 15; __VA_ARGS__; } break; \
+  }
+
+// Host: classes of subdomains sharing a factor (rep_of from dedup.cu), batch size and geometry.
+// Cost model: the chain is 2m steps per batch whatever B, a step's shared-memory traffic grows with B,
+// so take the B that runs every batch in the fewest waves, then the smallest such B.
+int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
+  int on = 1;
+  if (const char* e = std::getenv("DGAS_MRHS")) on = std::atoi(e) != 0;
+  if (!on || ctx->p < 1 || ctx->p > 4 || ctx->max_sub_cells <= 1) return 0;
+  const int nsub = ctx->nsub, np = ctx->np, mc = ctx->max_sub_cells;
+  std::map<int, std::vector<int>> cls;
+  for (int s2 = 0; s2 < nsub; ++s2) cls[rep_of[s2]].push_back(s2);
+  // worth it only when subdomains really share factors (on average several per class)
+  double minavg = 4.0;
+  if (const char* e = std::getenv("DGAS_MR_MINAVG")) minavg = std::atof(e);  // tests: small meshes
+  if ((double)nsub / (double)cls.size() < minavg) return 0;
+  int dev = 0, nsm = 148, smem_sm = 233472, optin = 232448;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // widest panel of the representatives (bytes, 128-aligned slot)
+  const int dpk = (np * (np + 1) / 2 + 1) / 2 * 2;
+  int maxn = 0;
+  for (auto& kv : cls) {
+    const int rep = kv.first;
+    for (int c = ctx->sub_ptr_h[rep]; c < ctx->sub_ptr_h[rep + 1]; ++c) {
+      const int k = c - ctx->sub_ptr_h[rep];
+      maxn = std::max(maxn, dpk + (k - ctx->first_h[c]) * np * np);
+    }
+  }
+  const uint32_t slot = (uint32_t)((((maxn + 1) & ~1) * 8 + 127) / 128 * 128);
+  // window: the widest backward reach k - min_{j >= k} f_j (>= the forward reach k - f_k) + prefetch distance
+  int maxbw = 0;
+  for (auto& kv : cls) {
+    const int rep = kv.first, c0 = ctx->sub_ptr_h[rep], m = ctx->sub_ptr_h[rep + 1] - c0;
+    int mn = 1 << 30;
+    for (int k = m - 1; k >= 0; --k) {
+      mn = std::min(mn, ctx->first_h[c0 + k]);
+      maxbw = std::max(maxbw, k - mn);
+    }
+  }
+  const int WC = std::min(mc, maxbw + MR_PD + 1);
+  int S = 4;
+  if (const char* e = std::getenv("DGAS_MR_S")) S = std::max(2, std::atoi(e));
+  while (S & (S - 1)) ++S;  // power of two
+  // room for one coarse-solve CTA per SM beside the local solves (the coarse chain runs concurrently)
+  size_t reserve = 8 * 1024;
+  if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;
+  int bforce = 0;
+  if (const char* e = std::getenv("DGAS_MR_B")) bforce = std::max(1, std::min(32, std::atoi(e)));
+  // fewest waves, then fewest batches (a step's instruction count per warp hardly depends on B <= 32)
+  int bestB = 0, bestW = 1 << 30, bestCps = 0;
+  int64_t bestNb = 1LL << 40;
+  for (int B = 1; B <= 32; ++B) {
+    if (bforce && B != bforce) continue;
+    const int BS = B | 1;
+    const size_t need = MrLayout(mc, np, B, BS, WC, S, slot).total;
+    if (need > (size_t)optin) continue;
+    const int cps = std::min<int>(2048 / MR_T, (int)(((size_t)smem_sm - std::min((size_t)smem_sm / 2, reserve)) / (need + 1024)));
+    if (cps < 1) continue;
+    int64_t nb = 0;
+    for (auto& kv : cls) nb += ((int64_t)kv.second.size() + B - 1) / B;
+    const int waves = (int)((nb + (int64_t)cps * nsm - 1) / ((int64_t)cps * nsm));
+    if (waves < bestW || (waves == bestW && nb < bestNb)) { bestW = waves; bestB = B; bestCps = cps; bestNb = nb; }
+  }
+  if (!bestB) return 0;
+  const int B = bestB, BS = B | 1;
+  // batches: each class split into ceil(n/B) batches of near-equal size, largest first
+  std::vector<int4> bat;
+  std::vector<int> mem;
+  for (auto& kv : cls) {
+    const int n = (int)kv.second.size(), nbat = (n + B - 1) / B;
+    int off = 0;
+    for (int t = 0; t < nbat; ++t) {
+      const int cnt = n / nbat + (t < n % nbat ? 1 : 0);
+      bat.push_back(make_int4(kv.first, (int)mem.size(), cnt, 0));
+      for (int u = 0; u < cnt; ++u) mem.push_back(kv.second[off + u]);
+      off += cnt;
+    }
+  }
+  std::stable_sort(bat.begin(), bat.end(), [](const int4& a, const int4& b2) { return a.z > b2.z; });
+  int st;
+  if ((st = dev_upload(ctx, &ctx->d_mr_batches, bat)) || (st = dev_upload(ctx, &ctx->d_mr_members, mem))) return st;
+  ctx->mr_nbatch = (int)bat.size();
+  ctx->mr_B = B;
+  ctx->mr_BS = BS;
+  ctx->mr_S = S;
+  ctx->mr_slot = slot;
+  ctx->mr_WC = WC;
+  ctx->mr_smem = MrLayout(mc, np, B, BS, WC, S, slot).total;
+  ctx->mr_grid = std::min(ctx->mr_nbatch, bestCps * nsm);
+  ctx->mr_classes = (int)cls.size();
+  cudaError_t e = cudaSuccess;
+  DISPATCH_MR(ctx->p, ({
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, k_local_mrhs<NP_>);
+    if (e == cudaSuccess && (size_t)optin < ctx->mr_smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_local_mrhs<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  }));
+  if (e != cudaSuccess) { ctx->detail = std::string("mrhs local smem: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
+  if (std::getenv("DGAS_VERBOSE")) {
+    size_t big = 0;
+    for (auto& kv : cls) big = std::max(big, kv.second.size());
+    fprintf(stderr, "dgas: multi-RHS local solve: %d classes (largest %zu), %d batches of <= %d, %d CTAs (%d/SM, %d wave(s)), "
+            "window %d cells, ring %d x %u B, smem/CTA %zu\n", ctx->mr_classes, big, ctx->mr_nbatch, B, ctx->mr_grid,
+            bestCps, bestW, WC, S, slot, ctx->mr_smem);
+  }
+  ctx->local_kernel = 5;
+  return 0;
+}
+
+void launch_local_mrhs(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s) {
+  DISPATCH_MR(ctx->p, (k_local_mrhs<NP_><<<ctx->mr_grid, MR_T, ctx->mr_smem, s>>>(
+                          mode, ctx->mr_nbatch, ctx->d_mr_batches, ctx->d_mr_members, ctx->d_sub_ptr, ctx->d_first,
+                          ctx->d_p_off, reinterpret_cast<const double*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->mr_S,
+                          ctx->mr_slot, ctx->mr_B, ctx->mr_BS, ctx->mr_WC, ctx->max_sub_cells)));
+}

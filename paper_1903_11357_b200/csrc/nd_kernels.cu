@@ -9,14 +9,15 @@
 #include "internal.h"
 
 #define ND_T 256
-#define ND_ROWS 32  // rows of a front per CTA in the solve
+#define ND_ROWS 16  // rows of a front per CTA in the solve
+#define ND_RW (ND_ROWS / (ND_T / 32))  // rows per warp, computed together
 
 // Solve-phase operator loads (X_F, M_F, M_F^T) carry an L2 evict-last policy: the chain of level
 // launches is latency-bound and runs beside the HBM-saturating local solves, so it should find its
 // factors in L2 (the streamed SpMV / local-solve copies are evict-first). DGAS_ND_L2=0 disables it.
 __device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
   double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ uint64_t nd_policy(int keep) {
@@ -198,15 +199,42 @@ __global__ void __launch_bounds__(ND_T) k_nd_fwd(int nq, const int2* __restrict_
   }
   if (row0 == 0)
     for (int k = threadIdx.x; k < nf; k += ND_T) Tg[offT[f] + k] = t[k];
+  // GEMV rows: each warp owns ND_RW rows and keeps ND_RW x 4 loads in flight per lane (a level is a
+  // short dependent chain: memory latency, not bandwidth, sets its time)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* M = Mg + offM[f];
   const int rend = min(nu, row0 + ND_ROWS);
-  for (int r = row0 + w; r < rend; r += ND_T / 32) {
-    const double* mr = M + (size_t)r * nf;
-    double v = 0;
-    for (int k = lane; k < nf; k += 32) v += ld_keep(mr + k, pol) * t[k];
-    v = warp_sum(v);
-    if (lane == 0) ug[offu[f] + r] = t[nf + r] - v;
+  const double* mr[ND_RW];
+  double v[ND_RW];
+#pragma unroll
+  for (int i = 0; i < ND_RW; ++i) {
+    const int r = row0 + w + (ND_T / 32) * i;
+    mr[i] = M + (size_t)(r < rend ? r : row0) * nf;
+    v[i] = 0.0;
+  }
+  for (int k0 = 0; k0 < nf; k0 += 128) {
+    double tk[4], a[ND_RW][4];
+    int kk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + lane + 32 * u;
+      kk[u] = min(k, nf - 1);
+      tk[u] = k < nf ? t[k] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < ND_RW; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[i][u] = ld_keep(mr[i] + kk[u], pol);
+#pragma unroll
+    for (int i = 0; i < ND_RW; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[i] += a[i][u] * tk[u];
+  }
+#pragma unroll
+  for (int i = 0; i < ND_RW; ++i) {
+    const int r = row0 + w + (ND_T / 32) * i;
+    const double vv = warp_sum(v[i]);
+    if (lane == 0 && r < rend) ug[offu[f] + r] = t[nf + r] - vv;
   }
   }
 }
@@ -233,23 +261,49 @@ __global__ void __launch_bounds__(ND_T) k_nd_bwd(int nq, const int2* __restrict_
   for (int k = threadIdx.x; k < nf; k += ND_T) tF[k] = Tg[offT[f] + k];
   for (int k = threadIdx.x; k < nu; k += ND_T) {
     const size_t g = (size_t)Ue[offUe[f] + k / nq] * nq + k % nq;
-    xU[k] = z0[g] / dsc[g];  // the scaled unknown of an ancestor front
+    xU[k] = -z0[g] / dsc[g];  // the scaled unknown of an ancestor front (negated: one dot product)
   }
   __syncthreads();
+  // row j: x_F[j] = sum_k X[j][k] tF[k] + sum_k MT[j][k] (-x_U[k]) over the concatenated k in [0, nf + nu)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* X = Xg + offX[f];
   const double* MT = MTg + offM[f];
-  const int rend = min(nf, row0 + ND_ROWS);
-  for (int j = row0 + w; j < rend; j += ND_T / 32) {
-    const double* xr = X + (size_t)j * nf;
-    const double* mr = MT + (size_t)j * nu;
-    double v = 0;
-    for (int k = lane; k < nf; k += 32) v += ld_keep(xr + k, pol) * tF[k];
-    for (int k = lane; k < nu; k += 32) v -= ld_keep(mr + k, pol) * xU[k];
-    v = warp_sum(v);
-    if (lane == 0) {
+  const int rend = min(nf, row0 + ND_ROWS), nk = nf + nu;
+  const double* xr[ND_RW];
+  const double* mr[ND_RW];
+  double v[ND_RW];
+#pragma unroll
+  for (int i = 0; i < ND_RW; ++i) {
+    const int j = row0 + w + (ND_T / 32) * i, jj = j < rend ? j : row0;
+    xr[i] = X + (size_t)jj * nf;
+    mr[i] = MT + (size_t)jj * nu - nf;
+    v[i] = 0.0;
+  }
+  for (int k0 = 0; k0 < nk; k0 += 128) {
+    double sk[4], a[ND_RW][4];
+    int kk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + lane + 32 * u;
+      kk[u] = min(k, nk - 1);
+      sk[u] = k < nk ? sh[k] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < ND_RW; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[i][u] = ld_keep((kk[u] < nf ? xr[i] : mr[i]) + kk[u], pol);
+#pragma unroll
+    for (int i = 0; i < ND_RW; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[i] += a[i][u] * sk[u];
+  }
+#pragma unroll
+  for (int i = 0; i < ND_RW; ++i) {
+    const int j = row0 + w + (ND_T / 32) * i;
+    const double vv = warp_sum(v[i]);
+    if (lane == 0 && j < rend) {
       const size_t g = (size_t)Fe[offFe[f] + j / nq] * nq + j % nq;
-      z0[g] = v * dsc[g];
+      z0[g] = vv * dsc[g];
     }
   }
   }
@@ -262,6 +316,8 @@ static int up(dgas_ctx ctx, T** d, const std::vector<T>& h) {
   if (!h.empty()) DGAS_CUDA(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
   return 0;
 }
+
+static int nd_v2_build(dgas_ctx ctx);
 
 int nd_setup_run(dgas_ctx ctx) {
   NdPlan& P = ctx->nd;
@@ -334,7 +390,278 @@ int nd_setup_run(dgas_ctx ctx) {
   cudaFree(dS);
   cudaFree(dUpd);
   P.bytes = (P.h_offX[nf] + 2 * P.h_offM[nf]) * 8;
+  P.v2 = 1;
+  if (const char* e = std::getenv("DGAS_ND_V2")) P.v2 = std::atoi(e) != 0;
+  P.pdl = 1;
+  if (const char* e = std::getenv("DGAS_ND_PDL")) P.pdl = std::atoi(e) != 0;
+  if (P.v2) {
+    const int r = nd_v2_build(ctx);
+    if (r < 0) return -r;
+    if (r > 0) P.v2 = 0;
+  }
+  if (!P.v2) P.pdl = 0;
   return 0;
+}
+
+
+// ------------------------------------------------------------------ solve v2
+// Same arithmetic as k_nd_fwd / k_nd_bwd (the t assembly adds r0 dsc, then child 1, then child 2),
+// with fewer dependent memory rounds per level: one 64-byte descriptor per work item, the global
+// indices of F and U precomputed (gF, gU), and for every position of t the child-u sources (tsrc).
+// With programmatic dependent launch (DGAS_ND_PDL) a level's CTAs start while the previous level runs
+// and load their static tables before griddepcontrol.wait.
+struct __align__(16) NdItem {
+  int f, row0, nf, nu;
+  int offT, offu, gofs, sofs;
+  long long offM, offX;
+  int gUofs, pad0, pad1, pad2;
+};
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+__global__ void __launch_bounds__(ND_T) k_nd_fwd2(const NdItem* __restrict__ items, int nwork, const int* __restrict__ gF,
+                                                  const int2* __restrict__ tsrc, const double* __restrict__ Mg,
+                                                  const double* __restrict__ dsc, const double* r0, double* Tg,
+                                                  double* ug, const PcgState* st, int mode, int keep) {
+  extern __shared__ double t[];
+  pdl_launch();
+  const uint64_t pol = nd_policy(keep);
+  if (mode >= 1 && st->done) return;
+  bool waited = false;
+  for (int wk = blockIdx.x; wk < nwork; wk += gridDim.x) {
+    if (wk != (int)blockIdx.x) __syncthreads();
+    const NdItem it = items[wk];
+    const int nf = it.nf, nu = it.nu, n = nf + nu;
+    constexpr int KPT = 4;  // positions per thread held across the wait (n <= KPT * ND_T handled in one pass)
+    int gk[KPT];
+    int2 sk[KPT];
+    for (int k0 = 0; k0 < n; k0 += KPT * ND_T) {
+#pragma unroll
+      for (int u = 0; u < KPT; ++u) {
+        const int k = k0 + threadIdx.x + u * ND_T;
+        gk[u] = k < nf ? gF[it.gofs + k] : -1;
+        sk[u] = k < n ? tsrc[it.sofs + k] : make_int2(-1, -1);
+      }
+      if (!waited) { pdl_wait(); waited = true; }
+#pragma unroll
+      for (int u = 0; u < KPT; ++u) {
+        const int k = k0 + threadIdx.x + u * ND_T;
+        if (k < n) {
+          double v = gk[u] >= 0 ? r0[gk[u]] * dsc[gk[u]] : 0.0;
+          if (sk[u].x >= 0) v += ug[sk[u].x];
+          if (sk[u].y >= 0) v += ug[sk[u].y];
+          t[k] = v;
+        }
+      }
+    }
+    __syncthreads();
+    if (it.row0 == 0)
+      for (int k = threadIdx.x; k < nf; k += ND_T) Tg[it.offT + k] = t[k];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* M = Mg + it.offM;
+    const int row0 = it.row0, rend = min(nu, row0 + ND_ROWS);
+    const double* mr[ND_RW];
+    double v[ND_RW];
+#pragma unroll
+    for (int i = 0; i < ND_RW; ++i) {
+      const int r = row0 + w + (ND_T / 32) * i;
+      mr[i] = M + (size_t)(r < rend ? r : row0) * nf;
+      v[i] = 0.0;
+    }
+    for (int k0 = 0; k0 < nf; k0 += 128) {
+      double tk[4], a[ND_RW][4];
+      int kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + lane + 32 * u;
+        kk[u] = min(k, nf - 1);
+        tk[u] = k < nf ? t[k] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < ND_RW; ++i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[i][u] = ld_keep(mr[i] + kk[u], pol);
+#pragma unroll
+      for (int i = 0; i < ND_RW; ++i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[i] += a[i][u] * tk[u];
+    }
+#pragma unroll
+    for (int i = 0; i < ND_RW; ++i) {
+      const int r = row0 + w + (ND_T / 32) * i;
+      const double vv = warp_sum(v[i]);
+      if (lane == 0 && r < rend) ug[it.offu + r] = t[nf + r] - vv;
+    }
+  }
+  if (!waited) pdl_wait();
+}
+
+__global__ void __launch_bounds__(ND_T) k_nd_bwd2(const NdItem* __restrict__ items, int nwork, const int* __restrict__ gF,
+                                                  const int* __restrict__ gU, const double* __restrict__ Xg,
+                                                  const double* __restrict__ MTg, const double* __restrict__ dsc,
+                                                  const double* Tg, double* z0, const PcgState* st, int mode, int keep) {
+  extern __shared__ double sh[];
+  pdl_launch();
+  const uint64_t pol = nd_policy(keep);
+  if (mode >= 1 && st->done) return;
+  bool waited = false;
+  for (int wk = blockIdx.x; wk < nwork; wk += gridDim.x) {
+    if (wk != (int)blockIdx.x) __syncthreads();
+    const NdItem it = items[wk];
+    const int nf = it.nf, nu = it.nu, nk = nf + nu;
+    constexpr int KPT = 4;
+    int gk[KPT];
+    for (int k0 = 0; k0 < nk; k0 += KPT * ND_T) {
+#pragma unroll
+      for (int u = 0; u < KPT; ++u) {
+        const int k = k0 + threadIdx.x + u * ND_T;
+        gk[u] = (k >= nf && k < nk) ? gU[it.gUofs + k - nf] : -1;
+      }
+      if (!waited) { pdl_wait(); waited = true; }
+#pragma unroll
+      for (int u = 0; u < KPT; ++u) {
+        const int k = k0 + threadIdx.x + u * ND_T;
+        if (k < nf) sh[k] = Tg[it.offT + k];
+        else if (k < nk) sh[k] = -z0[gk[u]] / dsc[gk[u]];  // scaled unknown of an ancestor front, negated
+      }
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* X = Xg + it.offX;
+    const double* MT = MTg + it.offM;
+    const int row0 = it.row0, rend = min(nf, row0 + ND_ROWS);
+    const double* xr[ND_RW];
+    const double* mr[ND_RW];
+    double v[ND_RW];
+#pragma unroll
+    for (int i = 0; i < ND_RW; ++i) {
+      const int j = row0 + w + (ND_T / 32) * i, jj = j < rend ? j : row0;
+      xr[i] = X + (size_t)jj * nf;
+      mr[i] = MT + (size_t)jj * nu - nf;
+      v[i] = 0.0;
+    }
+    for (int k0 = 0; k0 < nk; k0 += 128) {
+      double sk[4], a[ND_RW][4];
+      int kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + lane + 32 * u;
+        kk[u] = min(k, nk - 1);
+        sk[u] = k < nk ? sh[k] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < ND_RW; ++i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[i][u] = ld_keep((kk[u] < nf ? xr[i] : mr[i]) + kk[u], pol);
+#pragma unroll
+      for (int i = 0; i < ND_RW; ++i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[i] += a[i][u] * sk[u];
+    }
+#pragma unroll
+    for (int i = 0; i < ND_RW; ++i) {
+      const int j = row0 + w + (ND_T / 32) * i;
+      const double vv = warp_sum(v[i]);
+      if (lane == 0 && j < rend) {
+        const int g = gF[it.gofs + j];
+        z0[g] = vv * dsc[g];
+      }
+    }
+  }
+  if (!waited) pdl_wait();
+}
+
+// host tables of the v2 solve (after nd_setup_run's plan upload); 0 = built, 1 = not applicable
+static int nd_v2_build(dgas_ctx ctx) {
+  NdPlan& P = ctx->nd;
+  const int nq = ctx->nq;
+  std::vector<int> gF, gU, gofs(P.nf), gUofs(P.nf), sofs(P.nf);
+  std::vector<int2> tsrc;
+  for (int f = 0; f < P.nf; ++f) {
+    const int nf = P.h_nF[f], nu = P.h_nU[f];
+    gofs[f] = (int)gF.size();
+    for (int k = 0; k < nf; ++k) gF.push_back(P.h_Fe[P.h_offFe[f] + k / nq] * nq + k % nq);
+    gUofs[f] = (int)gU.size();
+    for (int k = 0; k < nu; ++k) gU.push_back(P.h_Ue[P.h_offUe[f] + k / nq] * nq + k % nq);
+    sofs[f] = (int)tsrc.size();
+    std::vector<int2> src(nf + nu, make_int2(-1, -1));
+    for (int ci = P.h_childptr[f]; ci < P.h_childptr[f + 1]; ++ci) {
+      const int c = P.h_childs[ci];
+      for (int a = 0; a < P.h_nU[c]; ++a) {
+        const int pos = P.h_cmap[P.h_cmap_ptr[ci] + a / nq] * nq + a % nq;
+        int2& sp = src[pos];
+        if (sp.x < 0) sp.x = P.h_offu[c] + a;
+        else if (sp.y < 0) sp.y = P.h_offu[c] + a;
+        else return 1;  // more than two contributions to one position: keep the v1 kernels
+      }
+    }
+    tsrc.insert(tsrc.end(), src.begin(), src.end());
+  }
+  auto item = [&](int f, int row0) {
+    NdItem it{};
+    it.f = f; it.row0 = row0; it.nf = P.h_nF[f]; it.nu = P.h_nU[f];
+    it.offT = P.h_offT[f]; it.offu = P.h_offu[f]; it.gofs = gofs[f]; it.sofs = sofs[f];
+    it.offM = P.h_offM[f]; it.offX = P.h_offX[f]; it.gUofs = gUofs[f];
+    return it;
+  };
+  std::vector<NdItem> wf, wb;
+  for (int L = 0; L < P.nlev; ++L)
+    for (int k = P.h_lev_ptr[L]; k < P.h_lev_ptr[L + 1]; ++k) {
+      const int f = P.h_lev_fronts[k];
+      for (int r = 0; r < std::max(1, P.h_nU[f]); r += ND_ROWS) wf.push_back(item(f, r));
+      for (int r = 0; r < P.h_nF[f]; r += ND_ROWS) wb.push_back(item(f, r));
+    }
+  int st;
+  if ((st = up(ctx, &P.d_gF, gF)) || (st = up(ctx, &P.d_gU, gU)) || (st = up(ctx, &P.d_tsrc, tsrc))) return -st;
+  NdItem *dwf = nullptr, *dwb = nullptr;
+  if ((st = up(ctx, &dwf, wf)) || (st = up(ctx, &dwb, wb))) return -st;
+  P.d_wf2 = dwf;
+  P.d_wb2 = dwb;
+  return 0;
+}
+
+template <typename K, typename... Args>
+static void nd_launch(bool pdl, K kern, int grid, size_t smem, cudaStream_t s, Args... args) {
+  if (!pdl) {
+    kern<<<grid, ND_T, smem, s>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ND_T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+static void nd_solve_once_v2(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s, const double* rin, double* zout) {
+  NdPlan& P = ctx->nd;
+  const size_t shf = (size_t)P.maxN * 8, shb = (size_t)(P.maxF + P.maxU) * 8;
+  const NdItem* wf = static_cast<const NdItem*>(P.d_wf2);
+  const NdItem* wb = static_cast<const NdItem*>(P.d_wb2);
+  bool first = true;  // the first level of a chain waits for the restriction (another stream): plain launch
+  for (int L = 0; L < P.nlev; ++L) {
+    const int n = P.h_wf_ptr[L + 1] - P.h_wf_ptr[L];
+    if (!n) continue;
+    nd_launch(P.pdl && !first, k_nd_fwd2, std::min(n, ctx->nd_grid), shf, s, wf + P.h_wf_ptr[L], n,
+              (const int*)P.d_gF, (const int2*)P.d_tsrc, (const double*)P.d_M, (const double*)P.d_dsc, rin, P.d_T,
+              P.d_u, st, mode, ctx->nd_l2);
+    first = false;
+  }
+  for (int L = P.nlev - 1; L >= 0; --L) {
+    const int n = P.h_wb_ptr[L + 1] - P.h_wb_ptr[L];
+    if (!n) continue;
+    nd_launch(P.pdl && !first, k_nd_bwd2, std::min(n, ctx->nd_grid), shb, s, wb + P.h_wb_ptr[L], n,
+              (const int*)P.d_gF, (const int*)P.d_gU, (const double*)P.d_X, (const double*)P.d_MT,
+              (const double*)P.d_dsc, (const double*)P.d_T, zout, st, mode, ctx->nd_l2);
+    first = false;
+  }
 }
 
 // res = b - A0 z  (coarse block rows, warp per coarse element; A0 blocks per coupled pair)
@@ -389,6 +716,7 @@ void nd_solve_launch(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s)
 
 static void nd_solve_once(dgas_ctx ctx, int mode, const PcgState* st, cudaStream_t s, const double* rin, double* zout) {
   NdPlan& P = ctx->nd;
+  if (P.v2) { nd_solve_once_v2(ctx, mode, st, s, rin, zout); return; }
   const size_t shf = (size_t)P.maxN * 8, shb = (size_t)(P.maxF + P.maxU) * 8;
   for (int L = 0; L < P.nlev; ++L) {
     const int n = P.h_wf_ptr[L + 1] - P.h_wf_ptr[L];
@@ -518,7 +846,7 @@ void nd_free(dgas_ctx ctx) {
   void* ptrs[] = {P.d_nF, P.d_nU, P.d_offX, P.d_offM, P.d_offUpd, P.d_offS, P.d_offT, P.d_offu, P.d_offFe, P.d_offUe,
                   P.d_Fe, P.d_Ue, P.d_childptr, P.d_childs, P.d_cmap_ptr, P.d_cmap, P.d_asm_ptr, P.d_asm,
                   P.d_lev_fronts, P.d_X, P.d_M, P.d_MT, P.d_T, P.d_u, P.d_wf, P.d_wb, P.d_prow, P.d_rb, P.d_zb,
-                  P.d_dsc};
+                  P.d_dsc, P.d_wf2, P.d_wb2, P.d_gF, P.d_gU, P.d_tsrc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }

@@ -14,8 +14,13 @@
 #include "internal.h"
 #include "tma.cuh"
 
+#include <algorithm>
+#include <map>
+
 #define SR_NW 8    // consumer warps per CTA
 #define SR_NB 32   // cells in flight per CTA (mbarrier pairs)
+#define CLS_MAXDEG 6  // k_spmv_cls: neighbours per cell incl. itself (Cartesian meshes: 5)
+#define CLS_DEPTH 4   // k_spmv_cls: gathers in flight per warp (cells ahead)
 
 template <int NP>
 struct SrCfg {
@@ -351,6 +356,189 @@ __global__ void __launch_bounds__(SR_NW * 32) k_spmv_dd(
   }
 }
 
+// p.q of the PCG SpMV: per-CTA partial, the last CTA to arrive sums the partials in CTA order
+// (deterministic) and sets alpha = gamma / p.q (breakdown if p.q <= 0); same protocol as above
+template <int NTT>
+__device__ __forceinline__ void spmv_pq_epilogue(double mydot, double* wdot, double* red, PcgState* st, double* partials,
+                                                 double* alpha_hist, int it) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  mydot = warp_sum(mydot);
+  if (lane == 0) wdot[w] = mydot;
+  __syncthreads();
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    double t0 = 0;
+    for (int k = 0; k < NTT / 32; ++k) t0 += wdot[k];
+    partials[blockIdx.x] = t0;
+    __threadfence();
+    am_last = atomicAdd(&st->cnt[0], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double sacc = 0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += NTT) sacc += __ldcg(partials + k);
+  sacc = warp_sum(sacc);
+  if (lane == 0) red[w] = sacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double pq = 0;
+    for (int k = 0; k < NTT / 32; ++k) pq += red[k];
+    st->cnt[0] = 0;
+    st->pq = pq;
+    if (!(pq > 0) || !isfinite(pq)) { st->done = 1; st->status = DGAS_E_BREAKDOWN; }
+    else { st->alpha = st->gamma / pq; alpha_hist[it] = st->alpha; }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_spmv_cls — q = A p (+ the same PCG fusion) over de-duplicated A, cells grouped by their distinct
+// row-block ("class"; config 3: 262,144 cells, 1,225 classes). A work item is a run of cells of one
+// class; its warp loads the class row-block ONCE into registers (lane (a, h) holds A[a][h + LPR t])
+// and then only gathers neighbour values per cell (one cell ahead) and multiplies: no per-cell
+// re-read of the 4-8 KB row-block through L1/L2 (k_spmv_dd: ~200 instructions and ~5 us of latency
+// per cell on config 3). Same product order as k_spmv_dd within a slice h (t ascending), slices
+// summed by shuffles in h order. Items are dealt round-robin to the grid's warps.
+template <int NP>
+struct ClsCfg {
+  static constexpr int LPR = 32 / NP > 0 ? 32 / NP : 1;
+  static constexpr int LANES = NP * LPR;
+  static constexpr int MAXC = (CLS_MAXDEG * NP + LPR - 1) / LPR;  // register columns per lane
+  static constexpr int E = (CLS_MAXDEG * NP + 31) / 32;           // gathered entries per lane
+  static constexpr int XS = (32 * E > LPR * MAXC ? 32 * E : LPR * MAXC);
+};
+
+template <int NP>
+__global__ void __launch_bounds__(SR_NW * 32) k_spmv_cls(
+    int mode, int nitems, const int4* __restrict__ items, const int64_t* __restrict__ cls_off,
+    const int* __restrict__ cells, const int* __restrict__ cls_nb, const double* __restrict__ A, const double* x,
+    double* y, const double* z, double* const* pbuf, PcgState* st, double* partials, double* alpha_hist) {
+  using C = ClsCfg<NP>;
+  constexpr int LPR = C::LPR, E = C::E, XS = C::XS, MAXC = C::MAXC;
+  constexpr int NTT = SR_NW * 32;
+  __shared__ double red[NTT / 32];
+  __shared__ double wdot[NTT / 32];
+  __shared__ double xs_all[SR_NW * XS];
+  int it = 0;
+  double beta = 0;
+  const double* pold = nullptr;
+  double* pnew = nullptr;
+  const bool pcg = mode == 1 || mode == 3;
+  if (pcg) {
+    if (st->done) return;
+    it = st->it;
+    beta = it > 0 ? st->beta : 0.0;
+    pold = pbuf[it & 1];
+    pnew = pbuf[(it + 1) & 1];
+    if (mode == 3) x = pnew;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* xs = xs_all + w * XS;
+  for (int t = lane; t < XS; t += 32) xs[t] = 0.0;
+  auto colval = [&](int64_t id) -> double {
+    return mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
+  };
+  const int a = lane % NP, h = lane / NP;
+  const bool rl = h < LPR && lane < C::LANES;
+  double mydot = 0;
+  const int gw = blockIdx.x * SR_NW + w, nw = gridDim.x * SR_NW;
+  constexpr int D = CLS_DEPTH;
+  for (int wi = gw; wi < nitems; wi += nw) {
+    const int4 itm = items[wi];  // (class, first cell in `cells`, count, W = deg NP)
+    const int W = itm.w, n = itm.z;
+    const int* cl = cells + itm.y;
+    const int* cnb = cls_nb + (size_t)itm.y * CLS_MAXDEG;  // neighbour cells of each cell, nbr order
+    double Ar[MAXC];
+    {
+      const double* Ab = A + cls_off[itm.x] + a;
+#pragma unroll
+      for (int t = 0; t < MAXC; ++t) {
+        const int col = h + LPR * t;
+        Ar[t] = (rl && col < W) ? __ldg(Ab + col * NP) : 0.0;
+      }
+    }
+    // software pipeline over the item's cells (slot d = i mod D): neighbour ids 2D cells ahead, gathered
+    // values D cells ahead; lane j < deg holds neighbour j's id, the gather lanes take it by shuffle
+    const int deg = W / NP;
+    auto ids = [&](int i) -> int { return (i < n && lane < deg) ? __ldg(cnb + (size_t)i * CLS_MAXDEG + lane) : 0; };
+    auto cid = [&](int i) -> int { return i < n ? __ldg(cl + i) : 0; };
+    auto gather = [&](int idr, bool on, double* v) {
+#pragma unroll
+      for (int t = 0; t < E; ++t) {
+        const int e = lane + 32 * t;
+        const int nb = __shfl_sync(0xffffffffu, idr, (e / NP) & 31);
+        v[t] = (on && e < W) ? colval((int64_t)nb * NP + e % NP) : 0.0;
+      }
+    };
+    double v[D][E];
+    int idr[D], cA[D], cB[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      cA[d] = cid(d);
+      gather(ids(d), d < n, v[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      idr[d] = ids(d + D);
+      cB[d] = cid(d + D);
+    }
+    for (int i0 = 0; i0 < n; i0 += D) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int i = i0 + d;
+        if (i < n) {  // warp-uniform
+          const int c = cA[d];
+          __syncwarp();
+#pragma unroll
+          for (int t = 0; t < E; ++t) xs[lane + 32 * t] = v[d][t];
+          __syncwarp();
+          gather(idr[d], i + D < n, v[d]);  // cell i + D
+          cA[d] = cB[d];
+          idr[d] = ids(i + 2 * D);
+          cB[d] = cid(i + 2 * D);
+          double pn = 0;
+          if (pcg && h == 0 && lane < NP) {
+            const size_t id = (size_t)c * NP + a;
+            pn = mode == 3 ? x[id] : it > 0 ? z[id] + beta * pold[id] : z[id];
+          }
+          double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+          for (int t = 0; t + 3 < MAXC; t += 4) {
+            s0 += Ar[t] * xs[h + LPR * t];
+            s1 += Ar[t + 1] * xs[h + LPR * (t + 1)];
+            s2 += Ar[t + 2] * xs[h + LPR * (t + 2)];
+            s3 += Ar[t + 3] * xs[h + LPR * (t + 3)];
+          }
+#pragma unroll
+          for (int t = MAXC / 4 * 4; t < MAXC; ++t) s0 += Ar[t] * xs[h + LPR * t];
+          const double vv = (s0 + s1) + (s2 + s3);
+          double tot = vv;
+#pragma unroll
+          for (int h2 = 1; h2 < LPR; ++h2) tot += __shfl_sync(0xffffffffu, vv, (a + NP * h2) & 31);
+          if (h == 0 && lane < NP) {
+            const size_t id = (size_t)c * NP + a;
+            y[id] = tot;
+            if (pcg) {
+              if (mode == 1) pnew[id] = pn;
+              mydot += pn * tot;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (!pcg) return;
+  spmv_pq_epilogue<NTT>(mydot, wdot, red, st, partials, alpha_hist, it);
+}
+
+#define DISPATCH_P15S(P, ...)                               \
+  switch (P) {                                              \
+    case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
+    case 2: { constexpr int NP_ = 6; __VA_ARGS__; } break;  \
+    case 3: { constexpr int NP_ = 10; __VA_ARGS__; } break; \
+    case 4: { constexpr int NP_ = 15; __VA_ARGS__; } break; \
+  }
+
 #define DISPATCH_PSR(P, ...)                                \
   switch (P) {                                              \
     case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
@@ -432,6 +620,12 @@ void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgSta
     k_pupdate<<<nsm * 8, 256, 0, s>>>(ctx->N, ctx->d_z, ctx->d_pbuf, st);
     mode = 3;
   }
+  if (ctx->d_cls_items) {
+    DISPATCH_P15S(ctx->p, (k_spmv_cls<NP_><<<ctx->cls_grid, SR_NW * 32, 0, s>>>(
+                              mode, ctx->cls_nitems, ctx->d_cls_items, ctx->d_cls_off, ctx->d_cls_cells, ctx->d_cls_nb,
+                              ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha)));
+    return;
+  }
   if (ctx->d_a_dd) {
     const int grid = ctx->dd_grid, chunk = (ctx->nc + grid - 1) / grid;
     DISPATCH_PSR(ctx->p, (k_spmv_dd<NP_><<<grid, SR_NW * 32, 0, s>>>(mode, ctx->nc, chunk, ctx->d_nbr_ptr, ctx->d_nbr,
@@ -465,4 +659,59 @@ void launch_spmv_range(dgas_ctx ctx, int cb, int ce, const double* x, double* y,
                            0, n, chunk, ctx->d_nbr_ptr + cb, ctx->d_nbr, ctx->d_a_off + cb, ctx->d_A, x,
                            y + (size_t)cb * NP_, ctx->d_z, ctx->d_pbuf, nullptr, ctx->d_partials, ctx->d_alpha,
                            ctx->sr_ring_bytes, ctx->sr_G, ctx->d_a_dd ? ctx->d_a_dd + cb : nullptr)));
+}
+
+// Host: class-sorted work items for k_spmv_cls (dd[c] = compact offset of cell c's row-block). Cells of a
+// class in ascending order, cut into runs of about nc / (2 x grid warps) cells. Off for p > 4 (register
+// row-blocks) or cells with more than CLS_MAXDEG neighbours; DGAS_SPMV_CLS=0 disables it.
+int spmv_cls_setup(dgas_ctx ctx, const std::vector<int64_t>& dd) {
+  int on = 1;
+  if (const char* e = std::getenv("DGAS_SPMV_CLS")) on = std::atoi(e) != 0;
+  if (!on || ctx->p < 1 || ctx->p > 4 || ctx->max_deg > CLS_MAXDEG) return 0;
+  const int nc = ctx->nc;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int cps = 1;  // resident CTAs per SM (register-bound: the row-block lives in registers)
+  DISPATCH_P15S(ctx->p, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_spmv_cls<NP_>, SR_NW * 32, 0)));
+  cps = std::max(1, cps);
+  if (const char* e = std::getenv("DGAS_CLS_CPS")) cps = std::max(1, std::atoi(e));
+  const int grid = std::min(cps * nsm, std::max(1, nc / SR_NW));
+  std::map<int64_t, std::vector<int>> cls;
+  for (int c = 0; c < nc; ++c) cls[dd[c]].push_back(c);
+  int run = std::max(4, (int)(nc / (2LL * grid * SR_NW)));
+  if (const char* e = std::getenv("DGAS_CLS_RUN")) run = std::max(1, std::atoi(e));
+  std::vector<int4> items;
+  std::vector<int64_t> off;
+  std::vector<int> cells;
+  cells.reserve(nc);
+  for (auto& kv : cls) {
+    const int ci = (int)off.size();
+    off.push_back(kv.first);
+    const int c0 = kv.second[0];
+    const int W = (ctx->nbr_ptr_h[c0 + 1] - ctx->nbr_ptr_h[c0]) * ctx->np;
+    const int n = (int)kv.second.size(), nrun = (n + run - 1) / run;
+    for (int t = 0; t < nrun; ++t) {
+      const int b0 = (int)((int64_t)n * t / nrun), b1 = (int)((int64_t)n * (t + 1) / nrun);
+      items.push_back(make_int4(ci, (int)cells.size() + b0, b1 - b0, W));
+    }
+    cells.insert(cells.end(), kv.second.begin(), kv.second.end());
+  }
+  // longest runs first so the round-robin deal ends evenly
+  std::stable_sort(items.begin(), items.end(), [](const int4& u, const int4& v) { return u.z > v.z; });
+  std::vector<int> nb((size_t)nc * CLS_MAXDEG);
+  for (int i = 0; i < nc; ++i) {
+    const int c = cells[i], lo = ctx->nbr_ptr_h[c], d = ctx->nbr_ptr_h[c + 1] - lo;
+    for (int j = 0; j < CLS_MAXDEG; ++j) nb[(size_t)i * CLS_MAXDEG + j] = j < d ? ctx->nbr_h[lo + j] : c;
+  }
+  int st;
+  if ((st = dev_upload(ctx, &ctx->d_cls_items, items)) || (st = dev_upload(ctx, &ctx->d_cls_off, off)) ||
+      (st = dev_upload(ctx, &ctx->d_cls_cells, cells)) || (st = dev_upload(ctx, &ctx->d_cls_nb, nb)))
+    return st;
+  ctx->cls_nitems = (int)items.size();
+  ctx->cls_grid = grid;
+  if (std::getenv("DGAS_VERBOSE"))
+    fprintf(stderr, "dgas: class SpMV: %zu row-block classes, %d items (runs <= %d cells), %d CTAs\n", cls.size(),
+            ctx->cls_nitems, run, grid);
+  return 0;
 }

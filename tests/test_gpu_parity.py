@@ -34,6 +34,15 @@ CASES = {
     "cfg2": lambda: g.config(2),
     "cfg2s": lambda: g.config(2, scale="small"),
     "cfg3s": lambda: g.config(3, scale="small"),
+    # config-3-style Cartesian meshes with many subdomains sharing a factor (multi-RHS local solve)
+    "cart128_p3": lambda: g.generate(0, 128, sub_mode=0, sub_tile=8, coarse_mode=2, coarse_tile=4, name="cart128_p3",
+                                     p=3, q=1, f_kind=g.F_SINSIN),
+    "cart64_p1": lambda: g.generate(0, 64, sub_mode=0, sub_tile=8, coarse_mode=2, coarse_tile=4, name="cart64_p1",
+                                    p=1, q=1, f_kind=g.F_SINSIN),
+    "cart64_p2": lambda: g.generate(0, 64, sub_mode=0, sub_tile=8, coarse_mode=2, coarse_tile=4, name="cart64_p2",
+                                    p=2, q=2, f_kind=g.F_SINSIN),
+    "cart64_p4": lambda: g.generate(0, 64, sub_mode=0, sub_tile=8, coarse_mode=2, coarse_tile=4, name="cart64_p4",
+                                    p=4, q=1, f_kind=g.F_SINSIN),
     "cfg4s": lambda: g.config(4, scale="small"),
     "cfg5s_p1q1": lambda: g.config(5, 1, 1, scale="small"),
     "cfg5s_p3q1": lambda: g.config(5, 3, 1, scale="small"),
@@ -422,6 +431,15 @@ def test_eager_path_matches_graph(monkeypatch, name):
     ("cfg3s", {"DGAS_PANEL_KEEP": "0", "DGAS_LOCAL_CPS": "3"}, 2),
     ("cfg5s_p6q1", {}, 1),  # n_p = 28: envelope kernel (faster there)
     ("cfg5s_p4q4", {"DGAS_LOCAL_CPS": "7"}, 2),  # 128-thread CTAs on a small problem
+    # multi-RHS solve over subdomains sharing a de-duplicated factor (local_mrhs.cu): default geometry,
+    # batches of 1 (chain per subdomain), 2-slot ring, B > 16 (one b per lane), every n_p
+    ("cart128_p3", {}, 5),
+    ("cart128_p3", {"DGAS_MR_B": "1", "DGAS_MR_S": "2"}, 5),
+    ("cart128_p3", {"DGAS_MR_B": "24"}, 5),
+    ("cart128_p3", {"DGAS_MR_B": "3"}, 5),
+    ("cart64_p1", {"DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p2", {"DGAS_MR_MINAVG": "1", "DGAS_MR_B": "17", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p4", {"DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
 ])
 def test_local_kernel_variants(monkeypatch, name, env, kernel):
     """Both local-solve kernels (envelope k_local, panel k_local_panel) and the panel kernel's ring
@@ -553,6 +571,7 @@ def test_dedup_is_bitwise_identical(monkeypatch):
     for bit, with and without de-duplication."""
     P = CASES["cfg3s"]()
     out = []
+    monkeypatch.setenv("DGAS_MRHS", "0")  # same local kernel (warp per subdomain) in both runs
     for dd in ("0", "1"):
         monkeypatch.setenv("DGAS_DEDUP", dd)
         monkeypatch.setenv("DGAS_DD_CPS", "2")
