@@ -121,7 +121,7 @@ struct dgas_ctx_s {
   int64_t* d_cls_off = nullptr;        // compact-store offset per row-block class
   int* d_cls_cells = nullptr;          // cells grouped by class
   int* d_cls_nb = nullptr;             // [nc][CLS_MAXDEG] neighbour cells of d_cls_cells[i]
-  int cls_nitems = 0, cls_grid = 0;
+  int cls_nitems = 0, cls_grid = 0, cls_minb = 1;
   std::vector<int64_t> a_dd_h;
   int64_t a_unique = 0, a_bytes_stored = 0;  // distinct row-blocks, bytes of the compact A
   int p_unique = 0;                   // distinct subdomain factors (panel store)
@@ -129,6 +129,7 @@ struct dgas_ctx_s {
   int4* d_mr_batches = nullptr;       // (representative subdomain, first member, count, 0) per batch
   int* d_mr_members = nullptr;        // member subdomains, grouped by batch
   int mr_nbatch = 0, mr_B = 0, mr_BS = 1, mr_S = 4, mr_WC = 1, mr_grid = 0, mr_classes = 0;
+  int mr_kernel = 1, mr_G = 8, mr_NW = 4;  // 2: k_local_mrhs_w (warp chains: NW warps x G columns)
   uint32_t mr_slot = 0;
   size_t mr_smem = 0;
   int64_t p_bytes_stored = 0;

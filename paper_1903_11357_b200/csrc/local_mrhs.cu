@@ -275,12 +275,322 @@ __global__ void __launch_bounds__(MR_T) k_local_mrhs(int mode, int nbatch, const
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// k_local_mrhs_w — the same multi-RHS solve with INDEPENDENT WARP CHAINS (default). ncu on k_local_mrhs
+// (config 3): ~2.4 us per chain step; stalls: shared-memory scoreboard 25%, CTA barrier 20%, fixed-latency
+// waits 24%; every step pays two CTA barriers and a cross-warp reduction through shared memory. Here the
+// right-hand sides of a batch are dealt to the warps, G per warp, and a warp never synchronises with the
+// others: lane (g, ks) works on RHS column g and the panel columns q = ks (mod KS), KS = 32 / G.
+//   forward  : acc[0..NP) over the lane's columns, summed over ks by KS-1 xor-shuffles per row
+//   backward : u_k in registers, each lane owns its (q, g) entries (no reduction at all)
+// The panels of the class are streamed once per CTA by a producer warp into the S-slot ring (full / empty
+// mbarriers; empty counts one arrival per active consumer warp), so the warps drift apart by up to S steps.
+// Each warp keeps its own window W_w (WC cells x NP rows x G columns) and its own cp.async prefetch of
+// r (forward) / y (backward, from the temporaries in z); only __syncwarp on the chain.
+// Lanes whose column is beyond the batch (g >= its count) mirror the last valid column: they compute and
+// store the same values to the same addresses (benign), so the chain has no predication.
+template <int NP, int G>
+struct MrwCfg {
+  static constexpr int KS = 32 / G;
+  static constexpr int BS = G | 1;  // odd row stride of the window
+};
+
+struct MrwLayout {
+  size_t off_fk, off_fm, off_slt, off_po, off_W, off_ring, total;
+  __host__ __device__ MrwLayout(int mc, int np, int nw, int bs, int wc, int S, uint32_t slot) {
+    off_fk = 256;  // full[16] | empty[16]
+    off_fm = off_fk + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_slt = off_fm + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_po = off_slt + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_W = off_po + (size_t)mc * 8;
+    off_ring = (off_W + (size_t)nw * wc * np * bs * 8 + 127) & ~(size_t)127;
+    total = off_ring + (size_t)S * slot;
+  }
+};
+
+template <int NP, int G>
+__global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, const int4* __restrict__ batches,
+                                                         const int* __restrict__ members,
+                                                         const int* __restrict__ sub_ptr, const int* __restrict__ first,
+                                                         const int64_t* __restrict__ p_off, const double* __restrict__ P,
+                                                         const double* r_in, double* const* rbuf, double* z,
+                                                         const PcgState* st, int NW, int S, uint32_t slot_bytes, int WC,
+                                                         int max_cells) {
+  constexpr int DPK = mr_dpk<NP>(), KS = MrwCfg<NP, G>::KS, BS = MrwCfg<NP, G>::BS, PD = MR_PD;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const double* r = r_in;
+  if (mode >= 1) {
+    if (st->done) return;
+    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+  }
+  const MrwLayout L(max_cells, NP, NW, BS, WC, S, slot_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + 16;
+  int* fk = reinterpret_cast<int*>(sm + L.off_fk);
+  int* fm = reinterpret_cast<int*>(sm + L.off_fm);
+  int* slt = reinterpret_cast<int*>(sm + L.off_slt);
+  int64_t* po = reinterpret_cast<int64_t*>(sm + L.off_po);
+  unsigned char* ring = sm + L.off_ring;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int4 bt = batches[blockIdx.x];
+  const int rep = bt.x, moff = bt.y, B = bt.z;
+  const int s0 = sub_ptr[rep], m = sub_ptr[rep + 1] - s0, T2 = 2 * m;
+  const int nwact = (B + G - 1) / G;  // consumer warps with at least one right-hand side
+  for (int k = tid; k < m; k += blockDim.x) {
+    fk[k] = first[s0 + k];
+    po[k] = p_off[s0 + k];
+    slt[k] = k % WC;
+  }
+  if (tid == 0) {
+    for (int t = 0; t < S; ++t) { mbar_init(&full[t], 1); mbar_init(&empty[t], nwact); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {  // fm_k = min_{j >= k} f_j (the backward window's low end, monotone)
+    int mn = 1 << 30;
+    for (int k = m - 1; k >= 0; --k) { mn = min(mn, fk[k]); fm[k] = mn; }
+  }
+  __syncthreads();
+  const int SM1 = S - 1;
+  if (w == NW) {
+    // ---------------- producer warp: step t = forward cell t (t < m), backward cell 2m-1-t
+    if (lane != 0) return;
+    const uint64_t pol = l2_evict_last();  // every batch of the class re-reads its factor: keep it in L2
+    for (int t = 0; t < T2; ++t) {
+      const int sl = t & SM1;
+      if (t >= S) mbar_wait(&empty[sl], (uint32_t)(((t / S) - 1) & 1));
+      const int k = t < m ? t : T2 - 1 - t;
+      const int n = DPK + (k - fk[k]) * NP * NP;
+      bulk_load(ring + (size_t)sl * slot_bytes, P + po[k], (uint32_t)(((n + 1) & ~1) * 8), &full[sl], pol);
+    }
+    return;
+  }
+  if (w >= nwact) return;
+  // ---------------- consumer warp w: columns w G .. w G + G - 1 of the batch
+  const int g = lane % G, ks = lane / G;
+  const int cnt = min(G, B - w * G);           // valid columns of this warp (>= 1)
+  const int ge = min(g, cnt - 1);              // mirrored column
+  const int64_t mbase = (int64_t)sub_ptr[members[moff + w * G + ge]] * NP;
+  double* Ww = reinterpret_cast<double*>(sm + L.off_W) + (size_t)w * WC * NP * BS;
+  const int WR = WC * NP;
+  // cp.async of NP rows x G columns of cell c (src: r, or the y temporaries in z) into its window slot
+  auto fetch = [&](const double* src, int c) {
+    double* dst = Ww + (size_t)slt[c] * NP * BS;
+#pragma unroll
+    for (int e0 = 0; e0 < NP * G; e0 += 32) {
+      const int e = e0 + lane;
+      const int gb = e / NP, i = e - gb * NP;
+      const int64_t mbb = __shfl_sync(0xffffffffu, mbase, gb & 31);  // lane gb (ks = 0) holds column gb's base
+      if (e < NP * G) cp_async8(dst + (size_t)i * BS + gb, src + mbb + (int64_t)c * NP + i);
+    }
+  };
+  for (int c = 0; c < PD; ++c) {
+    if (c < m) fetch(r, c);
+    cp_async_commit();
+  }
+  cp_async_wait<PD - 1>();
+  __syncwarp();
+  // ------------------------------------------------ forward sweep
+  // U columns of the panel per loop trip, all their loads issued before the first product (the chain is
+  // latency-bound: ncu 0.37 issue slots per cycle, stalls on fixed latencies and shared-memory loads); a
+  // column beyond the panel is clamped to column 0 with a zero multiplier, so there is no remainder loop
+  constexpr int U = NP <= 10 ? 4 : 2;
+  constexpr int NPAD = (NP + KS - 1) / KS * KS, RPL = NPAD / KS;  // rows per lane after the reduce-scatter
+  for (int k = 0; k < m; ++k) {
+    const int sl = k & SM1;
+    mbar_wait(&full[sl], (uint32_t)((k / S) & 1));
+    const double* __restrict__ Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+    const int f = fk[k], KU = (k - f) * NP, rk = slt[k] * NP, rf = slt[f] * NP;
+    double acc[NPAD];
+#pragma unroll
+    for (int i = 0; i < NPAD; ++i) acc[i] = 0.0;
+    for (int q = ks; q < NP; q += KS) {  // D column q (rows q..NP-1) times r_k[q]
+      const double rv = Ww[(size_t)(rk + q) * BS + g];
+      const double* col = Ps + mr_dcol(NP, q) - q;
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+        if (i >= q) acc[i] += col[i] * rv;
+    }
+    for (int j0 = ks; j0 < KU; j0 += KS * U) {  // -U column j times y_old[j] (window rows wrap at WR)
+      double yv[U];
+      const double* col[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int jj = j0 + u * KS;
+        const bool ok = jj < KU;
+        const int j = ok ? jj : 0;
+        int row = rf + j;
+        row -= row >= WR ? WR : 0;
+        const double wv = Ww[(size_t)row * BS + g];
+        yv[u] = ok ? wv : 0.0;
+        col[u] = Ps + DPK + j * NP;
+      }
+      if constexpr (NP % 2 == 0) {
+        double2 pv[U][NP / 2];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < NP / 2; ++i) pv[u][i] = reinterpret_cast<const double2*>(col[u])[i];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < NP / 2; ++i) {
+            acc[2 * i] += pv[u][i].x * yv[u];
+            acc[2 * i + 1] += pv[u][i].y * yv[u];
+          }
+      } else {
+        double pv[U][NP];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) pv[u][i] = col[u][i];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) acc[i] += pv[u][i] * yv[u];
+      }
+    }
+    // reduce-scatter over the KS slices: at each level a lane keeps one half of its rows and adds the
+    // partner's sums of that half; lane ks ends with the rows RPL ks .. RPL ks + RPL - 1 (fixed order)
+    {
+      int n = NPAD;
+#pragma unroll
+      for (int o = 16; o >= G; o >>= 1) {
+        const int h = n / 2;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < NPAD / 2; ++i)
+          if (i < h) {
+            const double snd = up ? acc[i] : acc[h + i];
+            const double kep = up ? acc[h + i] : acc[i];
+            acc[i] = kep + __shfl_xor_sync(0xffffffffu, snd, o);
+          }
+        n = h;
+      }
+    }
+    __syncwarp();  // every lane is done with the ring slot and with the window rows it read
+    if (lane == 0) mbar_arrive(&empty[sl]);
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int row = ks * RPL + i;
+      if (row < NP) {
+        Ww[(size_t)(rk + row) * BS + g] = acc[i];
+        z[mbase + (int64_t)k * NP + row] = acc[i];  // y_k, read back by the backward sweep
+      }
+    }
+    if (k + PD < m) fetch(r, k + PD);  // slot of cell k + PD - WC < f_k: free
+    cp_async_commit();
+    cp_async_wait<PD - 1>();  // r_{k+1} landed (this lane's copies)
+    __syncwarp();             // ... and everybody's, and y_k is visible
+  }
+  // ------------------------------------------------ backward sweep
+  // the window holds y of cells max(0, m - WC) .. m-1; cells below are fetched PD steps ahead
+  int lo = max(0, m - WC);
+  for (int kk = m - 1; kk >= max(0, m - PD); --kk) {
+    if (fm[kk] < lo) {
+      for (int c = fm[kk]; c < lo; ++c) fetch(z, c);
+      lo = fm[kk];
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<PD - 1>();
+  __syncwarp();
+  for (int k = m - 1; k >= 0; --k) {
+    const int t = T2 - 1 - k, sl = t & SM1;
+    mbar_wait(&full[sl], (uint32_t)((t / S) & 1));
+    const double* __restrict__ Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+    const int f = fk[k], KU = (k - f) * NP, rk = slt[k] * NP, rf = slt[f] * NP;
+    double uk[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) uk[i] = Ww[(size_t)(rk + i) * BS + g];
+    for (int q = ks; q < NP; q += KS) {  // z_k[q] = (D_k^T u_k)[q]
+      const double* col = Ps + mr_dcol(NP, q) - q;
+      double v = 0;
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+        if (i >= q) v += col[i] * uk[i];
+      z[mbase + (int64_t)k * NP + q] = v;
+    }
+    for (int j0 = ks; j0 < KU; j0 += KS * U) {  // y_old[j] += (-U_k^T u_k)[j]: U independent columns per trip
+      double* wp[U];
+      double wv[U], v0[U], v1[U];
+      const double* col[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int jj = j0 + u * KS;
+        ok[u] = jj < KU;
+        const int j = ok[u] ? jj : 0;
+        int row = rf + j;
+        row -= row >= WR ? WR : 0;
+        wp[u] = Ww + (size_t)row * BS + g;
+        wv[u] = *wp[u];
+        col[u] = Ps + DPK + j * NP;
+        v0[u] = 0;
+        v1[u] = 0;
+      }
+      if constexpr (NP % 2 == 0) {
+        double2 pv[U][NP / 2];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < NP / 2; ++i) pv[u][i] = reinterpret_cast<const double2*>(col[u])[i];
+#pragma unroll
+        for (int i = 0; i < NP / 2; ++i)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            v0[u] += pv[u][i].x * uk[2 * i];
+            v1[u] += pv[u][i].y * uk[2 * i + 1];
+          }
+      } else {
+        double pv[U][NP];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) pv[u][i] = col[u][i];
+#pragma unroll
+        for (int i = 0; i + 1 < NP; i += 2)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            v0[u] += pv[u][i] * uk[i];
+            v1[u] += pv[u][i + 1] * uk[i + 1];
+          }
+#pragma unroll
+        for (int u = 0; u < U; ++u) v0[u] += pv[u][NP - 1] * uk[NP - 1];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) *wp[u] = wv[u] + (v0[u] + v1[u]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sl]);
+    // y rows of the cells the step k - PD needs (slots of cells > k, done)
+    const int k2 = k - PD;
+    if (k2 >= 0 && fm[k2] < lo) {
+      for (int c = fm[k2]; c < lo; ++c) fetch(z, c);
+      lo = fm[k2];
+    }
+    cp_async_commit();
+    cp_async_wait<PD - 1>();
+    __syncwarp();
+  }
+}
+
 #define DISPATCH_MR(P, ...)                                 \
   switch (P) {                                              \
     case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
     case 2: { constexpr int NP_ = 6; __VA_ARGS__; } break;  \
     case 3: { constexpr int NP_ = 10; __VA_ARGS__; } break; \
     case 4: { constexpr int NP_ = 15; __VA_ARGS__; } break; \
+  }
+
+#define DISPATCH_MRG(G, ...)                          \
+  switch (G) {                                        \
+    case 2: { constexpr int G_ = 2; __VA_ARGS__; } break;   \
+    case 4: { constexpr int G_ = 4; __VA_ARGS__; } break;   \
+    case 8: { constexpr int G_ = 8; __VA_ARGS__; } break;   \
+    case 16: { constexpr int G_ = 16; __VA_ARGS__; } break; \
+    case 32: { constexpr int G_ = 32; __VA_ARGS__; } break; \
   }
 
 // Host: classes of subdomains sharing a factor (rep_of from dedup.cu), batch size and geometry.
@@ -330,6 +640,69 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
   // room for one coarse-solve CTA per SM beside the local solves (the coarse chain runs concurrently)
   size_t reserve = 8 * 1024;
   if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;
+  int kern = 2;  // 2: independent warp chains (k_local_mrhs_w), 1: CTA-wide steps (k_local_mrhs)
+  if (const char* e = std::getenv("DGAS_MR_KERNEL")) kern = std::atoi(e) == 1 ? 1 : 2;
+  if (kern == 2) {
+    // config 3 sweep (PCG it/s): 8 warps x 2 columns 2028, 4 x 4 1751, 4 x 8 1758, 8 x 4 1756, 4 x 2 1750
+    int G = 2, NW = 8;
+    if (!std::getenv("DGAS_MR_S")) S = 8;
+    if (const char* e = std::getenv("DGAS_MR_G")) G = std::atoi(e);
+    if (const char* e = std::getenv("DGAS_MR_NW")) NW = std::max(1, std::min(8, std::atoi(e)));
+    if (G != 2 && G != 4 && G != 8 && G != 16 && G != 32) G = 2;
+    if (S > 16) S = 16;
+    const int B = G * NW, BSw = G | 1;
+    const size_t need = MrwLayout(mc, np, NW, BSw, WC, S, slot).total;
+    if (need > (size_t)optin) kern = 1;
+    else {
+      std::vector<int4> bat;
+      std::vector<int> mem;
+      for (auto& kv : cls) {
+        const int n = (int)kv.second.size(), nbat = (n + B - 1) / B;
+        int off = 0;
+        for (int t = 0; t < nbat; ++t) {
+          const int cnt = n / nbat + (t < n % nbat ? 1 : 0);
+          bat.push_back(make_int4(kv.first, (int)mem.size(), cnt, 0));
+          for (int u = 0; u < cnt; ++u) mem.push_back(kv.second[off + u]);
+          off += cnt;
+        }
+      }
+      std::stable_sort(bat.begin(), bat.end(), [](const int4& a, const int4& b2) { return a.z > b2.z; });
+      int st;
+      if ((st = dev_upload(ctx, &ctx->d_mr_batches, bat)) || (st = dev_upload(ctx, &ctx->d_mr_members, mem))) return st;
+      ctx->mr_nbatch = (int)bat.size();
+      ctx->mr_B = B;
+      ctx->mr_BS = BSw;
+      ctx->mr_S = S;
+      ctx->mr_slot = slot;
+      ctx->mr_WC = WC;
+      ctx->mr_G = G;
+      ctx->mr_NW = NW;
+      ctx->mr_smem = need;
+      ctx->mr_grid = ctx->mr_nbatch;
+      ctx->mr_classes = (int)cls.size();
+      cudaError_t e = cudaSuccess;
+      DISPATCH_MR(ctx->p, DISPATCH_MRG(G, ({
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, k_local_mrhs_w<NP_, G_>);
+        if (e == cudaSuccess && (size_t)optin < ctx->mr_smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(k_local_mrhs_w<NP_, G_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   optin - (int)fa.sharedSizeBytes);
+      })));
+      if (e != cudaSuccess) { ctx->detail = std::string("mrhs local smem: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
+      if (std::getenv("DGAS_VERBOSE")) {
+        size_t big = 0;
+        for (auto& kv : cls) big = std::max(big, kv.second.size());
+        fprintf(stderr, "dgas: multi-RHS local solve (warp chains): %d classes (largest %zu), %d batches of <= %d "
+                "(%d warps x %d columns, %d K-slices), window %d cells, ring %d x %u B, smem/CTA %zu\n", ctx->mr_classes,
+                big, ctx->mr_nbatch, B, NW, G, 32 / G, WC, S, slot, ctx->mr_smem);
+      }
+      ctx->mr_kernel = 2;
+      ctx->local_kernel = 5;
+      return 0;
+    }
+  }
+  ctx->mr_kernel = 1;
   int bforce = 0;
   if (const char* e = std::getenv("DGAS_MR_B")) bforce = std::max(1, std::min(32, std::atoi(e)));
   // fewest waves, then fewest batches (a step's instruction count per warp hardly depends on B <= 32)
@@ -395,6 +768,13 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
 }
 
 void launch_local_mrhs(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s) {
+  if (ctx->mr_kernel == 2) {
+    DISPATCH_MR(ctx->p, DISPATCH_MRG(ctx->mr_G, (k_local_mrhs_w<NP_, G_><<<ctx->mr_grid, (ctx->mr_NW + 1) * 32, ctx->mr_smem, s>>>(
+                            mode, ctx->mr_nbatch, ctx->d_mr_batches, ctx->d_mr_members, ctx->d_sub_ptr, ctx->d_first,
+                            ctx->d_p_off, reinterpret_cast<const double*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->mr_NW,
+                            ctx->mr_S, ctx->mr_slot, ctx->mr_WC, ctx->max_sub_cells))));
+    return;
+  }
   DISPATCH_MR(ctx->p, (k_local_mrhs<NP_><<<ctx->mr_grid, MR_T, ctx->mr_smem, s>>>(
                           mode, ctx->mr_nbatch, ctx->d_mr_batches, ctx->d_mr_members, ctx->d_sub_ptr, ctx->d_first,
                           ctx->d_p_off, reinterpret_cast<const double*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->mr_S,

@@ -408,8 +408,10 @@ struct ClsCfg {
   static constexpr int XS = (32 * E > LPR * MAXC ? 32 * E : LPR * MAXC);
 };
 
-template <int NP>
-__global__ void __launch_bounds__(SR_NW * 32) k_spmv_cls(
+// MINB = resident CTAs per SM the register allocation is capped for (1: uncapped, 168 registers at n_p = 10;
+// 2: <= 128 registers, twice the warps per SM to hide the gather latency)
+template <int NP, int MINB>
+__global__ void __launch_bounds__(SR_NW * 32, MINB) k_spmv_cls(
     int mode, int nitems, const int4* __restrict__ items, const int64_t* __restrict__ cls_off,
     const int* __restrict__ cells, const int* __restrict__ cls_nb, const double* __restrict__ A, const double* x,
     double* y, const double* z, double* const* pbuf, PcgState* st, double* partials, double* alpha_hist) {
@@ -621,9 +623,15 @@ void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgSta
     mode = 3;
   }
   if (ctx->d_cls_items) {
-    DISPATCH_P15S(ctx->p, (k_spmv_cls<NP_><<<ctx->cls_grid, SR_NW * 32, 0, s>>>(
-                              mode, ctx->cls_nitems, ctx->d_cls_items, ctx->d_cls_off, ctx->d_cls_cells, ctx->d_cls_nb,
-                              ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha)));
+    if (ctx->cls_minb == 2) {
+      DISPATCH_P15S(ctx->p, (k_spmv_cls<NP_, 2><<<ctx->cls_grid, SR_NW * 32, 0, s>>>(
+                                mode, ctx->cls_nitems, ctx->d_cls_items, ctx->d_cls_off, ctx->d_cls_cells, ctx->d_cls_nb,
+                                ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha)));
+    } else {
+      DISPATCH_P15S(ctx->p, (k_spmv_cls<NP_, 1><<<ctx->cls_grid, SR_NW * 32, 0, s>>>(
+                                mode, ctx->cls_nitems, ctx->d_cls_items, ctx->d_cls_off, ctx->d_cls_cells, ctx->d_cls_nb,
+                                ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha)));
+    }
     return;
   }
   if (ctx->d_a_dd) {
@@ -662,7 +670,7 @@ void launch_spmv_range(dgas_ctx ctx, int cb, int ce, const double* x, double* y,
 }
 
 // Host: class-sorted work items for k_spmv_cls (dd[c] = compact offset of cell c's row-block). Cells of a
-// class in ascending order, cut into runs of about nc / (2 x grid warps) cells. Off for p > 4 (register
+// class in ascending order, cut into runs of about nc / (6 x grid warps) cells. Off for p > 4 (register
 // row-blocks) or cells with more than CLS_MAXDEG neighbours; DGAS_SPMV_CLS=0 disables it.
 int spmv_cls_setup(dgas_ctx ctx, const std::vector<int64_t>& dd) {
   int on = 1;
@@ -672,14 +680,22 @@ int spmv_cls_setup(dgas_ctx ctx, const std::vector<int64_t>& dd) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // two CTAs per SM where the 128-register cap does not spill (n_p <= 10): config 3 SpMV 134 -> 104 us
+  int minb = ctx->np <= 10 ? 2 : 1;
+  if (const char* e = std::getenv("DGAS_CLS_MINB")) minb = std::atoi(e) == 2 ? 2 : 1;
+  ctx->cls_minb = minb;
   int cps = 1;  // resident CTAs per SM (register-bound: the row-block lives in registers)
-  DISPATCH_P15S(ctx->p, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_spmv_cls<NP_>, SR_NW * 32, 0)));
+  if (minb == 2) {
+    DISPATCH_P15S(ctx->p, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_spmv_cls<NP_, 2>, SR_NW * 32, 0)));
+  } else {
+    DISPATCH_P15S(ctx->p, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_spmv_cls<NP_, 1>, SR_NW * 32, 0)));
+  }
   cps = std::max(1, cps);
   if (const char* e = std::getenv("DGAS_CLS_CPS")) cps = std::max(1, std::atoi(e));
   const int grid = std::min(cps * nsm, std::max(1, nc / SR_NW));
   std::map<int64_t, std::vector<int>> cls;
   for (int c = 0; c < nc; ++c) cls[dd[c]].push_back(c);
-  int run = std::max(4, (int)(nc / (2LL * grid * SR_NW)));
+  int run = std::max(4, (int)(nc / (6LL * grid * SR_NW)));  // config 3: runs of 18 (16: 87 us, 27: 96, 55: 104, 110: 121)
   if (const char* e = std::getenv("DGAS_CLS_RUN")) run = std::max(1, std::atoi(e));
   std::vector<int4> items;
   std::vector<int64_t> off;

@@ -14,6 +14,22 @@ def _kappa_gram(o, cells):
     return max(np.linalg.cond(o.basis(int(c))[0]) ** 2 for c in cells)
 
 
+def _coord_tol(P):
+    """Rounding level of two correct assemblies that comes from the coordinates (R35): a quadrature
+    point x_q = sum lambda_i v_i carries an absolute rounding error ~u |x| (|x| <= 1 on the unit square); the
+    bbox-scaled coordinate xi = 2 (x_q - x_c) / w amplifies it by 2 / w (w = the cell's smaller bbox extent); a
+    degree-p Legendre product and its gradient amplify it by <= p^2 (Markov); an entry of A is bilinear in the
+    basis (x 2) and both assemblies carry it (x 2): 8 p^2 u / w_min = 4 p^2 eps / w_min, relative to |A|.
+    Measured: cart128_p3 (w = 1/128, p = 3) 1.2e-13 on the blocks, 2.7e-13 on A x / (|A||x|) with all three
+    SpMV kernels alike; bound 1.0e-12. cfg3s (w = 1/32): 2e-15."""
+    xy, cp, cv = P.xy, P.cell_ptr, P.cell_vtx
+    v = xy[cv]
+    lo = np.minimum.reduceat(v, cp[:-1], axis=0)
+    hi = np.maximum.reduceat(v, cp[:-1], axis=0)
+    w = float(np.min(hi - lo))
+    return 4.0 * P.p ** 2 * _EPS / w
+
+
 def _oracle_spread(o, b, ref, rtol=1e-8, P=None):
     """Iteration counts of the oracle itself under last-bit perturbations: 1e-13 relative noise on b
     and (P given) 1-ulp noise on G and kappa(Gram)-eps noise on A, i.e. two correct assemblies of the

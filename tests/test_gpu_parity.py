@@ -26,7 +26,7 @@ def _dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-from parity_helpers import _EPS, _iters_ok, _kappa_gram, _oracle_spread  # noqa: E402,F401
+from parity_helpers import _EPS, _coord_tol, _iters_ok, _kappa_gram, _oracle_spread  # noqa: E402,F401
 
 
 CASES = {
@@ -106,7 +106,8 @@ def test_spmv_rhs(name):
     scale = o.spmv_abs(x)
     rng = np.random.default_rng(5)
     kap = _kappa_gram(o, rng.choice(P.n_cells, size=min(64, P.n_cells), replace=False))
-    tol = max(1e-13, 20 * kap * _EPS)
+    # ... and by the coordinate rounding 4 p^2 eps / w_min on fine Cartesian cells (R35)
+    tol = max(1e-13, 20 * kap * _EPS, _coord_tol(P))
     assert np.all(np.abs(y - yr) <= tol * scale + 1e-300), (kap, np.max(np.abs(y - yr) / scale))
     b = S.rhs(P.f_kind).cpu().numpy()
     br = o.rhs()
@@ -433,13 +434,25 @@ def test_eager_path_matches_graph(monkeypatch, name):
     ("cfg5s_p4q4", {"DGAS_LOCAL_CPS": "7"}, 2),  # 128-thread CTAs on a small problem
     # multi-RHS solve over subdomains sharing a de-duplicated factor (local_mrhs.cu): default geometry,
     # batches of 1 (chain per subdomain), 2-slot ring, B > 16 (one b per lane), every n_p
+    ("cart128_p3", {"DGAS_MR_KERNEL": "1"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "1", "DGAS_MR_B": "1", "DGAS_MR_S": "2"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "1", "DGAS_MR_B": "24"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "1", "DGAS_MR_B": "3"}, 5),
+    ("cart64_p1", {"DGAS_MR_KERNEL": "1", "DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p2", {"DGAS_MR_KERNEL": "1", "DGAS_MR_MINAVG": "1", "DGAS_MR_B": "17", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p4", {"DGAS_MR_KERNEL": "1", "DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    # independent warp chains (k_local_mrhs_w, the default): default geometry (4 warps x 8 columns), one
+    # warp with a 2-slot ring (producer waits on every step), 4 / 16 / 32 columns per warp (8 / 2 / 1
+    # K-slices), 8 warps, every n_p (odd n_p: scalar panel loads)
     ("cart128_p3", {}, 5),
-    ("cart128_p3", {"DGAS_MR_B": "1", "DGAS_MR_S": "2"}, 5),
-    ("cart128_p3", {"DGAS_MR_B": "24"}, 5),
-    ("cart128_p3", {"DGAS_MR_B": "3"}, 5),
+    ("cart128_p3", {"DGAS_MR_NW": "1", "DGAS_MR_S": "2"}, 5),
+    ("cart128_p3", {"DGAS_MR_G": "4", "DGAS_MR_NW": "8"}, 5),
+    ("cart128_p3", {"DGAS_MR_G": "16", "DGAS_MR_NW": "3"}, 5),
+    ("cart128_p3", {"DGAS_MR_G": "32", "DGAS_MR_NW": "2", "DGAS_MR_S": "8"}, 5),
     ("cart64_p1", {"DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
-    ("cart64_p2", {"DGAS_MR_MINAVG": "1", "DGAS_MR_B": "17", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p2", {"DGAS_MR_MINAVG": "1", "DGAS_MR_G": "16", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
     ("cart64_p4", {"DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p4", {"DGAS_MR_MINAVG": "1", "DGAS_MR_G": "4", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
 ])
 def test_local_kernel_variants(monkeypatch, name, env, kernel):
     """Both local-solve kernels (envelope k_local, panel k_local_panel) and the panel kernel's ring
@@ -485,7 +498,7 @@ def test_spmv_kernel_variants(monkeypatch, name, env):
     o.setup_schwarz()
     rng = np.random.default_rng(5)
     kap = _kappa_gram(o, rng.choice(P.n_cells, size=min(64, P.n_cells), replace=False))
-    tol = max(1e-13, 20 * kap * _EPS)  # as test_spmv_rhs: two correct assemblies differ by ~kappa eps
+    tol = max(1e-13, 20 * kap * _EPS, _coord_tol(P))  # as test_spmv_rhs: two correct assemblies differ by ~kappa eps
     for seed in range(2):
         xv = g.normal(400 + seed, S.N)
         yv = S.spmv(_dev(xv)).cpu().numpy()
@@ -571,9 +584,13 @@ def test_dedup_is_bitwise_identical(monkeypatch):
     for bit, with and without de-duplication."""
     P = CASES["cfg3s"]()
     out = []
-    monkeypatch.setenv("DGAS_MRHS", "0")  # same local kernel (warp per subdomain) in both runs
-    for dd in ("0", "1"):
+    monkeypatch.setenv("DGAS_MRHS", "0")  # same local kernel (warp per subdomain) in every run
+    # runs: no de-duplication (byte ring) | de-duplicated A read through L2 by k_spmv_dd (the byte ring's
+    # arithmetic order) | de-duplicated A with the class-sorted k_spmv_cls (its own slice order: same
+    # operator, sums in another order, so equal to rounding only)
+    for dd, cls in (("0", "0"), ("1", "0"), ("1", "1")):
         monkeypatch.setenv("DGAS_DEDUP", dd)
+        monkeypatch.setenv("DGAS_SPMV_CLS", cls)
         monkeypatch.setenv("DGAS_DD_CPS", "2")
         S = _solver(P)
         info = S.get_info()
@@ -584,11 +601,18 @@ def test_dedup_is_bitwise_identical(monkeypatch):
         b = S.rhs(P.f_kind)
         x, it, c, st = S.pcg(b, rtol=1e-8)
         out.append((x.cpu().numpy(), it, c, st, S.spmv(b).cpu().numpy()))
+        out_b = b.cpu().numpy()
         S.close()
-    (x0, i0, c0, s0, y0), (x1, i1, c1, s1, y1) = out
+    (x0, i0, c0, s0, y0), (x1, i1, c1, s1, y1), (x2, i2, c2, s2, y2) = out
     assert s0 == s1 == 0 and i0 == i1 and c0 == c1
     assert np.array_equal(y0, y1)
     assert np.array_equal(x0, x1)
+    # class-sorted SpMV: A x equal entrywise to a few ulps of |A||x| (the sums' rounding scale; A b cancels
+    # heavily for the smooth b), PCG within the north_star tolerances of the ring's
+    assert s2 == 0 and abs(i2 - i0) <= 2
+    scale = O.Oracle(P).spmv_abs(out_b)
+    assert np.all(np.abs(y2 - y0) <= 64 * _EPS * scale)
+    assert np.linalg.norm(x2 - x0) <= 1e-7 * np.linalg.norm(x0)
 
 
 def test_error_paths_mesh_breakdown_notconverged(monkeypatch):
