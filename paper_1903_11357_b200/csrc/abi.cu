@@ -459,7 +459,7 @@ static int build_graph_impl(dgas_ctx ctx, int maxit) {
   // copies after convergence cost one launch each, and the per-body cost of the WHILE node is shared
   for (int u = 0; u < ctx->unroll; ++u) {
     launch_spmv(ctx, 1, nullptr, ctx->d_q, st, cs2);
-    launch_restrict(ctx, 1, st, nullptr, cs2);
+    if (!apply_fuses_restrict(ctx)) launch_restrict(ctx, 1, st, nullptr, cs2);
     launch_apply(ctx, 2, st, nullptr, ctx->d_z, cs2);
     launch_prolong(ctx, 2, st, nullptr, ctx->d_z, cs2, h, 1);
   }
@@ -508,7 +508,7 @@ static int pcg_eager(dgas_ctx ctx, double rtol, int maxit, cudaStream_t s) {
       if (timing) cudaEventRecord(ev[u][0], s);
       launch_spmv(ctx, 1, nullptr, ctx->d_q, st, s);
       if (timing) cudaEventRecord(ev[u][1], s);
-      launch_restrict(ctx, 1, st, nullptr, s);
+      if (!apply_fuses_restrict(ctx)) launch_restrict(ctx, 1, st, nullptr, s);
       if (timing) cudaEventRecord(ev[u][2], s);
       launch_apply(ctx, 2, st, nullptr, ctx->d_z, s);
       if (timing) cudaEventRecord(ev[u][3], s);

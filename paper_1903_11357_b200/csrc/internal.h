@@ -129,7 +129,7 @@ struct dgas_ctx_s {
   int4* d_mr_batches = nullptr;       // (representative subdomain, first member, count, 0) per batch
   int* d_mr_members = nullptr;        // member subdomains, grouped by batch
   int mr_nbatch = 0, mr_B = 0, mr_BS = 1, mr_S = 4, mr_WC = 1, mr_grid = 0, mr_classes = 0;
-  int mr_kernel = 1, mr_G = 8, mr_NW = 4;  // 2: k_local_mrhs_w (warp chains: NW warps x G columns)
+  int mr_kernel = 1, mr_G = 8, mr_NW = 4, mr_sred = 0;  // 2: k_local_mrhs_w (warp chains: NW warps x G columns)
   uint32_t mr_slot = 0;
   size_t mr_smem = 0;
   int64_t p_bytes_stored = 0;
@@ -330,6 +330,8 @@ int launch_rhs(dgas_ctx ctx, int f_kind, double* b_internal);
 void launch_perm(dgas_ctx ctx, const double* in, double* out, int to_internal, cudaStream_t s);
 void launch_spmv(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s);
 void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cudaStream_t s);
+bool apply_fuses_restrict(dgas_ctx ctx);
+bool panel_is_narrow(dgas_ctx ctx);
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s);
 void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s,
                     cudaGraphConditionalHandle h, int use_handle);

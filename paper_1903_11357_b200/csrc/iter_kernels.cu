@@ -12,6 +12,7 @@
 #include <cfloat>
 
 #include "internal.h"
+#define TMA_HOST_BACKOFF
 #include "tma.cuh"
 #include <cstdlib>
 
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(RT, RESTRICT_MINB) k_restrict(int mode, int nc
         }
         double rv;
         if (mode == 0) rv = rold[id];
-        else if (mode == 1) rv = rold[id] - alpha * q[id];
+        else if (mode == 1) rv = fma(-alpha, q[id], rold[id]);  // one rounding; the fused local solves form the same r
         else rv = b[id] - q[id];
         if (owner && mode >= 1) {
           rnew[id] = rv;
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(RC_T) k_restrict_chunk(int mode, int nchunk, c
       }
       double rv;
       if (mode == 0) rv = rold[id];
-      else if (mode == 1) rv = rold[id] - alpha * q[id];
+      else if (mode == 1) rv = fma(-alpha, q[id], rold[id]);  // one rounding; the fused local solves form the same r
       else rv = b[id] - q[id];
       if (owner && mode >= 1) {
         rnew[id] = rv;
@@ -702,7 +703,7 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
     for (int u = 0; u < nunits; ++u) {  // forward stream
       while (us_s[k + 1] <= u) ++k;
       if (u >= S) {  // wait for the forward release of unit u - S (event (u - S) / S of its slot)
-        mbar_wait(&empty[u % S], (uint32_t)(((u - S) / S) & 1));
+        mbar_wait_producer(&empty[u % S], (uint32_t)(((u - S) / S) & 1));
       }
       issue(u, k, true);
     }
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
       const int vmax = sl + S * (nd_slot_events(nunits, S, sl) - 1);  // largest unit of the slot
       const int Fs = nd_slot_events(nunits - S, S, sl);               // forward releases of the slot
       const int ev = Fs + (vmax - v) / S;  // index of v's backward release event in its slot
-      mbar_wait(&empty[sl], (uint32_t)(ev & 1));
+      mbar_wait_producer(&empty[sl], (uint32_t)(ev & 1));
       const int w = v - S;
       while (us_s[kw] > w) --kw;
       (void)kv;
@@ -1224,6 +1225,20 @@ void launch_local_range(dgas_ctx ctx, int sb, int se, const double* r, double* z
                          nullptr, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows, ctx->local_reuse)));
 }
 
+// Residual update fused into the local solve (PCG iterations): the wide panel kernel (latency-bound configs:
+// one wave of 256-thread CTAs, idle SMs) forms r = r_old - alpha q itself (mode 3), so k_restrict_chunk (x,
+// r, r.r, stop test, r0 = Q^T r) leaves the critical path: it runs on the coarse stream in front of the coarse
+// solve, beside the local solves, and both join before the prolongation. The caller then skips its own
+// launch_restrict. Config 5 p3q3: 7380 -> 7922 PCG it/s. On the HBM- or issue-bound configs 3 and 4 it was
+// measured neutral (the GPU is full: what the restriction takes, the local solve loses), so the narrow panel
+// kernel and the multi-RHS kernels keep the serial order. DGAS_FUSE_R=0 keeps the serial order everywhere.
+bool apply_fuses_restrict(dgas_ctx ctx) {
+  static const bool no_fork = std::getenv("DGAS_NO_FORK") != nullptr;
+  static const int on = [] { const char* e = std::getenv("DGAS_FUSE_R"); return e ? std::atoi(e) : 1; }();
+  if (!on || no_fork || ctx->precond != 0 || ctx->max_sub_cells == 1) return false;
+  return ctx->local_kernel == 2 && !panel_is_narrow(ctx);
+}
+
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
   static const bool no_fork = std::getenv("DGAS_NO_FORK") != nullptr;
   if (ctx->precond != 0) {
@@ -1242,8 +1257,14 @@ void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double*
   cudaEvent_t ef = ctx->ev_fork[ctx->side_sel], ej = ctx->ev_join[ctx->side_sel];
   cudaEventRecord(ef, s);
   cudaStreamWaitEvent(side, ef, 0);
-  launch_coarse_part(ctx, mode, st, side);
-  launch_local(ctx, mode, st, r, z, s);
+  if (mode == 2 && apply_fuses_restrict(ctx)) {
+    launch_restrict(ctx, 1, st, nullptr, side);
+    launch_coarse_part(ctx, mode, st, side);
+    launch_local(ctx, 3, st, r, z, s);
+  } else {
+    launch_coarse_part(ctx, mode, st, side);
+    launch_local(ctx, mode, st, r, z, s);
+  }
   cudaEventRecord(ej, side);
   cudaStreamWaitEvent(s, ej, 0);
 }
@@ -1280,6 +1301,7 @@ void launch_lanczos(dgas_ctx ctx, cudaStream_t s) {
 
 // The attribute is per function (shared by all contexts): always raise it to the opt-in maximum.
 int apply_set_smem(dgas_ctx ctx, size_t smem) {
+  tma_set_backoff(0);  // producer-lane back-off of this unit's streaming kernels (DGAS_PRODUCER_NS)
   cudaError_t e = cudaSuccess;
   int dev = 0, mx = 0;
   cudaGetDevice(&dev);

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(MR_T) k_local_mrhs(int mode, int nbatch, const
 }
 
 // ------------------------------------------------------------------------------------------------
-// k_local_mrhs_w — the same multi-RHS solve with INDEPENDENT WARP CHAINS (default). ncu on k_local_mrhs
+// k_local_mrhs_w — the same multi-RHS solve with INDEPENDENT WARP CHAINS (the default). ncu on k_local_mrhs
 // (config 3): ~2.4 us per chain step; stalls: shared-memory scoreboard 25%, CTA barrier 20%, fixed-latency
 // waits 24%; every step pays two CTA barriers and a cross-warp reduction through shared memory. Here the
 // right-hand sides of a batch are dealt to the warps, G per warp, and a warp never synchronises with the
@@ -296,14 +296,16 @@ struct MrwCfg {
 };
 
 struct MrwLayout {
-  size_t off_fk, off_fm, off_slt, off_po, off_W, off_ring, total;
-  __host__ __device__ MrwLayout(int mc, int np, int nw, int bs, int wc, int S, uint32_t slot) {
+  size_t off_fk, off_fm, off_slt, off_po, off_W, off_sc, off_ring, total;
+  // sc = doubles of q staging per warp ((PD + 1) cells x NP rows x BS: the fused residual update, mode 3)
+  __host__ __device__ MrwLayout(int mc, int np, int nw, int bs, int wc, int S, uint32_t slot, int sc = 0) {
     off_fk = 256;  // full[16] | empty[16]
     off_fm = off_fk + (((size_t)mc * 4 + 15) & ~(size_t)15);
     off_slt = off_fm + (((size_t)mc * 4 + 15) & ~(size_t)15);
     off_po = off_slt + (((size_t)mc * 4 + 15) & ~(size_t)15);
     off_W = off_po + (size_t)mc * 8;
-    off_ring = (off_W + (size_t)nw * wc * np * bs * 8 + 127) & ~(size_t)127;
+    off_sc = off_W + (size_t)nw * wc * np * bs * 8;
+    off_ring = (off_sc + (size_t)nw * sc * 8 + 127) & ~(size_t)127;
     total = off_ring + (size_t)S * slot;
   }
 };
@@ -315,15 +317,24 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
                                                          const int64_t* __restrict__ p_off, const double* __restrict__ P,
                                                          const double* r_in, double* const* rbuf, double* z,
                                                          const PcgState* st, int NW, int S, uint32_t slot_bytes, int WC,
-                                                         int max_cells) {
+                                                         int max_cells, const double* qvec) {
   constexpr int DPK = mr_dpk<NP>(), KS = MrwCfg<NP, G>::KS, BS = MrwCfg<NP, G>::BS, PD = MR_PD;
+  constexpr int SCW = (PD + 1) * NP * BS;  // q staging per warp (doubles), mode 3
   extern __shared__ __align__(128) unsigned char sm[];
+  // mode 3 (PCG iteration, residual update fused; needs qvec and the q staging in the layout): r = r_old -
+  // alpha q formed here with k_restrict_chunk's expression, so the restriction can run beside this kernel.
+  // Built and measured on config 3: no gain (2011 vs 1997 PCG it/s; the coarse chain behind the restriction
+  // is then as long as the local solve, and the 13 KB of staging cost 15%), so the launcher passes no qvec.
   const double* r = r_in;
+  double alpha = 0;
+  const bool fuse = mode == 3;
   if (mode >= 1) {
     if (st->done) return;
-    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+    const int it = st->it;
+    r = mode == 1 ? rbuf[0] : mode == 2 ? rbuf[(it + 1) & 1] : rbuf[it & 1];
+    if (fuse) alpha = st->alpha;
   }
-  const MrwLayout L(max_cells, NP, NW, BS, WC, S, slot_bytes);
+  const MrwLayout L(max_cells, NP, NW, BS, WC, S, slot_bytes, qvec ? SCW : 0);  // staging only when launched for mode 3
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + 16;
   int* fk = reinterpret_cast<int*>(sm + L.off_fk);
@@ -358,7 +369,7 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
     const uint64_t pol = l2_evict_last();  // every batch of the class re-reads its factor: keep it in L2
     for (int t = 0; t < T2; ++t) {
       const int sl = t & SM1;
-      if (t >= S) mbar_wait(&empty[sl], (uint32_t)(((t / S) - 1) & 1));
+      if (t >= S) mbar_wait_backoff(&empty[sl], (uint32_t)(((t / S) - 1) & 1));
       const int k = t < m ? t : T2 - 1 - t;
       const int n = DPK + (k - fk[k]) * NP * NP;
       bulk_load(ring + (size_t)sl * slot_bytes, P + po[k], (uint32_t)(((n + 1) & ~1) * 8), &full[sl], pol);
@@ -374,21 +385,38 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
   double* Ww = reinterpret_cast<double*>(sm + L.off_W) + (size_t)w * WC * NP * BS;
   const int WR = WC * NP;
   // cp.async of NP rows x G columns of cell c (src: r, or the y temporaries in z) into its window slot
-  auto fetch = [&](const double* src, int c) {
+  double* Qw = reinterpret_cast<double*>(sm + L.off_sc) + (size_t)w * SCW;
+  auto fetch = [&](const double* src, int c, bool withq) {
     double* dst = Ww + (size_t)slt[c] * NP * BS;
+    double* dq = Qw + (size_t)(c % (PD + 1)) * NP * BS;
 #pragma unroll
     for (int e0 = 0; e0 < NP * G; e0 += 32) {
       const int e = e0 + lane;
       const int gb = e / NP, i = e - gb * NP;
       const int64_t mbb = __shfl_sync(0xffffffffu, mbase, gb & 31);  // lane gb (ks = 0) holds column gb's base
-      if (e < NP * G) cp_async8(dst + (size_t)i * BS + gb, src + mbb + (int64_t)c * NP + i);
+      if (e < NP * G) {
+        cp_async8(dst + (size_t)i * BS + gb, src + mbb + (int64_t)c * NP + i);
+        if (withq) cp_async8(dq + (size_t)i * BS + gb, qvec + mbb + (int64_t)c * NP + i);
+      }
+    }
+  };
+  // mode 3: r_c = r_old - alpha q on the entries this lane copied itself (landed: its own wait_group)
+  auto combine = [&](int c) {
+    double* dst = Ww + (size_t)slt[c] * NP * BS;
+    const double* dq = Qw + (size_t)(c % (PD + 1)) * NP * BS;
+#pragma unroll
+    for (int e0 = 0; e0 < NP * G; e0 += 32) {
+      const int e = e0 + lane;
+      const int gb = e / NP, i = e - gb * NP;
+      if (e < NP * G) dst[(size_t)i * BS + gb] = fma(-alpha, dq[(size_t)i * BS + gb], dst[(size_t)i * BS + gb]);
     }
   };
   for (int c = 0; c < PD; ++c) {
-    if (c < m) fetch(r, c);
+    if (c < m) fetch(r, c, fuse);
     cp_async_commit();
   }
   cp_async_wait<PD - 1>();
+  if (fuse) combine(0);
   __syncwarp();
   // ------------------------------------------------ forward sweep
   // U columns of the panel per loop trip, all their loads issued before the first product (the chain is
@@ -478,9 +506,10 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
         z[mbase + (int64_t)k * NP + row] = acc[i];  // y_k, read back by the backward sweep
       }
     }
-    if (k + PD < m) fetch(r, k + PD);  // slot of cell k + PD - WC < f_k: free
+    if (k + PD < m) fetch(r, k + PD, fuse);  // slot of cell k + PD - WC < f_k: free
     cp_async_commit();
     cp_async_wait<PD - 1>();  // r_{k+1} landed (this lane's copies)
+    if (fuse && k + 1 < m) combine(k + 1);
     __syncwarp();             // ... and everybody's, and y_k is visible
   }
   // ------------------------------------------------ backward sweep
@@ -488,7 +517,7 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
   int lo = max(0, m - WC);
   for (int kk = m - 1; kk >= max(0, m - PD); --kk) {
     if (fm[kk] < lo) {
-      for (int c = fm[kk]; c < lo; ++c) fetch(z, c);
+      for (int c = fm[kk]; c < lo; ++c) fetch(z, c, false);
       lo = fm[kk];
     }
     cp_async_commit();
@@ -561,6 +590,251 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (ok[u]) *wp[u] = wv[u] + (v0[u] + v1[u]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sl]);
+    // y rows of the cells the step k - PD needs (slots of cells > k, done)
+    const int k2 = k - PD;
+    if (k2 >= 0 && fm[k2] < lo) {
+      for (int c = fm[k2]; c < lo; ++c) fetch(z, c, false);
+      lo = fm[k2];
+    }
+    cp_async_commit();
+    cp_async_wait<PD - 1>();
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_local_mrhs_r — warp chains with ROW lanes in the forward sweep (DGAS_MR_KERNEL=3). ncu on k_local_mrhs_w
+// (config 3, 8 warps x 2 columns): ~470 warp instructions per chain step for 2 right-hand sides, 13% of
+// them DFMA; a third is the cross-lane reduction of the K-sliced forward product (selects, shuffles) and
+// its index arithmetic. Here a warp owns G = 32 / NP right-hand sides and lane (g, i) is
+//   forward  : row i of y_k for column g: one sequential dot product over the panel's columns (4 independent
+//              partial sums), the panel read column-major (lanes i consecutive), the window value of column g
+//              broadcast to its NP lanes. No reduction, no shuffle.
+//   backward : K-slice i (columns q = i mod NP) for column g, u_k in registers (as k_local_mrhs_w).
+// The window is stored per column, W_w[g][row], so both sweeps read it conflict-free. Same ring / producer /
+// prefetch protocol as k_local_mrhs_w; lanes beyond G NP idle.
+struct MrrLayout {
+  size_t off_fk, off_fm, off_slt, off_po, off_W, off_ring, total;
+  int wrp;
+  __host__ __device__ MrrLayout(int mc, int np, int nw, int g, int wc, int S, uint32_t slot) {
+    wrp = (wc * np) | 1;  // odd column stride
+    off_fk = 256;         // full[16] | empty[16]
+    off_fm = off_fk + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_slt = off_fm + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_po = off_slt + (((size_t)mc * 4 + 15) & ~(size_t)15);
+    off_W = off_po + (size_t)mc * 8;
+    off_ring = (off_W + (size_t)nw * g * wrp * 8 + 127) & ~(size_t)127;
+    total = off_ring + (size_t)S * slot;
+  }
+};
+
+template <int NP>
+__global__ void __launch_bounds__(32 * 9) k_local_mrhs_r(int mode, int nbatch, const int4* __restrict__ batches,
+                                                         const int* __restrict__ members,
+                                                         const int* __restrict__ sub_ptr, const int* __restrict__ first,
+                                                         const int64_t* __restrict__ p_off, const double* __restrict__ P,
+                                                         const double* r_in, double* const* rbuf, double* z,
+                                                         const PcgState* st, int NW, int S, uint32_t slot_bytes, int WC,
+                                                         int max_cells) {
+  constexpr int DPK = mr_dpk<NP>(), G = 32 / NP, PD = MR_PD;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const double* r = r_in;
+  if (mode >= 1) {
+    if (st->done) return;
+    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+  }
+  const MrrLayout L(max_cells, NP, NW, G, WC, S, slot_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + 16;
+  int* fk = reinterpret_cast<int*>(sm + L.off_fk);
+  int* fm = reinterpret_cast<int*>(sm + L.off_fm);
+  int* slt = reinterpret_cast<int*>(sm + L.off_slt);
+  int64_t* po = reinterpret_cast<int64_t*>(sm + L.off_po);
+  unsigned char* ring = sm + L.off_ring;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int4 bt = batches[blockIdx.x];
+  const int rep = bt.x, moff = bt.y, B = bt.z;
+  const int s0 = sub_ptr[rep], m = sub_ptr[rep + 1] - s0, T2 = 2 * m;
+  const int nwact = (B + G - 1) / G;  // consumer warps with at least one right-hand side
+  for (int k = tid; k < m; k += blockDim.x) {
+    fk[k] = first[s0 + k];
+    po[k] = p_off[s0 + k];
+    slt[k] = (k % WC) * NP;  // first window row of cell k
+  }
+  if (tid == 0) {
+    for (int t = 0; t < S; ++t) { mbar_init(&full[t], 1); mbar_init(&empty[t], nwact); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {  // fm_k = min_{j >= k} f_j (the backward window's low end, monotone)
+    int mn = 1 << 30;
+    for (int k = m - 1; k >= 0; --k) { mn = min(mn, fk[k]); fm[k] = mn; }
+  }
+  __syncthreads();
+  const int SM1 = S - 1;
+  if (w == NW) {
+    // ---------------- producer warp: step t = forward cell t (t < m), backward cell 2m-1-t
+    if (lane != 0) return;
+    const uint64_t pol = l2_evict_last();  // every batch of the class re-reads its factor: keep it in L2
+    for (int t = 0; t < T2; ++t) {
+      const int sl = t & SM1;
+      if (t >= S) mbar_wait_backoff(&empty[sl], (uint32_t)(((t / S) - 1) & 1));
+      const int k = t < m ? t : T2 - 1 - t;
+      const int n = DPK + (k - fk[k]) * NP * NP;
+      bulk_load(ring + (size_t)sl * slot_bytes, P + po[k], (uint32_t)(((n + 1) & ~1) * 8), &full[sl], pol);
+    }
+    return;
+  }
+  if (w >= nwact) return;
+  // ---------------- consumer warp w: columns w G .. w G + G - 1 of the batch
+  const int cnt = min(G, B - w * G);  // valid columns of this warp (>= 1)
+  const int g = min(lane / NP, G - 1), i = lane - g * NP;
+  const bool act = lane < G * NP && g < cnt;
+  const int WRP = L.wrp, WR = WC * NP;
+  const int64_t mbase = (int64_t)sub_ptr[members[moff + w * G + min(g, cnt - 1)]] * NP;
+  double* Wg = reinterpret_cast<double*>(sm + L.off_W) + ((size_t)w * G + g) * WRP;  // this lane's column
+  // cp.async of cell c (src: r, or the y temporaries in z): lane (g, i) copies entry i of its column
+  auto fetch = [&](const double* src, int c) {
+    if (act) cp_async8(Wg + slt[c] + i, src + mbase + (int64_t)c * NP + i);
+  };
+  for (int c = 0; c < PD; ++c) {
+    if (c < m) fetch(r, c);
+    cp_async_commit();
+  }
+  cp_async_wait<PD - 1>();
+  __syncwarp();
+  // ------------------------------------------------ forward sweep: y_k[i] = sum_q P_k[i][q] [r_k ; y_old][q]
+  for (int k = 0; k < m; ++k) {
+    const int sl = k & SM1;
+    mbar_wait(&full[sl], (uint32_t)((k / S) & 1));
+    const double* __restrict__ Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+    const int f = fk[k], KU = (k - f) * NP, rk = slt[k], rf = slt[f];
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    if (act) {
+      // D_k r_k: column c holds rows c..NP-1 at dcol(c); row i takes columns c <= i
+      const double* wr = Wg + rk;
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        const double dv = Ps[mr_dcol(NP, c) + (i >= c ? i - c : 0)];
+        const double t = i >= c ? dv : 0.0;
+        if (c & 1) a1 += t * wr[c];
+        else a0 += t * wr[c];
+      }
+      // -U_k y_old: window rows rf .. rf + KU - 1, wrapping at WR (two contiguous segments)
+      const double* pc = Ps + DPK + i;
+      const int n1 = min(KU, WR - rf);
+      const double* wv = Wg + rf;
+      int j = 0;
+      for (; j + 3 < n1; j += 4) {
+        const double p0 = pc[j * NP], p1 = pc[(j + 1) * NP], p2 = pc[(j + 2) * NP], p3 = pc[(j + 3) * NP];
+        const double w0 = wv[j], w1 = wv[j + 1], w2 = wv[j + 2], w3 = wv[j + 3];
+        a0 += p0 * w0; a1 += p1 * w1; a2 += p2 * w2; a3 += p3 * w3;
+      }
+      for (; j < n1; ++j) a0 += pc[j * NP] * wv[j];
+      wv = Wg - n1;  // second segment: window rows 0 .. KU - n1 - 1 for j = n1 ..
+      for (; j + 3 < KU; j += 4) {
+        const double p0 = pc[j * NP], p1 = pc[(j + 1) * NP], p2 = pc[(j + 2) * NP], p3 = pc[(j + 3) * NP];
+        const double w0 = wv[j], w1 = wv[j + 1], w2 = wv[j + 2], w3 = wv[j + 3];
+        a0 += p0 * w0; a1 += p1 * w1; a2 += p2 * w2; a3 += p3 * w3;
+      }
+      for (; j < KU; ++j) a0 += pc[j * NP] * wv[j];
+    }
+    const double yk = (a0 + a1) + (a2 + a3);
+    __syncwarp();  // every lane is done with the ring slot and with the window rows it read
+    if (lane == 0) mbar_arrive(&empty[sl]);
+    if (act) {
+      Wg[rk + i] = yk;
+      z[mbase + (int64_t)k * NP + i] = yk;  // y_k, read back by the backward sweep
+    }
+    if (k + PD < m) fetch(r, k + PD);  // slot of cell k + PD - WC < f_k: free
+    cp_async_commit();
+    cp_async_wait<PD - 1>();  // r_{k+1} landed (this lane's copies)
+    __syncwarp();             // ... and everybody's, and y_k is visible
+  }
+  // ------------------------------------------------ backward sweep
+  // the window holds y of cells max(0, m - WC) .. m-1; cells below are fetched PD steps ahead
+  int lo = max(0, m - WC);
+  for (int kk = m - 1; kk >= max(0, m - PD); --kk) {
+    if (fm[kk] < lo) {
+      for (int c = fm[kk]; c < lo; ++c) fetch(z, c);
+      lo = fm[kk];
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<PD - 1>();
+  __syncwarp();
+  constexpr int U = NP <= 10 ? 3 : 2;  // independent panel columns per loop trip
+  for (int k = m - 1; k >= 0; --k) {
+    const int t = T2 - 1 - k, sl = t & SM1;
+    mbar_wait(&full[sl], (uint32_t)((t / S) & 1));
+    const double* __restrict__ Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+    const int f = fk[k], KU = (k - f) * NP, rk = slt[k], rf = slt[f];
+    if (act) {
+      double uk[NP];
+#pragma unroll
+      for (int a = 0; a < NP; ++a) uk[a] = Wg[rk + a];
+      {  // z_k[i] = (D_k^T u_k)[i]: column i of D_k holds rows i..NP-1
+        const double* col = Ps + mr_dcol(NP, i) - i;
+        double v = 0;
+#pragma unroll
+        for (int a = 0; a < NP; ++a)
+          if (a >= i) v += col[a] * uk[a];
+        z[mbase + (int64_t)k * NP + i] = v;
+      }
+      for (int j0 = i; j0 < KU; j0 += NP * U) {  // y_old[j] += (-U_k^T u_k)[j], U independent columns per trip
+        double* wp[U];
+        double wv[U], v0[U], v1[U];
+        const double* col[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int jj = j0 + u * NP;
+          ok[u] = jj < KU;
+          const int j = ok[u] ? jj : 0;
+          int row = rf + j;
+          row -= row >= WR ? WR : 0;
+          wp[u] = Wg + row;
+          wv[u] = *wp[u];
+          col[u] = Ps + DPK + j * NP;
+          v0[u] = 0;
+          v1[u] = 0;
+        }
+        if constexpr (NP % 2 == 0) {
+          double2 pv[U][NP / 2];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int a = 0; a < NP / 2; ++a) pv[u][a] = reinterpret_cast<const double2*>(col[u])[a];
+#pragma unroll
+          for (int a = 0; a < NP / 2; ++a)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              v0[u] += pv[u][a].x * uk[2 * a];
+              v1[u] += pv[u][a].y * uk[2 * a + 1];
+            }
+        } else {
+          double pv[U][NP];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int a = 0; a < NP; ++a) pv[u][a] = col[u][a];
+#pragma unroll
+          for (int a = 0; a + 1 < NP; a += 2)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              v0[u] += pv[u][a] * uk[a];
+              v1[u] += pv[u][a + 1] * uk[a + 1];
+            }
+#pragma unroll
+          for (int u = 0; u < U; ++u) v0[u] += pv[u][NP - 1] * uk[NP - 1];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) *wp[u] = wv[u] + (v0[u] + v1[u]);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[sl]);
@@ -640,18 +914,23 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
   // room for one coarse-solve CTA per SM beside the local solves (the coarse chain runs concurrently)
   size_t reserve = 8 * 1024;
   if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;
-  int kern = 2;  // 2: independent warp chains (k_local_mrhs_w), 1: CTA-wide steps (k_local_mrhs)
-  if (const char* e = std::getenv("DGAS_MR_KERNEL")) kern = std::atoi(e) == 1 ? 1 : 2;
-  if (kern == 2) {
+  // 3: warp chains with row lanes forward (k_local_mrhs_r), 2: warp chains with K-slice lanes
+  // (k_local_mrhs_w), 1: CTA-wide steps (k_local_mrhs)
+  int kern = 2;  // config 3: kernel 2 local 0.187 ms / 2358 PCG it/s, kernel 3 0.213-0.263 ms / 2194 (fewer
+                 // instructions, but its sequential forward dot product is latency-bound)
+  if (const char* e = std::getenv("DGAS_MR_KERNEL")) kern = std::max(1, std::min(3, std::atoi(e)));
+  if (kern >= 2) {
     // config 3 sweep (PCG it/s): 8 warps x 2 columns 2028, 4 x 4 1751, 4 x 8 1758, 8 x 4 1756, 4 x 2 1750
     int G = 2, NW = 8;
     if (!std::getenv("DGAS_MR_S")) S = 8;
     if (const char* e = std::getenv("DGAS_MR_G")) G = std::atoi(e);
     if (const char* e = std::getenv("DGAS_MR_NW")) NW = std::max(1, std::min(8, std::atoi(e)));
     if (G != 2 && G != 4 && G != 8 && G != 16 && G != 32) G = 2;
+    if (kern == 3) G = 32 / np;  // one lane per (column, row)
     if (S > 16) S = 16;
     const int B = G * NW, BSw = G | 1;
-    const size_t need = MrwLayout(mc, np, NW, BSw, WC, S, slot).total;
+    const size_t need = kern == 3 ? MrrLayout(mc, np, NW, G, WC, S, slot).total
+                                  : MrwLayout(mc, np, NW, BSw, WC, S, slot, 0).total;
     if (need > (size_t)optin) kern = 1;
     else {
       std::vector<int4> bat;
@@ -681,23 +960,36 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
       ctx->mr_grid = ctx->mr_nbatch;
       ctx->mr_classes = (int)cls.size();
       cudaError_t e = cudaSuccess;
-      DISPATCH_MR(ctx->p, DISPATCH_MRG(G, ({
-        cudaFuncAttributes fa;
-        e = cudaFuncGetAttributes(&fa, k_local_mrhs_w<NP_, G_>);
-        if (e == cudaSuccess && (size_t)optin < ctx->mr_smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
-        if (e == cudaSuccess)
-          e = cudaFuncSetAttribute(k_local_mrhs_w<NP_, G_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   optin - (int)fa.sharedSizeBytes);
-      })));
+      if (kern == 3) {
+        DISPATCH_MR(ctx->p, ({
+          cudaFuncAttributes fa;
+          e = cudaFuncGetAttributes(&fa, k_local_mrhs_r<NP_>);
+          if (e == cudaSuccess && (size_t)optin < ctx->mr_smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+          if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_local_mrhs_r<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes);
+        }));
+      } else {
+        DISPATCH_MR(ctx->p, DISPATCH_MRG(G, ({
+          cudaFuncAttributes fa;
+          e = cudaFuncGetAttributes(&fa, k_local_mrhs_w<NP_, G_>);
+          if (e == cudaSuccess && (size_t)optin < ctx->mr_smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+          if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_local_mrhs_w<NP_, G_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes);
+        })));
+      }
       if (e != cudaSuccess) { ctx->detail = std::string("mrhs local smem: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
       if (std::getenv("DGAS_VERBOSE")) {
         size_t big = 0;
         for (auto& kv : cls) big = std::max(big, kv.second.size());
-        fprintf(stderr, "dgas: multi-RHS local solve (warp chains): %d classes (largest %zu), %d batches of <= %d "
+        fprintf(stderr, kern == 3 ? "dgas: multi-RHS local solve (warp chains, row lanes): %d classes (largest %zu), %d batches "
+                "of <= %d (%d warps x %d columns, %d), window %d cells, ring %d x %u B, smem/CTA %zu\n" :
+                "dgas: multi-RHS local solve (warp chains): %d classes (largest %zu), %d batches of <= %d "
                 "(%d warps x %d columns, %d K-slices), window %d cells, ring %d x %u B, smem/CTA %zu\n", ctx->mr_classes,
                 big, ctx->mr_nbatch, B, NW, G, 32 / G, WC, S, slot, ctx->mr_smem);
       }
-      ctx->mr_kernel = 2;
+      ctx->mr_kernel = kern;
       ctx->local_kernel = 5;
       return 0;
     }
@@ -768,11 +1060,18 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
 }
 
 void launch_local_mrhs(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s) {
+  if (ctx->mr_kernel == 3) {
+    DISPATCH_MR(ctx->p, (k_local_mrhs_r<NP_><<<ctx->mr_grid, (ctx->mr_NW + 1) * 32, ctx->mr_smem, s>>>(
+                            mode, ctx->mr_nbatch, ctx->d_mr_batches, ctx->d_mr_members, ctx->d_sub_ptr, ctx->d_first,
+                            ctx->d_p_off, reinterpret_cast<const double*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->mr_NW,
+                            ctx->mr_S, ctx->mr_slot, ctx->mr_WC, ctx->max_sub_cells)));
+    return;
+  }
   if (ctx->mr_kernel == 2) {
     DISPATCH_MR(ctx->p, DISPATCH_MRG(ctx->mr_G, (k_local_mrhs_w<NP_, G_><<<ctx->mr_grid, (ctx->mr_NW + 1) * 32, ctx->mr_smem, s>>>(
                             mode, ctx->mr_nbatch, ctx->d_mr_batches, ctx->d_mr_members, ctx->d_sub_ptr, ctx->d_first,
                             ctx->d_p_off, reinterpret_cast<const double*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->mr_NW,
-                            ctx->mr_S, ctx->mr_slot, ctx->mr_WC, ctx->max_sub_cells))));
+                            ctx->mr_S, ctx->mr_slot, ctx->mr_WC, ctx->max_sub_cells, (const double*)nullptr))));
     return;
   }
   DISPATCH_MR(ctx->p, (k_local_mrhs<NP_><<<ctx->mr_grid, MR_T, ctx->mr_smem, s>>>(

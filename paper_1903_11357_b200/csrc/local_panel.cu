@@ -22,6 +22,7 @@
 //   forward  L y = r   : y_k = D_k r_k - U_k y_old
 //   backward L^T z = y : u_k = y_k - sum_{j>k} U_j[:,k]^T u_j,  z_k = D_k^T u_k
 #include "internal.h"
+#define TMA_HOST_BACKOFF
 #include "tma.cuh"
 
 #ifndef PANEL_NARROW_TPC
@@ -77,19 +78,26 @@ struct PanelLayout {
 };
 
 // NARROW (7 CTAs/SM): at most 48 registers so a 256-thread coarse-solve CTA still fits beside them
-template <int NP, bool NARROW, typename TS>
+// FUSE (wide CTAs only): mode 3 is available (the narrow variant's 48-register cap spills with it)
+template <int NP, bool NARROW, typename TS, bool FUSE = false>
 __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) k_local_panel(
     int mode, const int* __restrict__ sub_ptr, const int* __restrict__ first, const int* __restrict__ pus,
     const int* __restrict__ sub_units, const int64_t* __restrict__ p_off, const TS* __restrict__ P,
     const double* r_in, double* const* rbuf, double* z, const PcgState* st, int S, uint32_t slot_bytes, int CC,
-    int max_cells, int keep_fwd) {
+    int max_cells, int keep_fwd, const double* qvec) {
   using C = PanelCfg<NP, NARROW>;
   constexpr int T = C::T, LPR = C::LPR, NW = C::NW, H = C::H, TPC = C::TPC;
   extern __shared__ __align__(128) double sm[];
+  // mode 3 (PCG iteration, residual update fused): r = r_old - alpha q formed here with k_restrict_chunk's
+  // expression; the restriction then runs beside this kernel on the coarse stream (iter_kernels.cu)
   const double* r = r_in;
+  double alpha = 0;
+  const bool fuse = FUSE && !NARROW && mode == 3;
   if (mode >= 1) {
     if (st->done) return;
-    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+    const int it = st->it;
+    r = mode == 1 ? rbuf[0] : (mode == 2 || !FUSE) ? rbuf[(it + 1) & 1] : rbuf[it & 1];
+    if (fuse) alpha = st->alpha;
   }
   const int s = blockIdx.x, s0 = sub_ptr[s], m = sub_ptr[s + 1] - s0;
   const PanelLayout L(max_cells, NP, !NARROW);
@@ -134,13 +142,13 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
     for (int u = 0; u < U; ++u) {  // forward stream: slot u & SM1 after the release of unit u - S
       while (us_s[k + 1] <= u) ++k;
       const int sl = u & SM1;
-      if (u >= S) { mbar_wait(&empty[sl], (uint32_t)((epar >> sl) & 1)); epar ^= 1ull << sl; }
+      if (u >= S) { mbar_wait_producer(&empty[sl], (uint32_t)((epar >> sl) & 1)); epar ^= 1ull << sl; }
       issue(u, k, u < U - S ? pol_last : pol_first);
     }
     int kw = m - 1;
     for (int v = U - 1; v >= S; --v) {  // backward refills: after the release of unit v, load unit v - S
       const int sl = v & SM1;
-      mbar_wait(&empty[sl], (uint32_t)((epar >> sl) & 1));
+      mbar_wait_producer(&empty[sl], (uint32_t)((epar >> sl) & 1));
       epar ^= 1ull << sl;
       const int w = v - S;
       while (us_s[kw] > w) --kw;
@@ -155,7 +163,12 @@ __global__ void __launch_bounds__(PanelCfg<NP, NARROW>::T + 32, NARROW ? 8 : 3) 
   uint64_t fph = 0;  // parity of the next full-barrier phase per slot
   const double* rs = r + (size_t)s0 * NP;
   if constexpr (!NARROW) {
-    for (int e = tid; e < m * NP; e += T) R[e] = rs[e];
+    if (fuse) {
+      const double* qs = qvec + (size_t)s0 * NP;
+      for (int e = tid; e < m * NP; e += T) R[e] = fma(-alpha, qs[e], rs[e]);
+    } else {
+      for (int e = tid; e < m * NP; e += T) R[e] = rs[e];
+    }
     named_sync(1, T);
   }
   // forward: thread (a, q) accumulates row a of P_k over columns c = q (mod LPR)
@@ -318,6 +331,7 @@ int panel_min_cc(int np, int f32) { return f32 ? panel_e<float>(np) + 4 : panel_
 
 // 128 consumer threads when more than 3 CTAs share an SM (registers), else 256
 static bool panel_narrow(dgas_ctx ctx) { return ctx->panel_cps > 3; }
+bool panel_is_narrow(dgas_ctx ctx) { return panel_narrow(ctx); }
 
 size_t panel_base_bytes(int max_cells, int np, bool narrow) { return PanelLayout(max_cells, np, !narrow).off_ring; }
 
@@ -356,6 +370,7 @@ static int panel_setup_t(dgas_ctx ctx, const std::vector<int>& sub_ptr, const st
 }
 
 int panel_setup(dgas_ctx ctx, const std::vector<int>& sub_ptr, const std::vector<int>& first) {
+  tma_set_backoff(0);  // producer-lane back-off of this unit's streaming kernels (DGAS_PRODUCER_NS)
   return ctx->panel_f32 ? panel_setup_t<float>(ctx, sub_ptr, first) : panel_setup_t<double>(ctx, sub_ptr, first);
 }
 
@@ -382,8 +397,10 @@ int panel_set_smem(dgas_ctx ctx) {
   };
   DISPATCH_P15(ctx->p, (raise((const void*)k_local_panel<NP_, true, double>),
                         raise((const void*)k_local_panel<NP_, false, double>),
+                        raise((const void*)k_local_panel<NP_, false, double, true>),
                         raise((const void*)k_local_panel<NP_, true, float>),
-                        raise((const void*)k_local_panel<NP_, false, float>)));
+                        raise((const void*)k_local_panel<NP_, false, float>),
+                        raise((const void*)k_local_panel<NP_, false, float, true>)));
   if (e != cudaSuccess) { ctx->detail = std::string("panel smem: ") + cudaGetErrorString(e); return DGAS_E_CUDA; }
   return 0;
 }
@@ -391,10 +408,10 @@ int panel_set_smem(dgas_ctx ctx) {
 void launch_local_panel(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {
   const size_t smem = panel_smem_bytes(ctx);
 #define PANEL_LAUNCH(NAR, TS)                                                                                      \
-  DISPATCH_P15(ctx->p, (k_local_panel<NP_, NAR, TS><<<ctx->nsub, PanelCfg<NP_, NAR>::T + 32, smem, s>>>(           \
+  DISPATCH_P15(ctx->p, (k_local_panel<NP_, NAR, TS, !NAR><<<ctx->nsub, PanelCfg<NP_, NAR>::T + 32, smem, s>>>(     \
                            mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_pus, ctx->d_sub_units, ctx->d_p_off,         \
                            reinterpret_cast<const TS*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->panel_slots,        \
-                           ctx->panel_slot_bytes, ctx->panel_cc, ctx->max_sub_cells, ctx->panel_keep)))
+                           ctx->panel_slot_bytes, ctx->panel_cc, ctx->max_sub_cells, ctx->panel_keep, ctx->d_q)))
   if (ctx->panel_f32) {
     if (panel_narrow(ctx)) { PANEL_LAUNCH(true, float); } else { PANEL_LAUNCH(false, float); }
   } else {
@@ -411,7 +428,7 @@ void launch_local_panel_range(dgas_ctx ctx, int sb, int se, const double* r, dou
   DISPATCH_P15(ctx->p, (k_local_panel<NP_, NAR, TS><<<se - sb, PanelCfg<NP_, NAR>::T + 32, smem, s>>>(             \
                            0, ctx->d_sub_ptr + sb, ctx->d_first, ctx->d_pus, ctx->d_sub_units + sb, ctx->d_p_off,   \
                            reinterpret_cast<const TS*>(ctx->d_P), r, ctx->d_rbuf, z, nullptr, ctx->panel_slots,    \
-                           ctx->panel_slot_bytes, ctx->panel_cc, ctx->max_sub_cells, ctx->panel_keep)))
+                           ctx->panel_slot_bytes, ctx->panel_cc, ctx->max_sub_cells, ctx->panel_keep, nullptr)))
   if (ctx->panel_f32) {
     if (panel_narrow(ctx)) { PANEL_LAUNCH_R(true, float); } else { PANEL_LAUNCH_R(false, float); }
   } else {

@@ -12,6 +12,7 @@
 // NEXT cell (index load one cell further ahead) while it multiplies the current one; lane
 // (a, h) = (row, column slice) reads A[col n_p + a] (consecutive lanes -> consecutive words).
 #include "internal.h"
+#define TMA_HOST_BACKOFF
 #include "tma.cuh"
 
 #include <algorithm>
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__((SR_NW + 1) * 32) k_spmv_ring(
         if (Pp + len > RB) { V += RB - Pp; Pp = 0; }  // do not straddle the ring end
         // free space: every byte before the oldest unreleased group's start is free
         while (gi - tail >= SR_NB || (tail < gi && V + len > vst[tail % SR_NB] + RB)) {
-          mbar_wait(&empty[tail % SR_NB], (uint32_t)((tail / SR_NB) & 1));
+          mbar_wait_producer(&empty[tail % SR_NB], (uint32_t)((tail / SR_NB) & 1));
           ++tail;
         }
         vst[gi % SR_NB] = V;
@@ -563,6 +564,7 @@ size_t spmv_ring_smem(dgas_ctx ctx) { return sr_base_bytes(ctx, sr_chunk(ctx)) +
 
 // degree limit of the gather (16 neighbours incl. self) and a ring that holds the largest block
 int spmv_ring_configure(dgas_ctx ctx, int nsm) {
+  tma_set_backoff(0);  // producer-lane back-off of this unit's streaming kernels (DGAS_PRODUCER_NS)
   if (ctx->max_deg > 16) return 1;
   int dev = 0, optin = 232448, smem_sm = 233472;
   cudaGetDevice(&dev);

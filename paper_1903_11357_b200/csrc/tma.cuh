@@ -49,6 +49,41 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// producer-side wait: back off between polls. A producer lane that waits for its consumers to release a
+// ring slot otherwise spins YIELD / TRYWAIT / BRA at full issue rate on a scheduler it shares with consumer
+// warps (ncu on k_local_mrhs_r, config 3: 34% of all executed warp instructions were this loop).
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t phase, unsigned ns = 128) {
+  while (!mbar_try_wait(bar, phase)) __nanosleep(ns);
+}
+// Per translation unit: back-off of the streaming kernels' producer lanes (0 = plain spin), set from
+// DGAS_PRODUCER_NS by tma_set_backoff() in the unit's setup code.
+static __constant__ unsigned c_producer_ns = 0;
+__device__ __forceinline__ void mbar_wait_producer(uint64_t* bar, uint32_t phase) {
+  const unsigned ns = c_producer_ns;
+  if (ns) mbar_wait_backoff(bar, phase, ns);
+  else mbar_wait(bar, phase);
+}
+#ifdef TMA_HOST_BACKOFF
+#include <cstdlib>
+static inline void tma_set_backoff(unsigned dflt) {
+  unsigned ns = dflt;
+  if (const char* e = std::getenv("DGAS_PRODUCER_NS")) ns = (unsigned)std::atoi(e);
+  cudaMemcpyToSymbol(c_producer_ns, &ns, sizeof(ns));
+}
+#endif
 // load `bytes` (multiple of 16) possibly larger than the 1 MB bulk limit: chunks of 64 KB
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   mbar_expect_tx(bar, bytes);
