@@ -644,13 +644,18 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
                                                                 const double* __restrict__ Dinv, const double* r_in,
                                                                 double* const* rbuf, double* z, const PcgState* st,
                                                                 int S, uint32_t slot_bytes, int ymax_cells, int CC,
-                                                                int reuse) {
+                                                                int reuse, const double* qvec) {
   constexpr int T = LocalCfg<NP>::T, NW = LocalCfg<NP>::W;
   extern __shared__ __align__(128) double sm[];
+  // mode 3: residual update fused (r = r_old - alpha q formed here, see apply_fuses_restrict)
   const double* r = r_in;
+  double alpha = 0;
+  const bool fuse = mode == 3;
   if (mode >= 1) {
     if (st->done) return;
-    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+    const int it = st->it;
+    r = mode == 1 ? rbuf[0] : mode == 2 ? rbuf[(it + 1) & 1] : rbuf[it & 1];
+    if (fuse) alpha = st->alpha;
   }
   const int s = blockIdx.x;
   const int s0 = sub_ptr[s], m = sub_ptr[s + 1] - s0;
@@ -725,12 +730,23 @@ __global__ void __launch_bounds__(LocalCfg<NP>::T + 32) k_local(int mode, const 
   const int lane = threadIdx.x & 31;
   uint64_t ph = 0;
   const double* rs = r + (size_t)s0 * NP;
-  for (int e = threadIdx.x; e < m * NP; e += T) {
-    const int k = e / NP, a = e % NP;
-    const double* D = Dinv + ((size_t)(s0 + k) * NP + a) * NP;
-    double v = 0;
-    for (int c = 0; c <= a; ++c) v += __ldg(D + c) * rs[k * NP + c];
-    y[e] = v;
+  if (fuse) {
+    const double* qs = qvec + (size_t)s0 * NP;
+    for (int e = threadIdx.x; e < m * NP; e += T) {
+      const int k = e / NP, a = e % NP;
+      const double* D = Dinv + ((size_t)(s0 + k) * NP + a) * NP;
+      double v = 0;
+      for (int c = 0; c <= a; ++c) v += __ldg(D + c) * fma(-alpha, qs[k * NP + c], rs[k * NP + c]);
+      y[e] = v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < m * NP; e += T) {
+      const int k = e / NP, a = e % NP;
+      const double* D = Dinv + ((size_t)(s0 + k) * NP + a) * NP;
+      double v = 0;
+      for (int c = 0; c <= a; ++c) v += __ldg(D + c) * rs[k * NP + c];
+      y[e] = v;
+    }
   }
   named_sync(1, T);
   // forward: thread (a, q) accumulates row a over columns col = q (mod 8) of every unit of U_k
@@ -1200,7 +1216,8 @@ static void launch_local(dgas_ctx ctx, int mode, PcgState* st, const double* r, 
   const size_t smem = apply_smem_bytes(ctx);
   DISPATCH_P(ctx->p, (k_local<NP_><<<ctx->nsub, LocalCfg<NP_>::T + 32, smem, s>>>(
                          mode, ctx->d_sub_ptr, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
-                         st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows, ctx->local_reuse)));
+                         st, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows, ctx->local_reuse,
+                         ctx->d_q)));
 }
 
 // local solves of subdomains [sb, se) only (sharded solve, shard.cu; mode 0): the single-GPU kernels
@@ -1222,11 +1239,12 @@ void launch_local_range(dgas_ctx ctx, int sb, int se, const double* r, double* z
   const size_t smem = apply_smem_bytes(ctx);
   DISPATCH_P(ctx->p, (k_local<NP_><<<se - sb, LocalCfg<NP_>::T + 32, smem, s>>>(
                          0, ctx->d_sub_ptr + sb, ctx->d_first, ctx->d_u_off, ctx->d_U, ctx->d_Dinv, r, ctx->d_rbuf, z,
-                         nullptr, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows, ctx->local_reuse)));
+                         nullptr, ctx->ring_slots, ctx->slot_bytes, ctx->max_sub_cells, ctx->ring_rows, ctx->local_reuse,
+                         nullptr)));
 }
 
-// Residual update fused into the local solve (PCG iterations): the wide panel kernel (latency-bound configs:
-// one wave of 256-thread CTAs, idle SMs) forms r = r_old - alpha q itself (mode 3), so k_restrict_chunk (x,
+// Residual update fused into the local solve (PCG iterations): the wide panel kernel, the envelope kernel and
+// the explicit-inverse kernel (latency-bound configs: one wave of CTAs, idle SMs) form r = r_old - alpha q itself (mode 3), so k_restrict_chunk (x,
 // r, r.r, stop test, r0 = Q^T r) leaves the critical path: it runs on the coarse stream in front of the coarse
 // solve, beside the local solves, and both join before the prolongation. The caller then skips its own
 // launch_restrict. Config 5 p3q3: 7380 -> 7922 PCG it/s. On the HBM- or issue-bound configs 3 and 4 it was
@@ -1236,7 +1254,7 @@ bool apply_fuses_restrict(dgas_ctx ctx) {
   static const bool no_fork = std::getenv("DGAS_NO_FORK") != nullptr;
   static const int on = [] { const char* e = std::getenv("DGAS_FUSE_R"); return e ? std::atoi(e) : 1; }();
   if (!on || no_fork || ctx->precond != 0 || ctx->max_sub_cells == 1) return false;
-  return ctx->local_kernel == 2 && !panel_is_narrow(ctx);
+  return (ctx->local_kernel == 2 && !panel_is_narrow(ctx)) || ctx->local_kernel == 1 || ctx->local_kernel == 3;
 }
 
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s) {

@@ -40,12 +40,17 @@ __global__ void __launch_bounds__(INV_T) k_local_inv(int mode, int np, const int
                                                      const int* __restrict__ sub_ptr,
                                                      const int64_t* __restrict__ zoff, const double* __restrict__ Z,
                                                      const double* r_in, double* const* rbuf, double* z,
-                                                     const PcgState* st) {
+                                                     const PcgState* st, const double* qvec) {
   extern __shared__ double rs[];
+  // mode 3: residual update fused (r = r_old - alpha q formed while staging, see apply_fuses_restrict)
   const double* r = r_in;
+  double alpha = 0;
+  const bool fuse = mode == 3;
   if (mode >= 1) {
     if (st->done) return;
-    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+    const int it0 = st->it;
+    r = mode == 1 ? rbuf[0] : mode == 2 ? rbuf[(it0 + 1) & 1] : rbuf[it0 & 1];
+    if (fuse) alpha = st->alpha;
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
@@ -54,7 +59,8 @@ __global__ void __launch_bounds__(INV_T) k_local_inv(int mode, int np, const int
     const int s = wi.x, row0 = wi.y;
     const int n = (sub_ptr[s + 1] - sub_ptr[s]) * np;
     const size_t off = (size_t)sub_ptr[s] * np;
-    for (int k = threadIdx.x; k < n; k += INV_T) rs[k] = r[off + k];
+    if (fuse) for (int k = threadIdx.x; k < n; k += INV_T) rs[k] = fma(-alpha, qvec[off + k], r[off + k]);
+    else for (int k = threadIdx.x; k < n; k += INV_T) rs[k] = r[off + k];
     __syncthreads();
     const double* Zs = Z + zoff[s];
     const int r1 = min(n, row0 + INV_ROWS);
@@ -89,7 +95,7 @@ void launch_local_inv(dgas_ctx ctx, int mode, const PcgState* st, const double* 
   const int grid = std::min(ctx->inv_nitems, ctx->inv_grid);
   k_local_inv<<<grid, INV_T, (size_t)ctx->inv_maxn * 8, s>>>(mode, ctx->np, ctx->d_inv_items, ctx->inv_nitems,
                                                              ctx->d_sub_ptr, ctx->d_inv_zoff, ctx->d_inv_Z, r,
-                                                             ctx->d_rbuf, z, st);
+                                                             ctx->d_rbuf, z, st, ctx->d_q);
 }
 
 // the work items of subdomains [sb, se) only (sharded solve, mode 0)
@@ -97,7 +103,7 @@ void launch_local_inv_range(dgas_ctx ctx, int sb, int se, const double* r, doubl
   const int i0 = ctx->inv_item_ptr[sb], n = ctx->inv_item_ptr[se] - i0;
   if (n <= 0) return;
   k_local_inv<<<std::min(n, ctx->inv_grid), INV_T, (size_t)ctx->inv_maxn * 8, s>>>(
-      0, ctx->np, ctx->d_inv_items + i0, n, ctx->d_sub_ptr, ctx->d_inv_zoff, ctx->d_inv_Z, r, ctx->d_rbuf, z, nullptr);
+      0, ctx->np, ctx->d_inv_items + i0, n, ctx->d_sub_ptr, ctx->d_inv_zoff, ctx->d_inv_Z, r, ctx->d_rbuf, z, nullptr, nullptr);
 }
 
 // Build Z_i after the local-solve kernel is configured; switch local_kernel to 3 when accepted.
