@@ -361,6 +361,15 @@ def main():
     except Exception:
         pass
     spmv_apply_gbs = (alg["spmv"] + alg["apply_total"]) / ((kt["spmv"] + kt["apply_total"]) * 1e-3) / 1e9
+    # fp64 arithmetic of the dominant kernel against the CUDA-core FP64 peak (148 SMs x 64 FMA/clk x 2 flop at
+    # the SM clock: 37.2 TFLOP/s at 1965 MHz): every stored operator entry is one FMA per use
+    # (SpMV: all stored blocks; local solves: factor + D triangles, forward and backward sweep)
+    props = torch.cuda.get_device_properties(local)
+    fp64_peak = props.multi_processor_count * 64 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    flops = {"spmv": 2.0 * nnzb * npp * npp, "local": 4.0 * (info["bytes_U"] + dinv_tri) / 8.0}
+    alu = {"bound": "alu", "achieved": flops[dom] / (kt[dom] * 1e-3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+           "frac": flops[dom] / (kt[dom] * 1e-3) / 1e12 / fp64_peak,
+           "note": "fp64 FMA work of the same kernel against the CUDA-core FP64 peak (no tensor cores on this path)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "PCG it/s", "n_gpus": world, "steps": args.steps,
@@ -389,10 +398,12 @@ def main():
         "roofline": {"bound": "hbm", "achieved": kern[dom]["GBps"], "peak": hbm_peak, "unit": "GB/s",
                      "frac": kern[dom]["frac"], "traffic": traffic, "kernel": dom,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s",
+                     "alu": alu,
                      **({"note": (f"operators de-duplicated (exact, NEXT-4): A {info['dedup_A_bytes'] / 1e6:.1f} MB and "
                                   f"local factors {info['dedup_local_bytes'] / 1e6:.1f} MB stored, L2-resident; "
                                   f"'achieved' divides the SURVEY 8(d) algorithmic bytes (full envelope factor) by the "
-                                  f"launch time, 'traffic' is what ncu measured from DRAM")}
+                                  f"launch time (it can exceed the HBM peak: the shared operators are read from "
+                                  f"L2, the kernel is instruction-bound), 'traffic' is what ncu measured from DRAM")}
                         if info.get("dedup_A_bytes") else {})},
         "kernels": kern,
         "e2e": {"value": e2e_value, "unit": "PCG it/s", "h2d_bytes_per_step": 2 * N * 8,

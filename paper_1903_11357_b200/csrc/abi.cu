@@ -157,7 +157,7 @@ static int finish_setup_buffers(dgas_ctx ctx) {
       int dev = 0, nsm = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      int per_sm = 4;
+      int per_sm = std::min(4, restrict_ctas_per_sm(ctx));  // one wave (the kernel is persistent)
       if (const char* e2 = std::getenv("DGAS_RESTRICT_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e2));
       const int warps = restrict_chunk_threads() / 32;
       ctx->rc_grid = std::max(1, std::min(per_sm * nsm, (ctx->nchunk + warps - 1) / warps));
@@ -166,8 +166,8 @@ static int finish_setup_buffers(dgas_ctx ctx) {
     }
   }
   {
-    // persistent prolongation: 4 CTAs of 256 threads per SM (64 registers; DGAS_PROLONG_CTAS_PER_SM)
-    int dev = 0, nsm = 148, per = 4;
+    // persistent prolongation: one wave of 256-thread CTAs, at most 4 per SM (DGAS_PROLONG_CTAS_PER_SM)
+    int dev = 0, nsm = 148, per = std::min(4, prolong_ctas_per_sm(ctx));
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (const char* e = std::getenv("DGAS_PROLONG_CTAS_PER_SM")) per = std::max(1, std::atoi(e));

@@ -122,6 +122,7 @@ struct dgas_ctx_s {
   int* d_cls_cells = nullptr;          // cells grouped by class
   int* d_cls_nb = nullptr;             // [nc][CLS_MAXDEG] neighbour cells of d_cls_cells[i]
   int cls_nitems = 0, cls_grid = 0, cls_minb = 1;
+  int fuse_r = -1;  // residual update fused into the local solve (apply_fuses_restrict), -1 = not decided yet
   std::vector<int64_t> a_dd_h;
   int64_t a_unique = 0, a_bytes_stored = 0;  // distinct row-blocks, bytes of the compact A
   int p_unique = 0;                   // distinct subdomain factors (panel store)
@@ -331,6 +332,8 @@ void launch_perm(dgas_ctx ctx, const double* in, double* out, int to_internal, c
 void launch_spmv(dgas_ctx ctx, int mode, const double* x, double* y, PcgState* st, cudaStream_t s);
 void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cudaStream_t s);
 bool apply_fuses_restrict(dgas_ctx ctx);
+int restrict_ctas_per_sm(dgas_ctx ctx);
+int prolong_ctas_per_sm(dgas_ctx ctx);
 bool panel_is_narrow(dgas_ctx ctx);
 void launch_apply(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s);
 void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, double* z, cudaStream_t s,

@@ -453,6 +453,55 @@ __global__ void __launch_bounds__(RC_T) k_restrict_chunk(int mode, int nchunk, c
     const int ke = cd.z;
     int k = act ? cd.y + lane / L : ke;
     int2 rec = k < ke ? rrec[k] : make_int2(0, 0);
+    if constexpr (NQ <= 3) {
+      // two warp steps per trip with the loads of both issued first (latency-bound: one dependent round of
+      // loads per step); the sums keep the piece order (step A, then step B)
+      int2 recB = k + PPW < ke ? rrec[k + PPW] : rec;
+      for (; k < ke; k += 2 * PPW) {
+        const int2 recA2 = k + 2 * PPW < ke ? rrec[k + 2 * PPW] : rec;
+        const int2 recB2 = k + 3 * PPW < ke ? rrec[k + 3 * PPW] : rec;
+        const bool okB = k + PPW < ke;
+        const int2 rB = okB ? recB : rec;
+        const int cellA = rec.x, oA = rec.y & 0x7fffffff, cellB = rB.x, oB = rB.y & 0x7fffffff;
+        const bool ownA = rec.y < 0 && mode >= 1, ownB = okB && rB.y < 0 && mode >= 1;
+        const size_t idA = (size_t)cellA * NP + a, idB = (size_t)cellB * NP + a;
+        double gA[NQ], gB[NQ];
+        const double* GoA = G + ((size_t)oA * NP + a) * NQ;
+        const double* GoB = G + ((size_t)oB * NP + a) * NQ;
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) { gA[c] = __ldg(GoA + c); gB[c] = __ldg(GoB + c); }
+        double r1A = 0, r2A = 0, r1B = 0, r2B = 0, xA = 0, pA = 0, xB = 0, pB = 0;
+        if (mode == 0) { r1A = rold[idA]; r1B = rold[idB]; }
+        else if (mode == 1) { r1A = rold[idA]; r2A = q[idA]; r1B = rold[idB]; r2B = q[idB]; }
+        else { r1A = b[idA]; r2A = q[idA]; r1B = b[idB]; r2B = q[idB]; }
+        if (mode == 1) {
+          if (ownA) { xA = x[idA]; pA = pnew[idA]; }
+          if (ownB) { xB = x[idB]; pB = pnew[idB]; }
+        }
+        const double rvA = mode == 0 ? r1A : mode == 1 ? fma(-alpha, r2A, r1A) : r1A - r2A;
+        const double rvB = mode == 0 ? r1B : mode == 1 ? fma(-alpha, r2B, r1B) : r1B - r2B;
+        if (ownA) {
+          rnew[idA] = rvA;
+          rr += rvA * rvA;
+          if (mode == 1) x[idA] = xA + alpha * pA;
+          else bb += r1A * r1A;
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) accq[c] += gA[c] * rvA;
+        if (okB) {
+          if (ownB) {
+            rnew[idB] = rvB;
+            rr += rvB * rvB;
+            if (mode == 1) x[idB] = xB + alpha * pB;
+            else bb += r1B * r1B;
+          }
+#pragma unroll
+          for (int c = 0; c < NQ; ++c) accq[c] += gB[c] * rvB;
+        }
+        rec = recA2;
+        recB = recB2;
+      }
+    } else {
     for (; k < ke; k += PPW) {
       const int2 nrec = k + PPW < ke ? rrec[k + PPW] : rec;
       const int cell = rec.x, o = rec.y & 0x7fffffff;
@@ -483,6 +532,7 @@ __global__ void __launch_bounds__(RC_T) k_restrict_chunk(int mode, int nchunk, c
 #pragma unroll
       for (int c = 0; c < NQ; ++c) accq[c] += gv[c] * rv;
       rec = nrec;
+    }
     }
     double mine[NQ];
 #pragma unroll
@@ -856,6 +906,86 @@ __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int
   int g = blockIdx.x * PW + w;
   int c = g * CPW + lane / L;
   int4 rc = act && c < nc ? crec[c] : make_int4(0, 0, 0, 0);
+  // further pieces (non-nested cells) from prec, in piece order
+  auto extra = [&](const int4& q4, double v) -> double {
+    for (int t = 1; t < q4.z; ++t) {
+      const int2 pr = prec[q4.w + t];
+      const double* Go = G + ((size_t)pr.x * NP + a) * NQ;
+      const double* zj = z0 + (size_t)pr.y * NQ;
+      if constexpr (NQ % 2 == 0) {
+#pragma unroll
+        for (int b = 0; b < NQ; b += 2) {
+          const double2 g2 = __ldg(reinterpret_cast<const double2*>(Go + b));
+          v += g2.x * zj[b] + g2.y * zj[b + 1];
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < NQ; ++b) v += __ldg(Go + b) * zj[b];
+      }
+    }
+    return v;
+  };
+  if constexpr (NQ <= 3) {  // (NQ = 6: 128 registers, measured slower on config 4: 30 -> 40 us)
+    // two groups per trip, all first-piece loads of both issued before the first use (the kernel is
+    // latency-bound: one dependent round of loads per group), records two groups ahead
+    int cB = (g + gstep) * CPW + lane / L;
+    int4 rcB = act && g + gstep < ngroups && cB < nc ? crec[cB] : rc;
+    for (; g < ngroups; g += 2 * gstep) {
+      const int gA2 = g + 2 * gstep, gB2 = g + 3 * gstep;
+      const int cA2 = gA2 * CPW + lane / L, cB2 = gB2 * CPW + lane / L;
+      const int4 rcA2 = act && gA2 < ngroups && cA2 < nc ? crec[cA2] : rc;
+      const int4 rcB2 = act && gB2 < ngroups && cB2 < nc ? crec[cB2] : rc;
+      const bool okA = act && c < nc, okB = act && g + gstep < ngroups && cB < nc;
+      const size_t idA = (size_t)(okA ? c : 0) * NP + a, idB = (size_t)(okB ? cB : 0) * NP + a;
+      double vA = 0, vB = 0, rA = 0, rB = 0, gA[NQ], gB[NQ], zA[NQ], zB[NQ];
+      if (okA) {
+        vA = z[idA];
+        if (mode >= 1) rA = r[idA];
+        const double* Go = G + ((size_t)rc.x * NP + a) * NQ;
+        const double* zj = z0 + (size_t)rc.y * NQ;
+#pragma unroll
+        for (int b = 0; b < NQ; ++b) { gA[b] = __ldg(Go + b); zA[b] = zj[b]; }
+      }
+      if (okB) {
+        vB = z[idB];
+        if (mode >= 1) rB = r[idB];
+        const double* Go = G + ((size_t)rcB.x * NP + a) * NQ;
+        const double* zj = z0 + (size_t)rcB.y * NQ;
+#pragma unroll
+        for (int b = 0; b < NQ; ++b) { gB[b] = __ldg(Go + b); zB[b] = zj[b]; }
+      }
+      if (okA) {
+        if (rc.z > 0) {
+          if constexpr (NQ % 2 == 0) {
+#pragma unroll
+            for (int b = 0; b < NQ; b += 2) vA += gA[b] * zA[b] + gA[b + 1] * zA[b + 1];
+          } else {
+#pragma unroll
+            for (int b = 0; b < NQ; ++b) vA += gA[b] * zA[b];
+          }
+        }
+        if (rc.z > 1) vA = extra(rc, vA);
+        z[idA] = vA;
+        d += rA * vA;
+      }
+      if (okB) {
+        if (rcB.z > 0) {
+          if constexpr (NQ % 2 == 0) {
+#pragma unroll
+            for (int b = 0; b < NQ; b += 2) vB += gB[b] * zB[b] + gB[b + 1] * zB[b + 1];
+          } else {
+#pragma unroll
+            for (int b = 0; b < NQ; ++b) vB += gB[b] * zB[b];
+          }
+        }
+        if (rcB.z > 1) vB = extra(rcB, vB);
+        z[idB] = vB;
+        d += rB * vB;
+      }
+      rc = rcA2; c = cA2;
+      rcB = rcB2; cB = cB2;
+    }
+  } else {
   for (; g < ngroups; g += gstep) {
     const int gn = g + gstep, cn = gn * CPW + lane / L;
     const int4 rcn = act && gn < ngroups && cn < nc ? crec[cn] : rc;
@@ -864,11 +994,9 @@ __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int
       double v = z[id];
       const double rv = mode >= 1 ? r[id] : 0.0;
       // first piece from the cell record (o, J, n, k), further pieces (non-nested) from prec
-      for (int t = 0; t < rc.z; ++t) {
-        int o = rc.x, J = rc.y;
-        if (t > 0) { const int2 pr = prec[rc.w + t]; o = pr.x; J = pr.y; }
-        const double* Go = G + ((size_t)o * NP + a) * NQ;
-        const double* zj = z0 + (size_t)J * NQ;
+      if (rc.z > 0) {
+        const double* Go = G + ((size_t)rc.x * NP + a) * NQ;
+        const double* zj = z0 + (size_t)rc.y * NQ;
         if constexpr (NQ % 2 == 0) {
 #pragma unroll
           for (int b = 0; b < NQ; b += 2) {
@@ -880,11 +1008,13 @@ __global__ void __launch_bounds__(PW * 32) k_prolong(int mode, int nc, const int
           for (int b = 0; b < NQ; ++b) v += __ldg(Go + b) * zj[b];
         }
       }
+      if (rc.z > 1) v = extra(rc, v);
       z[id] = v;
       d += rv * v;
     }
     rc = rcn;
     c = cn;
+  }
   }
   if (mode == 0) return;
   d = warp_sum(d);
@@ -1252,8 +1382,11 @@ void launch_local_range(dgas_ctx ctx, int sb, int se, const double* r, double* z
 // kernel and the multi-RHS kernels keep the serial order. DGAS_FUSE_R=0 keeps the serial order everywhere.
 bool apply_fuses_restrict(dgas_ctx ctx) {
   static const bool no_fork = std::getenv("DGAS_NO_FORK") != nullptr;
-  static const int on = [] { const char* e = std::getenv("DGAS_FUSE_R"); return e ? std::atoi(e) : 1; }();
-  if (!on || no_fork || ctx->precond != 0 || ctx->max_sub_cells == 1) return false;
+  if (ctx->fuse_r < 0) {  // read once per context (the PCG graph is built with one choice)
+    const char* e = std::getenv("DGAS_FUSE_R");
+    ctx->fuse_r = e ? (std::atoi(e) != 0) : 1;
+  }
+  if (!ctx->fuse_r || no_fork || ctx->precond != 0 || ctx->max_sub_cells == 1) return false;
   return (ctx->local_kernel == 2 && !panel_is_narrow(ctx)) || ctx->local_kernel == 1 || ctx->local_kernel == 3;
 }
 
@@ -1306,6 +1439,18 @@ void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, doubl
                                             mode, ctx->nc, ctx->d_crec, ctx->d_prec, ctx->d_G,
                                             ctx->d_z0, z, ctx->d_rbuf, st, ctx->d_partials, ctx->d_beta, h,
                                             use_handle))));
+}
+
+// resident CTAs per SM of the persistent restriction / prolongation kernels (their grids are sized to one wave)
+int restrict_ctas_per_sm(dgas_ctx ctx) {
+  int n = 1;
+  DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_restrict_chunk<NP_, NQ_>, RC_T, 0))));
+  return std::max(1, n);
+}
+int prolong_ctas_per_sm(dgas_ctx ctx) {
+  int n = 1;
+  DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_prolong<NP_, NQ_>, PW * 32, 0))));
+  return std::max(1, n);
 }
 
 void launch_init_state(dgas_ctx ctx, PcgState* st, int maxit, double rtol, cudaStream_t s) {

@@ -386,30 +386,37 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
   const int WR = WC * NP;
   // cp.async of NP rows x G columns of cell c (src: r, or the y temporaries in z) into its window slot
   double* Qw = reinterpret_cast<double*>(sm + L.off_sc) + (size_t)w * SCW;
-  auto fetch = [&](const double* src, int c, bool withq) {
-    double* dst = Ww + (size_t)slt[c] * NP * BS;
-    double* dq = Qw + (size_t)(c % (PD + 1)) * NP * BS;
+  // cp.async of NP rows x G columns of cell c (src: r, or the y temporaries in z) into its window slot. The
+  // element (column gb, row i) a lane copies in round t is fixed: its source offset and window offset are
+  // computed once (no division or shuffle on the chain)
+  constexpr int FR = (NP * G + 31) / 32;
+  int64_t fsrc[FR];
+  int fdst[FR];
 #pragma unroll
-    for (int e0 = 0; e0 < NP * G; e0 += 32) {
-      const int e = e0 + lane;
-      const int gb = e / NP, i = e - gb * NP;
-      const int64_t mbb = __shfl_sync(0xffffffffu, mbase, gb & 31);  // lane gb (ks = 0) holds column gb's base
-      if (e < NP * G) {
-        cp_async8(dst + (size_t)i * BS + gb, src + mbb + (int64_t)c * NP + i);
-        if (withq) cp_async8(dq + (size_t)i * BS + gb, qvec + mbb + (int64_t)c * NP + i);
+  for (int t = 0; t < FR; ++t) {
+    const int e = t * 32 + lane;
+    const int gb = e / NP, i = e - gb * NP;
+    const int64_t mbb = __shfl_sync(0xffffffffu, mbase, gb & 31);  // lane gb (ks = 0) holds column gb's base
+    fsrc[t] = e < NP * G ? mbb + i : -1;
+    fdst[t] = i * BS + gb;
+  }
+  auto fetch = [&](const double* src, int c, bool withq) {
+    double* dst = Ww + slt[c] * (NP * BS);
+    double* dq = Qw + (c % (PD + 1)) * (NP * BS);
+#pragma unroll
+    for (int t = 0; t < FR; ++t)
+      if (fsrc[t] >= 0) {
+        cp_async8(dst + fdst[t], src + fsrc[t] + c * NP);
+        if (withq) cp_async8(dq + fdst[t], qvec + fsrc[t] + c * NP);
       }
-    }
   };
   // mode 3: r_c = r_old - alpha q on the entries this lane copied itself (landed: its own wait_group)
   auto combine = [&](int c) {
-    double* dst = Ww + (size_t)slt[c] * NP * BS;
-    const double* dq = Qw + (size_t)(c % (PD + 1)) * NP * BS;
+    double* dst = Ww + slt[c] * (NP * BS);
+    const double* dq = Qw + (c % (PD + 1)) * (NP * BS);
 #pragma unroll
-    for (int e0 = 0; e0 < NP * G; e0 += 32) {
-      const int e = e0 + lane;
-      const int gb = e / NP, i = e - gb * NP;
-      if (e < NP * G) dst[(size_t)i * BS + gb] = fma(-alpha, dq[(size_t)i * BS + gb], dst[(size_t)i * BS + gb]);
-    }
+    for (int t = 0; t < FR; ++t)
+      if (fsrc[t] >= 0) dst[fdst[t]] = fma(-alpha, dq[fdst[t]], dst[fdst[t]]);
   };
   for (int c = 0; c < PD; ++c) {
     if (c < m) fetch(r, c, fuse);
@@ -433,7 +440,7 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
 #pragma unroll
     for (int i = 0; i < NPAD; ++i) acc[i] = 0.0;
     for (int q = ks; q < NP; q += KS) {  // D column q (rows q..NP-1) times r_k[q]
-      const double rv = Ww[(size_t)(rk + q) * BS + g];
+      const double rv = Ww[(rk + q) * BS + g];
       const double* col = Ps + mr_dcol(NP, q) - q;
 #pragma unroll
       for (int i = 0; i < NP; ++i)
@@ -449,7 +456,7 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
         const int j = ok ? jj : 0;
         int row = rf + j;
         row -= row >= WR ? WR : 0;
-        const double wv = Ww[(size_t)row * BS + g];
+        const double wv = Ww[row * BS + g];
         yv[u] = ok ? wv : 0.0;
         col[u] = Ps + DPK + j * NP;
       }
@@ -502,7 +509,7 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
     for (int i = 0; i < RPL; ++i) {
       const int row = ks * RPL + i;
       if (row < NP) {
-        Ww[(size_t)(rk + row) * BS + g] = acc[i];
+        Ww[(rk + row) * BS + g] = acc[i];
         z[mbase + (int64_t)k * NP + row] = acc[i];  // y_k, read back by the backward sweep
       }
     }
@@ -531,7 +538,7 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
     const int f = fk[k], KU = (k - f) * NP, rk = slt[k] * NP, rf = slt[f] * NP;
     double uk[NP];
 #pragma unroll
-    for (int i = 0; i < NP; ++i) uk[i] = Ww[(size_t)(rk + i) * BS + g];
+    for (int i = 0; i < NP; ++i) uk[i] = Ww[(rk + i) * BS + g];
     for (int q = ks; q < NP; q += KS) {  // z_k[q] = (D_k^T u_k)[q]
       const double* col = Ps + mr_dcol(NP, q) - q;
       double v = 0;
@@ -552,7 +559,7 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_w(int mode, int nbatch, c
         const int j = ok[u] ? jj : 0;
         int row = rf + j;
         row -= row >= WR ? WR : 0;
-        wp[u] = Ww + (size_t)row * BS + g;
+        wp[u] = Ww + row * BS + g;
         wv[u] = *wp[u];
         col[u] = Ps + DPK + j * NP;
         v0[u] = 0;

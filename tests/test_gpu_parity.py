@@ -541,6 +541,34 @@ def test_pupdate_split_is_bitwise_identical(monkeypatch, name):
     assert np.array_equal(x0, x1) and np.array_equal(a0, a1)
 
 
+@pytest.mark.parametrize("name,env", [
+    ("cfg1", {}),                          # explicit inverses (k_local_inv)
+    ("cfg2", {"DGAS_LOCAL_INV": "0"}),     # wide panel kernel
+    ("cfg5s_p3q1", {}),                    # wide panel kernel, non-nested pieces
+    ("cfg5s_p6q1", {}),                    # envelope kernel (n_p = 28)
+    ("cfg4s", {"DGAS_LOCAL_KERNEL": "1"}),  # envelope kernel with rho jumps and the ND coarse path
+])
+def test_fused_residual_is_bitwise_identical(monkeypatch, name, env):
+    """DESIGN.md §6 item 19: with the residual update fused into the local solve (mode 3) the restriction
+    runs beside the local solves; both kernels form r = fma(-alpha, q, r_old), so PCG with and without the
+    fusion gives the same iterations, K, alphas and x bit for bit."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = CASES[name]()
+    b = _dev(g.normal(21, P.N))
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("DGAS_FUSE_R", v)
+        S = _solver(P)
+        x, it, c, st = S.pcg(b, rtol=1e-8)
+        a, bet = S.history()
+        out.append((x.cpu().numpy(), it, c, st, a))
+        S.close()
+    (x0, i0, c0, s0, a0), (x1, i1, c1, s1, a1) = out
+    assert s0 == s1 == 0 and i0 == i1 and c0 == c1
+    assert np.array_equal(a0, a1) and np.array_equal(x0, x1)
+
+
 def test_nd_two_contexts_smem_limit(monkeypatch):
     """the ND kernels' dynamic shared-memory limit is a per-function attribute; a second
     context with smaller fronts must not break the first one's launches (or its PCG graph)."""
