@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(ND_T) k_nd_fwd2(const NdItem* __restrict__ ite
   if (!waited) pdl_wait();
 }
 
-__global__ void __launch_bounds__(ND_T) k_nd_bwd2(const NdItem* __restrict__ items, int nwork, const int* __restrict__ gF,
+__global__ void __launch_bounds__(ND_T, 6) k_nd_bwd2(const NdItem* __restrict__ items, int nwork, const int* __restrict__ gF,
                                                   const int* __restrict__ gU, const double* __restrict__ Xg,
                                                   const double* __restrict__ MTg, const double* __restrict__ dsc,
                                                   const double* Tg, double* z0, const PcgState* st, int mode, int keep) {
