@@ -22,3 +22,12 @@ if [ -z "$SKIP_NCU" ]; then
   timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_local_mrhs_w|k_spmv_cls|k_restrict_chunk|k_prolong" -s 4 -c 4 -o gpurun_out/prof_default -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --kernel-reps 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc $?" >> $L
 fi
 cat $L
+# config 2 launch list (its setup builds the explicit inverses with ~1,200 launches: skip past them)
+if [ -z "$SKIP_NCU" ]; then
+  DGAS_EAGER=1 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s ${NCU_SKIP2:-2200} -c 60 --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_cfg2.log 2>&1; echo "ncu cfg2 launches rc $?" >> $L
+fi
+for c in cfg3 cfg4; do
+  DGAS_EAGER=1 DGAS_EAGER_TIMING=1 timeout 600 python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --kernel-reps 2 > gpurun_out/eager_$c.log 2> gpurun_out/eager_$c.err
+  echo "in-situ $c: $(grep -h 'eager timing' gpurun_out/eager_$c.err | tail -1)" >> $L
+done
+tail -4 $L
