@@ -20,10 +20,13 @@ LIB = os.path.join(ROOT, "paper_1903_11357_b200", "libdgas.so")
 # kernel-name regexes (demangled) -> where they run
 HOT = [
     (r"k_spmv_ring<15>", "I1 SpMV, config 4 (byte ring)"),
-    (r"k_spmv_cls<10>", "I1 SpMV, config 3 (class-sorted, de-duplicated A)"),
+    (r"k_spmv_cls<10, 2>", "I1 SpMV, config 3 (class-sorted, de-duplicated A, 2 CTAs/SM)"),
     (r"k_spmv_ring<28>", "I1 SpMV, config 5 p=6"),
-    (r"k_local_mrhs<10>", "I5 local solves, config 3 (multi-RHS over shared factors)"),
-    (r"k_local_panel<15, (true|false), double>", "I5 local solves, config 4 (merged panels)"),
+    (r"k_local_mrhs_w<10, 2>", "I5 local solves, config 3 (multi-RHS warp chains, default)"),
+    (r"k_local_mrhs_r<10>", "I5 local solves, multi-RHS, row lanes forward (variant)"),
+    (r"k_local_mrhs<10>", "I5 local solves, multi-RHS, CTA-wide steps (variant)"),
+    (r"k_local_panel<15, true, double, false>", "I5 local solves, config 4 (merged panels, narrow CTAs)"),
+    (r"k_local_panel<10, false, double, true>", "I5 local solves, config 5 p = 3 (merged panels, wide CTAs, fused residual)"),
     (r"k_local_warp<10>", "I5 local solves, warp per subdomain"),
     (r"k_local_inv\(", "I5 local solves, explicit inverses (configs 1, 2, 5 p1)"),
     (r"k_local<28>", "I5 local solves, envelope kernel (p >= 5)"),
