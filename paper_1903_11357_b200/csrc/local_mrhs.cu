@@ -730,24 +730,28 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_r(int mode, int nbatch, c
         if (c & 1) a1 += t * wr[c];
         else a0 += t * wr[c];
       }
-      // -U_k y_old: window rows rf .. rf + KU - 1, wrapping at WR (two contiguous segments)
-      const double* pc = Ps + DPK + i;
-      const int n1 = min(KU, WR - rf);
-      const double* wv = Wg + rf;
-      int j = 0;
-      for (; j + 3 < n1; j += 4) {
-        const double p0 = pc[j * NP], p1 = pc[(j + 1) * NP], p2 = pc[(j + 2) * NP], p3 = pc[(j + 3) * NP];
-        const double w0 = wv[j], w1 = wv[j + 1], w2 = wv[j + 2], w3 = wv[j + 3];
-        a0 += p0 * w0; a1 += p1 * w1; a2 += p2 * w2; a3 += p3 * w3;
+      // -U_k y_old, one cell (NP columns) per trip: its NP panel values and NP window values are all loaded
+      // before the first product (no remainder: the column count is a multiple of NP; the window wraps at a
+      // cell boundary)
+      const double* pc = Ps + DPK + i;  // column j at pc[j NP]
+      int slot = rf;
+#pragma unroll 2
+      for (int c = f; c < k; ++c) {
+        const double* wv = Wg + slot;
+        double pv[NP], wq[NP];
+#pragma unroll
+        for (int t = 0; t < NP; ++t) { pv[t] = pc[t * NP]; wq[t] = wv[t]; }
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+          if ((t & 3) == 0) a0 += pv[t] * wq[t];
+          else if ((t & 3) == 1) a1 += pv[t] * wq[t];
+          else if ((t & 3) == 2) a2 += pv[t] * wq[t];
+          else a3 += pv[t] * wq[t];
+        }
+        pc += NP * NP;
+        slot += NP;
+        slot -= slot >= WR ? WR : 0;
       }
-      for (; j < n1; ++j) a0 += pc[j * NP] * wv[j];
-      wv = Wg - n1;  // second segment: window rows 0 .. KU - n1 - 1 for j = n1 ..
-      for (; j + 3 < KU; j += 4) {
-        const double p0 = pc[j * NP], p1 = pc[(j + 1) * NP], p2 = pc[(j + 2) * NP], p3 = pc[(j + 3) * NP];
-        const double w0 = wv[j], w1 = wv[j + 1], w2 = wv[j + 2], w3 = wv[j + 3];
-        a0 += p0 * w0; a1 += p1 * w1; a2 += p2 * w2; a3 += p3 * w3;
-      }
-      for (; j < KU; ++j) a0 += pc[j * NP] * wv[j];
     }
     const double yk = (a0 + a1) + (a2 + a3);
     __syncwarp();  // every lane is done with the ring slot and with the window rows it read
@@ -923,7 +927,7 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
   if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;
   // 3: warp chains with row lanes forward (k_local_mrhs_r), 2: warp chains with K-slice lanes
   // (k_local_mrhs_w), 1: CTA-wide steps (k_local_mrhs)
-  int kern = 2;  // config 3: kernel 2 local 0.187 ms / 2358 PCG it/s, kernel 3 0.213-0.263 ms / 2194 (fewer
+  int kern = 2;  // config 3: kernel 2 local 0.187 ms / 2469 PCG it/s, kernel 3 0.210 ms / 2320 (fewer
                  // instructions, but its sequential forward dot product is latency-bound)
   if (const char* e = std::getenv("DGAS_MR_KERNEL")) kern = std::max(1, std::min(3, std::atoi(e)));
   if (kern >= 2) {
