@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(SR_NW * 32, MINB) k_spmv_cls(
   constexpr int NTT = SR_NW * 32;
   __shared__ double red[NTT / 32];
   __shared__ double wdot[NTT / 32];
-  __shared__ double xs_all[SR_NW * XS];
+  __shared__ double xs_all[SR_NW * CLS_DEPTH * XS];  // per warp: the gathered values of D cells
   int it = 0;
   double beta = 0;
   const double* pold = nullptr;
@@ -436,8 +436,8 @@ __global__ void __launch_bounds__(SR_NW * 32, MINB) k_spmv_cls(
     if (mode == 3) x = pnew;
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double* xs = xs_all + w * XS;
-  for (int t = lane; t < XS; t += 32) xs[t] = 0.0;
+  double* xs = xs_all + w * (CLS_DEPTH * XS);
+  for (int t = lane; t < CLS_DEPTH * XS; t += 32) xs[t] = 0.0;
   auto colval = [&](int64_t id) -> double {
     return mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
   };
@@ -485,46 +485,65 @@ __global__ void __launch_bounds__(SR_NW * 32, MINB) k_spmv_cls(
       idr[d] = ids(d + D);
       cB[d] = cid(d + D);
     }
+    // D cells per trip: their gathered values go to D shared-memory buffers behind ONE pair of warp barriers,
+    // the gathers of the next D cells are issued, then the D products run as independent chains (the kernel is
+    // latency-bound: ncu 0.32 issue slots per cycle with one cell at a time)
     for (int i0 = 0; i0 < n; i0 += D) {
+      int cc[D];
+      __syncwarp();  // the previous trip's reads of xs are done
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        cc[d] = cA[d];
+        if (i0 + d < n) {
+#pragma unroll
+          for (int t = 0; t < E; ++t) xs[d * XS + lane + 32 * t] = v[d][t];
+        }
+      }
+      __syncwarp();
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const int i = i0 + d;
-        if (i < n) {  // warp-uniform
-          const int c = cA[d];
-          __syncwarp();
+        gather(idr[d], i + D < n, v[d]);  // cell i + D
+        cA[d] = cB[d];
+        idr[d] = ids(i + 2 * D);
+        cB[d] = cid(i + 2 * D);
+      }
+      double pn[D], tot[D];
 #pragma unroll
-          for (int t = 0; t < E; ++t) xs[lane + 32 * t] = v[d][t];
-          __syncwarp();
-          gather(idr[d], i + D < n, v[d]);  // cell i + D
-          cA[d] = cB[d];
-          idr[d] = ids(i + 2 * D);
-          cB[d] = cid(i + 2 * D);
-          double pn = 0;
-          if (pcg && h == 0 && lane < NP) {
-            const size_t id = (size_t)c * NP + a;
-            pn = mode == 3 ? x[id] : it > 0 ? z[id] + beta * pold[id] : z[id];
-          }
-          double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      for (int d = 0; d < D; ++d) {
+        pn[d] = 0;
+        if (pcg && h == 0 && lane < NP && i0 + d < n) {
+          const size_t id = (size_t)cc[d] * NP + a;
+          pn[d] = mode == 3 ? x[id] : it > 0 ? z[id] + beta * pold[id] : z[id];
+        }
+      }
 #pragma unroll
-          for (int t = 0; t + 3 < MAXC; t += 4) {
-            s0 += Ar[t] * xs[h + LPR * t];
-            s1 += Ar[t + 1] * xs[h + LPR * (t + 1)];
-            s2 += Ar[t + 2] * xs[h + LPR * (t + 2)];
-            s3 += Ar[t + 3] * xs[h + LPR * (t + 3)];
-          }
+      for (int d = 0; d < D; ++d) {
+        const double* xd = xs + d * XS;
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
 #pragma unroll
-          for (int t = MAXC / 4 * 4; t < MAXC; ++t) s0 += Ar[t] * xs[h + LPR * t];
-          const double vv = (s0 + s1) + (s2 + s3);
-          double tot = vv;
+        for (int t = 0; t + 3 < MAXC; t += 4) {
+          s0 += Ar[t] * xd[h + LPR * t];
+          s1 += Ar[t + 1] * xd[h + LPR * (t + 1)];
+          s2 += Ar[t + 2] * xd[h + LPR * (t + 2)];
+          s3 += Ar[t + 3] * xd[h + LPR * (t + 3)];
+        }
 #pragma unroll
-          for (int h2 = 1; h2 < LPR; ++h2) tot += __shfl_sync(0xffffffffu, vv, (a + NP * h2) & 31);
-          if (h == 0 && lane < NP) {
-            const size_t id = (size_t)c * NP + a;
-            y[id] = tot;
-            if (pcg) {
-              if (mode == 1) pnew[id] = pn;
-              mydot += pn * tot;
-            }
+        for (int t = MAXC / 4 * 4; t < MAXC; ++t) s0 += Ar[t] * xd[h + LPR * t];
+        tot[d] = (s0 + s1) + (s2 + s3);
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const double vv = tot[d];
+        double tsum = vv;
+#pragma unroll
+        for (int h2 = 1; h2 < LPR; ++h2) tsum += __shfl_sync(0xffffffffu, vv, (a + NP * h2) & 31);
+        if (h == 0 && lane < NP && i0 + d < n) {
+          const size_t id = (size_t)cc[d] * NP + a;
+          y[id] = tsum;
+          if (pcg) {
+            if (mode == 1) pnew[id] = pn[d];
+            mydot += pn[d] * tsum;
           }
         }
       }
@@ -672,7 +691,7 @@ void launch_spmv_range(dgas_ctx ctx, int cb, int ce, const double* x, double* y,
 }
 
 // Host: class-sorted work items for k_spmv_cls (dd[c] = compact offset of cell c's row-block). Cells of a
-// class in ascending order, cut into runs of about nc / (6 x grid warps) cells. Off for p > 4 (register
+// class in ascending order, cut into runs of about nc / (5 x grid warps) cells. Off for p > 4 (register
 // row-blocks) or cells with more than CLS_MAXDEG neighbours; DGAS_SPMV_CLS=0 disables it.
 int spmv_cls_setup(dgas_ctx ctx, const std::vector<int64_t>& dd) {
   int on = 1;
@@ -697,7 +716,10 @@ int spmv_cls_setup(dgas_ctx ctx, const std::vector<int64_t>& dd) {
   const int grid = std::min(cps * nsm, std::max(1, nc / SR_NW));
   std::map<int64_t, std::vector<int>> cls;
   for (int c = 0; c < nc; ++c) cls[dd[c]].push_back(c);
-  int run = std::max(4, (int)(nc / (6LL * grid * SR_NW)));  // config 3: runs of 18 (16: 87 us, 27: 96, 55: 104, 110: 121)
+  // runs of about nc / (5 x grid warps) cells, a multiple of the D cells a trip processes (config 3: 24 cells,
+  // 0.077 ms; 12: 0.084, 18: 0.087, 36: 0.083)
+  int run = (int)(nc / (5LL * grid * SR_NW));
+  run = std::max(CLS_DEPTH, (run + CLS_DEPTH - 1) / CLS_DEPTH * CLS_DEPTH);
   if (const char* e = std::getenv("DGAS_CLS_RUN")) run = std::max(1, std::atoi(e));
   std::vector<int4> items;
   std::vector<int64_t> off;
