@@ -133,6 +133,54 @@ int dedup_setup(dgas_ctx ctx) {
       if ((st = mrhs_setup(ctx, rep_of))) return st;  // batched solves over the shared factors
     }
   }
+  // ---------------- restriction / prolongation blocks G (one np x nq block per overlap piece): nested
+  // Cartesian tilings repeat them. The iteration kernels get a compact store and copies of the piece
+  // records that index its distinct blocks (same bits, same order of operations); the originals stay
+  // for the sharded solve, which addresses G by piece.
+  {
+    int gon = 1;
+    if (const char* e = std::getenv("DGAS_DEDUP_G")) gon = std::atoi(e) != 0;
+    const int nov = ctx->nov;
+    const size_t blk = (size_t)ctx->np * ctx->nq;
+    if (gon && nov > 0) {
+      std::vector<double> G((size_t)nov * blk);
+      DGAS_CUDA(cudaMemcpy(G.data(), ctx->d_G, G.size() * 8, cudaMemcpyDeviceToHost));
+      std::unordered_map<uint64_t, std::vector<int>> rep;
+      std::vector<int> uidx(nov), reps;
+      for (int o = 0; o < nov; ++o) {
+        const uint64_t h = fnv_bytes(G.data() + (size_t)o * blk, blk * 8);
+        auto& lst = rep[h];
+        int found = -1;
+        for (int r : lst)
+          if (std::memcmp(G.data() + (size_t)r * blk, G.data() + (size_t)o * blk, blk * 8) == 0) { found = r; break; }
+        if (found < 0) { lst.push_back(o); uidx[o] = (int)reps.size(); reps.push_back(o); }
+        else uidx[o] = uidx[found];
+      }
+      if ((double)reps.size() < maxfrac * (double)nov) {
+        std::vector<double> Gc(reps.size() * blk);
+        for (size_t u = 0; u < reps.size(); ++u) std::memcpy(Gc.data() + u * blk, G.data() + (size_t)reps[u] * blk, blk * 8);
+        std::vector<int2> rrec(nov), prec(nov);
+        std::vector<int4> crec(nc);
+        DGAS_CUDA(cudaMemcpy(rrec.data(), ctx->d_rrec, (size_t)nov * sizeof(int2), cudaMemcpyDeviceToHost));
+        DGAS_CUDA(cudaMemcpy(prec.data(), ctx->d_prec, (size_t)nov * sizeof(int2), cudaMemcpyDeviceToHost));
+        DGAS_CUDA(cudaMemcpy(crec.data(), ctx->d_crec, (size_t)nc * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (int k = 0; k < nov; ++k) {
+          const int o = rrec[k].y & 0x7fffffff;
+          rrec[k].y = (rrec[k].y & (int)0x80000000u) | uidx[o];
+          prec[k].x = uidx[prec[k].x];
+        }
+        for (int c = 0; c < nc; ++c) crec[c].x = uidx[crec[c].x];
+        int st;
+        if ((st = dev_upload(ctx, &ctx->d_G_it, Gc)) || (st = dev_upload(ctx, &ctx->d_rrec_it, rrec)) ||
+            (st = dev_upload(ctx, &ctx->d_prec_it, prec)) || (st = dev_upload(ctx, &ctx->d_crec_it, crec)))
+          return st;
+        ctx->g_unique = (int64_t)reps.size();
+      }
+    }
+  }
+  if (std::getenv("DGAS_VERBOSE") && ctx->g_unique)
+    fprintf(stderr, "dgas: dedup: G %lld distinct blocks for %d pieces (%.2f MB stored)\n", (long long)ctx->g_unique,
+            ctx->nov, ctx->g_unique * ctx->np * ctx->nq * 8 / 1e6);
   if (std::getenv("DGAS_VERBOSE"))
     fprintf(stderr, "dgas: dedup: A %lld distinct row-blocks (%.1f MB stored), local factors %d distinct (%.1f MB)\n",
             (long long)ctx->a_unique, ctx->a_bytes_stored / 1e6, ctx->p_unique, ctx->p_bytes_stored / 1e6);

@@ -195,6 +195,13 @@ struct dgas_ctx_s {
   double* d_Cc = nullptr;         // [ncoarse][nq*nq]
   double* d_cbbox = nullptr;      // [ncoarse][4]
   double* d_G = nullptr;          // [nov][np*nq]
+  // iteration views of G and the piece records (launch_restrict / launch_prolong): the originals, or after
+  // exact de-duplication of G (dedup.cu) a compact store with records that index its distinct blocks
+  double* d_G_it = nullptr;
+  int2* d_rrec_it = nullptr;
+  int2* d_prec_it = nullptr;
+  int4* d_crec_it = nullptr;
+  int64_t g_unique = 0;
   double* d_A0t = nullptr;        // tile storage of A0 / its Cholesky factor
   double* d_Dinv0 = nullptr;      // [nT][CT*CT] inverse diagonal tiles
   double* d_W = nullptr;          // tile storage of L^-1 (dense only, scratch)

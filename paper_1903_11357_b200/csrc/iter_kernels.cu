@@ -1226,7 +1226,8 @@ int spmv_set_smem(dgas_ctx ctx, size_t smem) {
 void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cudaStream_t s) {
   if (ctx->d_chunks) {
     DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_restrict_chunk<NP_, NQ_><<<ctx->rc_grid, RC_T, 0, s>>>(
-                                              mode, ctx->nchunk, ctx->d_chunks, ctx->d_jchunk_ptr, ctx->d_rrec, ctx->d_G,
+                                              mode, ctx->nchunk, ctx->d_chunks, ctx->d_jchunk_ptr,
+                                              ctx->d_rrec_it ? ctx->d_rrec_it : ctx->d_rrec, ctx->d_G_it ? ctx->d_G_it : ctx->d_G,
                                               r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf, ctx->d_x, ctx->d_b, ctx->d_r0,
                                               ctx->d_cpart, ctx->d_jcnt2, st, ctx->d_partials))));
     return;
@@ -1234,7 +1235,9 @@ void launch_restrict(dgas_ctx ctx, int mode, PcgState* st, const double* r, cuda
   const int wpj = ctx->restrict_wpj, cpj = ctx->restrict_cpj;
   const int grid = cpj > 1 ? ctx->ncoarse * cpj : (ctx->ncoarse + (RT / 32 / wpj) - 1) / (RT / 32 / wpj);
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_restrict<NP_, NQ_><<<grid, RT, 0, s>>>(
-                                            mode, ctx->ncoarse, wpj, cpj, ctx->d_cov_ptr, ctx->d_rrec, ctx->d_G, r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf,
+                                            mode, ctx->ncoarse, wpj, cpj, ctx->d_cov_ptr,
+                                            ctx->d_rrec_it ? ctx->d_rrec_it : ctx->d_rrec,
+                                            ctx->d_G_it ? ctx->d_G_it : ctx->d_G, r, ctx->d_rbuf, ctx->d_q, ctx->d_pbuf,
                                             ctx->d_x, ctx->d_b, ctx->d_r0, ctx->d_rpart, ctx->d_jcnt, st,
                                             ctx->d_partials))));
 }
@@ -1436,7 +1439,9 @@ void launch_prolong(dgas_ctx ctx, int mode, PcgState* st, const double* r, doubl
   DISPATCH_P(ctx->p, (grid = (ctx->nc + PW * PackCfg<NP_>::PPW - 1) / (PW * PackCfg<NP_>::PPW)));
   grid = std::min<unsigned>(grid, (unsigned)ctx->prolong_grid);
   DISPATCH_P(ctx->p, DISPATCH_Q(ctx->q, (k_prolong<NP_, NQ_><<<grid, PW * 32, 0, s>>>(
-                                            mode, ctx->nc, ctx->d_crec, ctx->d_prec, ctx->d_G,
+                                            mode, ctx->nc, ctx->d_crec_it ? ctx->d_crec_it : ctx->d_crec,
+                                            ctx->d_prec_it ? ctx->d_prec_it : ctx->d_prec,
+                                            ctx->d_G_it ? ctx->d_G_it : ctx->d_G,
                                             ctx->d_z0, z, ctx->d_rbuf, st, ctx->d_partials, ctx->d_beta, h,
                                             use_handle))));
 }

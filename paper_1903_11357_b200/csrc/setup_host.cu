@@ -604,7 +604,8 @@ static void free_ctx(dgas_ctx ctx) {
   for (void* p2 : {(void*)ctx->d_prow, (void*)ctx->d_dsc0, (void*)ctx->d_rb0, (void*)ctx->d_zb0, (void*)ctx->d_inv_Z,
                    (void*)ctx->d_inv_zoff, (void*)ctx->d_inv_items, (void*)ctx->d_lw_pus, (void*)ctx->d_lw_units,
                    (void*)ctx->d_lw_cnt, (void*)ctx->d_a_dd, (void*)ctx->d_mr_batches, (void*)ctx->d_mr_members,
-                   (void*)ctx->d_cls_items, (void*)ctx->d_cls_off, (void*)ctx->d_cls_cells, (void*)ctx->d_cls_nb})
+                   (void*)ctx->d_cls_items, (void*)ctx->d_cls_off, (void*)ctx->d_cls_cells, (void*)ctx->d_cls_nb,
+                   (void*)ctx->d_G_it, (void*)ctx->d_rrec_it, (void*)ctx->d_prec_it, (void*)ctx->d_crec_it})
     if (p2) cudaFree(p2);
   nd_free(ctx);
   shard_free(ctx);
