@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(MR_T) k_local_mrhs(int mode, int nbatch, const
 }
 
 // ------------------------------------------------------------------------------------------------
-// k_local_mrhs_w — the same multi-RHS solve with INDEPENDENT WARP CHAINS (the default). ncu on k_local_mrhs
+// k_local_mrhs_w — the same multi-RHS solve with INDEPENDENT WARP CHAINS (DGAS_MR_KERNEL=2). ncu on k_local_mrhs
 // (config 3): ~2.4 us per chain step; stalls: shared-memory scoreboard 25%, CTA barrier 20%, fixed-latency
 // waits 24%; every step pays two CTA barriers and a cross-warp reduction through shared memory. Here the
 // right-hand sides of a batch are dealt to the warps, G per warp, and a warp never synchronises with the
@@ -861,6 +861,345 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_r(int mode, int nbatch, c
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// k_local_mrhs_t — the multi-RHS warp chains on the FP64 TENSOR CORES (mma.sync m8n8k4 f64; the default).
+// With many right-hand sides per factor the chain step IS a dense contraction: Y_k (NP x 8) = P_k (NP x K) .
+// W (K x 8) forward, and [z_k ; y_old] (K x 8) += P_k^T (K x NP) . U_k (NP x 8) backward, for the 8 columns a
+// warp owns. One DMMA does 8 x 8 x 4 = 256 FMAs and sums over k inside the instruction: no K-slicing across
+// lanes, no shuffle reduction, ~5x fewer instructions per right-hand side than k_local_mrhs_w (ncu there:
+// instruction-bound, 13% DFMA). Fragments (PTX ISA, m8n8k4 f64): lane l holds A[l / 4][l % 4], B[l % 4][l / 4],
+// C[l / 4][2 (l % 4) .. + 1]. The window is W_w[row][8] (8 columns, no padding): a B fragment reads 32
+// consecutive doubles, a C fragment is one 16-byte access per lane, both conflict-free.
+//   forward  : C(2 m-tiles of 8 rows x 8 columns) = sum over k-steps of 4 panel columns; the D triangle first
+//              (masked to its lower part), columns beyond the panel masked to zero in A and B.
+//   backward : B = u_k (NP x 8) loaded once (3 k-steps); z_k = D_k^T u_k (2 m-tiles), then per tile of 8 rows
+//              of y_old: C = y_old (16-byte loads), C += (-U_k^T) u_k, stored back.
+// Ring, producer warp, windows, cp.async prefetch and the y temporaries in z as in k_local_mrhs_w.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int NP>
+__global__ void __launch_bounds__(32 * 9) k_local_mrhs_t(int mode, int nbatch, const int4* __restrict__ batches,
+                                                         const int* __restrict__ members,
+                                                         const int* __restrict__ sub_ptr, const int* __restrict__ first,
+                                                         const int64_t* __restrict__ p_off, const double* __restrict__ P,
+                                                         const double* r_in, double* const* rbuf, double* z,
+                                                         const PcgState* st, int NW, int S, uint32_t slot_bytes, int WC,
+                                                         int max_cells) {
+  constexpr int DPK = mr_dpk<NP>(), G = 8, BS = 8, PD = MR_PD;
+  constexpr int MT = (NP + 7) / 8;  // m-tiles of the NP rows
+  constexpr int KT = (NP + 3) / 4;  // k-steps over NP
+  extern __shared__ __align__(128) unsigned char sm[];
+  const double* r = r_in;
+  if (mode >= 1) {
+    if (st->done) return;
+    r = mode == 1 ? rbuf[0] : rbuf[(st->it + 1) & 1];
+  }
+  const MrwLayout L(max_cells, NP, NW, BS, WC, S, slot_bytes, 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + 16;
+  int* fk = reinterpret_cast<int*>(sm + L.off_fk);
+  int* fm = reinterpret_cast<int*>(sm + L.off_fm);
+  int* slt = reinterpret_cast<int*>(sm + L.off_slt);
+  int64_t* po = reinterpret_cast<int64_t*>(sm + L.off_po);
+  unsigned char* ring = sm + L.off_ring;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int4 bt = batches[blockIdx.x];
+  const int rep = bt.x, moff = bt.y, B = bt.z;
+  const int s0 = sub_ptr[rep], m = sub_ptr[rep + 1] - s0, T2 = 2 * m;
+  const int nwact = (B + G - 1) / G;
+  for (int k = tid; k < m; k += blockDim.x) {
+    fk[k] = first[s0 + k];
+    po[k] = p_off[s0 + k];
+    slt[k] = (k % WC) * NP;  // first window row of cell k
+  }
+  if (tid == 0) {
+    for (int t = 0; t < S; ++t) { mbar_init(&full[t], 1); mbar_init(&empty[t], nwact); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int mn = 1 << 30;
+    for (int k = m - 1; k >= 0; --k) { mn = min(mn, fk[k]); fm[k] = mn; }
+  }
+  // the ring is read up to 6 doubles past a panel (rows 10..15 of a fragment) and the window holds padding
+  // rows: start from finite data
+  for (int e = tid; e < (int)((size_t)S * slot_bytes / 8); e += blockDim.x) reinterpret_cast<double*>(ring)[e] = 0.0;
+  __syncthreads();
+  const int SM1 = S - 1;
+  if (w == NW) {
+    if (lane != 0) return;
+    fence_proxy_async();  // the zero fill (generic proxy) before the bulk copies (async proxy) into the ring
+    const uint64_t pol = l2_evict_last();
+    for (int t = 0; t < T2; ++t) {
+      const int sl = t & SM1;
+      if (t >= S) mbar_wait_backoff(&empty[sl], (uint32_t)(((t / S) - 1) & 1));
+      const int k = t < m ? t : T2 - 1 - t;
+      const int n = DPK + (k - fk[k]) * NP * NP;
+      bulk_load(ring + (size_t)sl * slot_bytes, P + po[k], (uint32_t)(((n + 1) & ~1) * 8), &full[sl], pol);
+    }
+    return;
+  }
+  if (w >= nwact) return;
+  // ---------------- consumer warp w: columns 8 w .. 8 w + 7 of the batch
+  const int cnt = min(G, B - w * G);
+  const int lr = lane >> 2, lk = lane & 3;  // fragment row / k index of this lane
+  bool rowok[MT], kok[KT];                  // lane-constant masks: fragment row 8 t + lr / k index 4 kt + lk < NP
+#pragma unroll
+  for (int t = 0; t < MT; ++t) rowok[t] = 8 * t + lr < NP;
+#pragma unroll
+  for (int kt = 0; kt < KT; ++kt) kok[kt] = 4 * kt + lk < NP;
+  const int gcol = lane & 7;                // lanes 0..7 (and their mirrors) hold column gcol's base
+  const int64_t mbase = (int64_t)sub_ptr[members[moff + w * G + min(gcol, cnt - 1)]] * NP;
+  const int64_t mb0 = __shfl_sync(0xffffffffu, mbase, 2 * lk), mb1 = __shfl_sync(0xffffffffu, mbase, 2 * lk + 1);
+  double* Ww = reinterpret_cast<double*>(sm + L.off_W) + (size_t)w * WC * NP * BS;
+  const int WR = WC * NP;
+  for (int e = lane; e < WR * BS; e += 32) Ww[e] = 0.0;
+  constexpr int FR = (NP * G + 31) / 32;
+  int64_t fsrc[FR];
+  int fdst[FR];
+#pragma unroll
+  for (int t = 0; t < FR; ++t) {
+    const int e = t * 32 + lane;
+    const int gb = e / NP, i = e - gb * NP;
+    const int64_t mbb = __shfl_sync(0xffffffffu, mbase, gb & 7);
+    fsrc[t] = e < NP * G ? mbb + i : -1;
+    fdst[t] = i * BS + gb;
+  }
+  auto fetch = [&](const double* src, int c) {
+    double* dst = Ww + slt[c] * BS;
+#pragma unroll
+    for (int t = 0; t < FR; ++t)
+      if (fsrc[t] >= 0) cp_async8(dst + fdst[t], src + fsrc[t] + c * NP);
+  };
+  __syncwarp();
+  for (int c = 0; c < PD; ++c) {
+    if (c < m) fetch(r, c);
+    cp_async_commit();
+  }
+  cp_async_wait<PD - 1>();
+  __syncwarp();
+  // ------------------------------------------------ forward sweep
+  for (int k = 0; k < m; ++k) {
+    const int sl = k & SM1;
+    mbar_wait(&full[sl], (uint32_t)((k / S) & 1));
+    const double* __restrict__ Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+    const int f = fk[k], KU = (k - f) * NP, rk = slt[k], rf = slt[f];
+    double c0[MT], c1[MT];
+#pragma unroll
+    for (int t = 0; t < MT; ++t) { c0[t] = 0.0; c1[t] = 0.0; }
+    // D_k r_k: k-steps over the NP columns of the packed lower triangle
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const int c = 4 * kt + lk;
+      const bool cv = c < NP;
+      const int cc = cv ? c : 0;
+      const double bv = cv ? Ww[(rk + cc) * BS + lr] : 0.0;
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const int row = 8 * t + lr;
+        const bool av = cv && row < NP && row >= c;
+        const double a = av ? Ps[mr_dcol(NP, cc) + (av ? row - cc : 0)] : 0.0;
+        dmma884(c0[t], c1[t], a, bv);
+      }
+    }
+    // -U_k y_old: k-steps of 4 panel columns (window rows wrap at WR), UK k-steps per trip with all fragment
+    // loads first and one accumulator set per k-step of the trip (independent DMMA chains: with ~1 warp per
+    // scheduler the chain latency is what the step costs)
+    constexpr int UK = 4;
+    double ca[UK][MT][2];
+#pragma unroll
+    for (int u = 0; u < UK; ++u)
+#pragma unroll
+      for (int t = 0; t < MT; ++t) { ca[u][t][0] = 0.0; ca[u][t][1] = 0.0; }
+    {
+      // full trips (16 columns, no column masks): lane-constant fragment pointers advanced per trip
+      const double* pA = Ps + DPK + lk * NP + lr;  // A[row lr (+ 8 t)][column lk] of the trip's first k-step
+      int wrow = rf + lk;                          // window row of that column, kept in [0, WR)
+      wrow -= wrow >= WR ? WR : 0;
+      int j0 = 0;
+      for (; j0 + 4 * UK <= KU; j0 += 4 * UK) {
+        double av[UK][MT], bv[UK];
+#pragma unroll
+        for (int u = 0; u < UK; ++u) {
+          int row = wrow + 4 * u;
+          row -= row >= WR ? WR : 0;
+          bv[u] = Ww[row * BS + lr];
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            const double pv = pA[4 * u * NP + 8 * t];  // rows beyond NP: masked below (reads stay inside the ring + its 128-byte pad)
+            av[u][t] = rowok[t] ? pv : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UK; ++u)
+#pragma unroll
+          for (int t = 0; t < MT; ++t) dmma884(ca[u][t][0], ca[u][t][1], av[u][t], bv[u]);
+        pA += 4 * UK * NP;
+        wrow += 4 * UK;
+        wrow -= wrow >= WR ? WR : 0;
+      }
+      if (j0 < KU) {  // last, partial trip: columns beyond the panel masked to zero in A and B
+        double av[UK][MT], bv[UK];
+#pragma unroll
+        for (int u = 0; u < UK; ++u) {
+          const bool jv = j0 + 4 * u + lk < KU;
+          int row = wrow + 4 * u;
+          row -= row >= WR ? WR : 0;
+          const double wv = Ww[(jv ? row : 0) * BS + lr];
+          bv[u] = jv ? wv : 0.0;
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            const bool ok = jv && rowok[t];
+            const double pv = pA[ok ? 4 * u * NP + 8 * t : 0];
+            av[u][t] = ok ? pv : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UK; ++u)
+#pragma unroll
+          for (int t = 0; t < MT; ++t) dmma884(ca[u][t][0], ca[u][t][1], av[u][t], bv[u]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      c0[t] += (ca[0][t][0] + ca[1][t][0]) + (ca[2][t][0] + ca[3][t][0]);
+      c1[t] += (ca[0][t][1] + ca[1][t][1]) + (ca[2][t][1] + ca[3][t][1]);
+    }
+    __syncwarp();  // every lane is done with the ring slot and with the window rows it read
+    if (lane == 0) mbar_arrive(&empty[sl]);
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      const int row = 8 * t + lr;
+      if (row < NP) {
+        *reinterpret_cast<double2*>(Ww + (rk + row) * BS + 2 * lk) = make_double2(c0[t], c1[t]);
+        z[mb0 + (int64_t)k * NP + row] = c0[t];  // y_k, read back by the backward sweep
+        z[mb1 + (int64_t)k * NP + row] = c1[t];
+      }
+    }
+    if (k + PD < m) fetch(r, k + PD);
+    cp_async_commit();
+    cp_async_wait<PD - 1>();
+    __syncwarp();
+  }
+  // ------------------------------------------------ backward sweep
+  int lo = max(0, m - WC);
+  for (int kk = m - 1; kk >= max(0, m - PD); --kk) {
+    if (fm[kk] < lo) {
+      for (int c = fm[kk]; c < lo; ++c) fetch(z, c);
+      lo = fm[kk];
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<PD - 1>();
+  __syncwarp();
+  for (int k = m - 1; k >= 0; --k) {
+    const int t2 = T2 - 1 - k, sl = t2 & SM1;
+    mbar_wait(&full[sl], (uint32_t)((t2 / S) & 1));
+    const double* __restrict__ Ps = reinterpret_cast<const double*>(ring + (size_t)sl * slot_bytes);
+    const int f = fk[k], KU = (k - f) * NP, rk = slt[k], rf = slt[f];
+    double bu[KT];  // B fragments of u_k (NP x 8)
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const int i = 4 * kt + lk;
+      const double wv = Ww[(rk + (i < NP ? i : 0)) * BS + lr];
+      bu[kt] = i < NP ? wv : 0.0;
+    }
+    // z_k = D_k^T u_k: row q, k-dimension i >= q (column q of D_k holds rows q..NP-1)
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      const int q = 8 * t + lr;
+      double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const int i = 4 * kt + lk;
+        const bool av = q < NP && i < NP && i >= q;
+        const double a = av ? Ps[mr_dcol(NP, av ? q : 0) + (av ? i - q : 0)] : 0.0;
+        dmma884(z0, z1, a, bu[kt]);
+      }
+      if (q < NP) {
+        z[mb0 + (int64_t)k * NP + q] = z0;
+        z[mb1 + (int64_t)k * NP + q] = z1;
+      }
+    }
+    // y_old += (-U_k^T) u_k, tiles of 8 rows of y_old, UT independent tiles per trip (loads first)
+    constexpr int UT = 3;
+    {
+      const double* pB = Ps + DPK + lr * NP + lk;  // A[row j = lr (+ 8 u)][i = lk (+ 4 kt)] = (-U_k)[i][j]
+      int wrow = rf + lr;                          // window row of y_old row lr, kept in [0, WR)
+      wrow -= wrow >= WR ? WR : 0;
+      int jt = 0;
+      for (; jt + 8 * UT <= KU; jt += 8 * UT) {  // full trips: no row masks
+        double2* wp[UT];
+        double2 cv[UT];
+        double av[UT][KT];
+#pragma unroll
+        for (int u = 0; u < UT; ++u) {
+          int row = wrow + 8 * u;
+          row -= row >= WR ? WR : 0;
+          wp[u] = reinterpret_cast<double2*>(Ww + row * BS + 2 * lk);
+          cv[u] = *wp[u];
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            const double pv = pB[8 * u * NP + (kok[kt] ? 4 * kt : 0)];
+            av[u][kt] = kok[kt] ? pv : 0.0;
+          }
+        }
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+          for (int u = 0; u < UT; ++u) dmma884(cv[u].x, cv[u].y, av[u][kt], bu[kt]);
+#pragma unroll
+        for (int u = 0; u < UT; ++u) *wp[u] = cv[u];
+        pB += 8 * UT * NP;
+        wrow += 8 * UT;
+        wrow -= wrow >= WR ? WR : 0;
+        wrow -= wrow >= WR ? WR : 0;
+      }
+      if (jt < KU) {  // last, partial trip
+        double2* wp[UT];
+        double2 cv[UT];
+        double av[UT][KT];
+        bool jv[UT];
+#pragma unroll
+        for (int u = 0; u < UT; ++u) {
+          jv[u] = jt + 8 * u + lr < KU;
+          int row = wrow + 8 * u;
+          row -= row >= WR ? WR : 0;
+          wp[u] = reinterpret_cast<double2*>(Ww + (jv[u] ? row : 0) * BS + 2 * lk);
+          cv[u] = *wp[u];
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            const bool ok = jv[u] && kok[kt];
+            const double pv = pB[ok ? 8 * u * NP + 4 * kt : 0];
+            av[u][kt] = ok ? pv : 0.0;
+          }
+        }
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+          for (int u = 0; u < UT; ++u) dmma884(cv[u].x, cv[u].y, av[u][kt], bu[kt]);
+#pragma unroll
+        for (int u = 0; u < UT; ++u)
+          if (jv[u]) *wp[u] = cv[u];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sl]);
+    const int k2 = k - PD;
+    if (k2 >= 0 && fm[k2] < lo) {
+      for (int c = fm[k2]; c < lo; ++c) fetch(z, c);
+      lo = fm[k2];
+    }
+    cp_async_commit();
+    cp_async_wait<PD - 1>();
+    __syncwarp();
+  }
+}
+
 #define DISPATCH_MR(P, ...)                                 \
   switch (P) {                                              \
     case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
@@ -927,9 +1266,11 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
   if (ctx->coarse_mode == 2) reserve += (size_t)std::max(ctx->nd.maxN, ctx->nd.maxF + ctx->nd.maxU) * 8 + 1024;
   // 3: warp chains with row lanes forward (k_local_mrhs_r), 2: warp chains with K-slice lanes
   // (k_local_mrhs_w), 1: CTA-wide steps (k_local_mrhs)
-  int kern = 2;  // config 3: kernel 2 local 0.187 ms / 2469 PCG it/s, kernel 3 0.210 ms / 2320 (fewer
-                 // instructions, but its sequential forward dot product is latency-bound)
-  if (const char* e = std::getenv("DGAS_MR_KERNEL")) kern = std::max(1, std::min(3, std::atoi(e)));
+  // config 3 (PCG it/s with everything else equal): kernel 4 (FP64 tensor cores, 2 warps x 8 columns) local
+  // 0.160 ms / 2989; kernel 2 0.187 ms / 2750; kernel 3 0.210 ms (fewer instructions than 2, but its
+  // sequential forward dot product is latency-bound)
+  int kern = 4;
+  if (const char* e = std::getenv("DGAS_MR_KERNEL")) kern = std::max(1, std::min(4, std::atoi(e)));
   if (kern >= 2) {
     // config 3 sweep (PCG it/s): 8 warps x 2 columns 2028, 4 x 4 1751, 4 x 8 1758, 8 x 4 1756, 4 x 2 1750
     int G = 2, NW = 8;
@@ -938,9 +1279,14 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
     if (const char* e = std::getenv("DGAS_MR_NW")) NW = std::max(1, std::min(8, std::atoi(e)));
     if (G != 2 && G != 4 && G != 8 && G != 16 && G != 32) G = 2;
     if (kern == 3) G = 32 / np;  // one lane per (column, row)
+    if (kern == 4) {             // tensor-core chains: 8 columns per warp (the n of m8n8k4)
+      G = 8;
+      if (!std::getenv("DGAS_MR_NW")) NW = 2;  // config 3: 2 warps 2989, 4 warps 2870, 8 warps 2915 PCG it/s
+    }
     if (S > 16) S = 16;
-    const int B = G * NW, BSw = G | 1;
-    const size_t need = kern == 3 ? MrrLayout(mc, np, NW, G, WC, S, slot).total
+    const int B = G * NW, BSw = kern == 4 ? 8 : (G | 1);
+    const size_t need = kern == 4 ? MrwLayout(mc, np, NW, BSw, WC, S, slot, 0).total + 128 :
+                        kern == 3 ? MrrLayout(mc, np, NW, G, WC, S, slot).total
                                   : MrwLayout(mc, np, NW, BSw, WC, S, slot, 0).total;
     if (need > (size_t)optin) kern = 1;
     else {
@@ -971,7 +1317,16 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
       ctx->mr_grid = ctx->mr_nbatch;
       ctx->mr_classes = (int)cls.size();
       cudaError_t e = cudaSuccess;
-      if (kern == 3) {
+      if (kern == 4) {
+        DISPATCH_MR(ctx->p, ({
+          cudaFuncAttributes fa;
+          e = cudaFuncGetAttributes(&fa, k_local_mrhs_t<NP_>);
+          if (e == cudaSuccess && (size_t)optin < ctx->mr_smem + fa.sharedSizeBytes) e = cudaErrorInvalidValue;
+          if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_local_mrhs_t<NP_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes);
+        }));
+      } else if (kern == 3) {
         DISPATCH_MR(ctx->p, ({
           cudaFuncAttributes fa;
           e = cudaFuncGetAttributes(&fa, k_local_mrhs_r<NP_>);
@@ -1071,6 +1426,13 @@ int mrhs_setup(dgas_ctx ctx, const std::vector<int>& rep_of) {
 }
 
 void launch_local_mrhs(dgas_ctx ctx, int mode, const PcgState* st, const double* r, double* z, cudaStream_t s) {
+  if (ctx->mr_kernel == 4) {
+    DISPATCH_MR(ctx->p, (k_local_mrhs_t<NP_><<<ctx->mr_grid, (ctx->mr_NW + 1) * 32, ctx->mr_smem, s>>>(
+                            mode, ctx->mr_nbatch, ctx->d_mr_batches, ctx->d_mr_members, ctx->d_sub_ptr, ctx->d_first,
+                            ctx->d_p_off, reinterpret_cast<const double*>(ctx->d_P), r, ctx->d_rbuf, z, st, ctx->mr_NW,
+                            ctx->mr_S, ctx->mr_slot, ctx->mr_WC, ctx->max_sub_cells)));
+    return;
+  }
   if (ctx->mr_kernel == 3) {
     DISPATCH_MR(ctx->p, (k_local_mrhs_r<NP_><<<ctx->mr_grid, (ctx->mr_NW + 1) * 32, ctx->mr_smem, s>>>(
                             mode, ctx->mr_nbatch, ctx->d_mr_batches, ctx->d_mr_members, ctx->d_sub_ptr, ctx->d_first,

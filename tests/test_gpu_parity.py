@@ -441,22 +441,33 @@ def test_eager_path_matches_graph(monkeypatch, name):
     ("cart64_p1", {"DGAS_MR_KERNEL": "1", "DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
     ("cart64_p2", {"DGAS_MR_KERNEL": "1", "DGAS_MR_MINAVG": "1", "DGAS_MR_B": "17", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
     ("cart64_p4", {"DGAS_MR_KERNEL": "1", "DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
-    # independent warp chains (k_local_mrhs_w, the default): default geometry (4 warps x 8 columns), one
+    # independent warp chains (k_local_mrhs_w): default geometry (4 warps x 8 columns), one
     # warp with a 2-slot ring (producer waits on every step), 4 / 16 / 32 columns per warp (8 / 2 / 1
     # K-slices), 8 warps, every n_p (odd n_p: scalar panel loads)
-    # independent warp chains (k_local_mrhs_w, the default): default geometry (8 warps x 2 columns, 16 K-slices),
+    # independent warp chains (k_local_mrhs_w): default geometry (8 warps x 2 columns, 16 K-slices),
     # one warp with a 2-slot ring (producer waits on every
     # step), 4 / 16 / 32 columns per warp (8 / 2 / 1 K-slices), every n_p (odd n_p: scalar panel loads)
+    ("cart128_p3", {"DGAS_MR_KERNEL": "2"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "2", "DGAS_MR_NW": "1", "DGAS_MR_S": "2"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "2", "DGAS_MR_G": "4", "DGAS_MR_NW": "8"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "2", "DGAS_MR_G": "4", "DGAS_MR_NW": "3"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "2", "DGAS_MR_G": "16", "DGAS_MR_NW": "3"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "2", "DGAS_MR_G": "32", "DGAS_MR_NW": "2", "DGAS_MR_S": "8"}, 5),
+    ("cart64_p1", {"DGAS_MR_KERNEL": "2", "DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p2", {"DGAS_MR_KERNEL": "2", "DGAS_MR_MINAVG": "1", "DGAS_MR_G": "16", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p4", {"DGAS_MR_KERNEL": "2", "DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p4", {"DGAS_MR_KERNEL": "2", "DGAS_MR_MINAVG": "1", "DGAS_MR_G": "4", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    # warp chains on the FP64 tensor cores (k_local_mrhs_t, mma.sync m8n8k4, the default): default geometry, one warp with a
+    # 2-slot ring, 3 and 8 warps (ragged last warp: mirrored columns), every n_p (1 or 2 m-tiles, 1..4 k-steps)
     ("cart128_p3", {}, 5),
-    ("cart128_p3", {"DGAS_MR_NW": "1", "DGAS_MR_S": "2"}, 5),
-    ("cart128_p3", {"DGAS_MR_G": "4", "DGAS_MR_NW": "8"}, 5),
-    ("cart128_p3", {"DGAS_MR_G": "4", "DGAS_MR_NW": "3"}, 5),
-    ("cart128_p3", {"DGAS_MR_G": "16", "DGAS_MR_NW": "3"}, 5),
-    ("cart128_p3", {"DGAS_MR_G": "32", "DGAS_MR_NW": "2", "DGAS_MR_S": "8"}, 5),
+    ("cart128_p3", {"DGAS_MR_NW": "4"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "4", "DGAS_MR_NW": "1", "DGAS_MR_S": "2"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "4", "DGAS_MR_NW": "3", "DGAS_MR_S": "4"}, 5),
+    ("cart128_p3", {"DGAS_MR_KERNEL": "4", "DGAS_MR_NW": "8"}, 5),
     ("cart64_p1", {"DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
-    ("cart64_p2", {"DGAS_MR_MINAVG": "1", "DGAS_MR_G": "16", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p2", {"DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
     ("cart64_p4", {"DGAS_MR_MINAVG": "1", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
-    ("cart64_p4", {"DGAS_MR_MINAVG": "1", "DGAS_MR_G": "4", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
+    ("cart64_p4", {"DGAS_MR_KERNEL": "4", "DGAS_MR_MINAVG": "1", "DGAS_MR_NW": "2", "DGAS_DEDUP_MAXFRAC": "1"}, 5),
     # warp chains with row lanes in the forward sweep (k_local_mrhs_r): default geometry, one warp with a
     # 2-slot ring, 3 warps (ragged last warp), every n_p (3 / 5 / 10 / 2 columns per warp)
     ("cart128_p3", {"DGAS_MR_KERNEL": "3"}, 5),
