@@ -22,7 +22,8 @@ HOT = [
     (r"k_spmv_ring<15>", "I1 SpMV, config 4 (byte ring)"),
     (r"k_spmv_cls<10, 2>", "I1 SpMV, config 3 (class-sorted, de-duplicated A, 2 CTAs/SM)"),
     (r"k_spmv_ring<28>", "I1 SpMV, config 5 p=6"),
-    (r"k_local_mrhs_w<10, 2>", "I5 local solves, config 3 (multi-RHS warp chains, default)"),
+    (r"k_local_mrhs_t<10>", "I5 local solves, config 3 (multi-RHS warp chains on the FP64 tensor cores, default)"),
+    (r"k_local_mrhs_w<10, 2>", "I5 local solves, multi-RHS warp chains, K-slice lanes (variant)"),
     (r"k_local_mrhs_r<10>", "I5 local solves, multi-RHS, row lanes forward (variant)"),
     (r"k_local_mrhs<10>", "I5 local solves, multi-RHS, CTA-wide steps (variant)"),
     (r"k_local_panel<15, true, double, false>", "I5 local solves, config 4 (merged panels, narrow CTAs)"),
@@ -95,8 +96,9 @@ def main():
     dem = dict(zip(names, demangle(names)))
     lines = ["# SASS instruction histogram of the hot kernels (`tools/sass_hist.py`, cuobjdump -sass libdgas.so)", "",
              "Static counts per kernel instantiation (sm_100a). `UBLKCP` = `cp.async.bulk` (TMA bulk copy), `SYNCS` = "
-             "mbarrier arrive/try_wait, `LDGSTS` = `cp.async`. No kernel on the iteration path holds a tensor-core "
-             "instruction (fp64 GEMV-class work, DESIGN.md §6).", ""]
+             "mbarrier arrive/try_wait, `LDGSTS` = `cp.async`, `DMMA` = `mma.sync.m8n8k4.f64`. The single-RHS kernels are "
+             "fp64 GEMV-class work on the CUDA cores; the multi-RHS local solve (shared factors) is a dense "
+             "contraction and runs on the FP64 tensor cores (DESIGN.md §6).", ""]
     hdr = ["kernel", "role", "instr", "regs"] + [c for c, _ in CLASSES[:-1]] + ["other top mnemonics"]
     lines.append("| " + " | ".join(hdr) + " |")
     lines.append("|" + "---|" * len(hdr))
