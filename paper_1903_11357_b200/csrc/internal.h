@@ -121,7 +121,7 @@ struct dgas_ctx_s {
   int64_t* d_cls_off = nullptr;        // compact-store offset per row-block class
   int* d_cls_cells = nullptr;          // cells grouped by class
   int* d_cls_nb = nullptr;             // [nc][CLS_MAXDEG] neighbour cells of d_cls_cells[i]
-  int cls_nitems = 0, cls_grid = 0, cls_minb = 1;
+  int cls_nitems = 0, cls_grid = 0, cls_minb = 1, cls_tc = 0;
   int fuse_r = -1;  // residual update fused into the local solve (apply_fuses_restrict), -1 = not decided yet
   std::vector<int64_t> a_dd_h;
   int64_t a_unique = 0, a_bytes_stored = 0;  // distinct row-blocks, bytes of the compact A

@@ -553,6 +553,134 @@ __global__ void __launch_bounds__(SR_NW * 32, MINB) k_spmv_cls(
   spmv_pq_epilogue<NTT>(mydot, wdot, red, st, partials, alpha_hist, it);
 }
 
+// ------------------------------------------------------------------------------------------------
+// k_spmv_cls_t — the class-sorted SpMV on the FP64 tensor cores (mma.sync m8n8k4 f64). For a run of cells of
+// one class the product is a dense contraction, Y (NP x 8 cells) = A_class (NP x W) X (W x 8 cells): the A
+// fragments (2 m-tiles x W / 4 k-steps) are loaded ONCE per item into registers; per tile of 8 cells every
+// lane gathers its own B-fragment entries (entry 4 s + l % 4 of the gathered vector of cell l / 4) straight
+// from global memory, all W / 4 gathers in flight before the first DMMA, and stores its C-fragment entries
+// of y. No shared-memory staging, no warp barrier on the loop, ~8x fewer instructions per cell than
+// k_spmv_cls (ncu there: latency-bound on the gathers, 0.32 issue slots per cycle).
+__device__ __forceinline__ void dmma884s(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int NP>
+__global__ void __launch_bounds__(SR_NW * 32, 2) k_spmv_cls_t(
+    int mode, int nitems, const int4* __restrict__ items, const int64_t* __restrict__ cls_off,
+    const int* __restrict__ cells, const int* __restrict__ cls_nb, const double* __restrict__ A, const double* x,
+    double* y, const double* z, double* const* pbuf, PcgState* st, double* partials, double* alpha_hist) {
+  constexpr int NTT = SR_NW * 32;
+  constexpr int MT = (NP + 7) / 8;                   // m-tiles of the NP rows
+  constexpr int KSM = (CLS_MAXDEG * NP + 3) / 4;     // k-steps of the widest row-block
+  __shared__ double red[NTT / 32];
+  __shared__ double wdot[NTT / 32];
+  int it = 0;
+  double beta = 0;
+  const double* pold = nullptr;
+  double* pnew = nullptr;
+  const bool pcg = mode == 1 || mode == 3;
+  if (pcg) {
+    if (st->done) return;
+    it = st->it;
+    beta = it > 0 ? st->beta : 0.0;
+    pold = pbuf[it & 1];
+    pnew = pbuf[(it + 1) & 1];
+    if (mode == 3) x = pnew;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  auto colval = [&](int64_t id) -> double {
+    return mode == 1 ? (it > 0 ? z[id] + beta * pold[id] : z[id]) : x[id];
+  };
+  double mydot = 0;
+  const int gw = blockIdx.x * SR_NW + w, nw = gridDim.x * SR_NW;
+  for (int wi = gw; wi < nitems; wi += nw) {
+    const int4 itm = items[wi];  // (class, first cell in `cells`, count, W = deg NP)
+    const int W = itm.w, n = itm.z;
+    const int* cl = cells + itm.y;
+    const int* cnb = cls_nb + (size_t)itm.y * CLS_MAXDEG;
+    // A fragments of the class row-block (column-major NP x W): a[t][s] = A[8 t + lr][4 s + lk]
+    double af[MT][KSM];
+    {
+      const double* Ab = A + cls_off[itm.x];
+#pragma unroll
+      for (int s = 0; s < KSM; ++s) {
+        const int col = 4 * s + lk;
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const int row = 8 * t + lr;
+          const bool ok = col < W && row < NP;
+          af[t][s] = ok ? __ldg(Ab + (ok ? col * NP + row : 0)) : 0.0;
+        }
+      }
+    }
+    for (int i0 = 0; i0 < n; i0 += 8) {
+      // this lane's B column is cell i0 + lr: its neighbour ids (nbr order, padded with the cell itself)
+      const int ic = min(i0 + lr, n - 1);
+      int ids[CLS_MAXDEG];
+#pragma unroll
+      for (int j = 0; j < CLS_MAXDEG; ++j) ids[j] = __ldg(cnb + (size_t)ic * CLS_MAXDEG + j);
+      const int mycell = __ldg(cl + ic);
+      double bf[KSM];
+#pragma unroll
+      for (int s = 0; s < KSM; ++s) {
+        // entry 4 s + lk of the gathered vector: neighbour j = col / NP (one of two compile-time candidates)
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int col = 4 * s + lk;
+        const int j0 = (4 * s) / NP;
+        const bool hi = col >= NP * (j0 + 1);
+        const int nb = hi ? ids[j0 + 1 < CLS_MAXDEG ? j0 + 1 : j0] : ids[j0];
+        const int comp = col - NP * (hi ? j0 + 1 : j0);
+        const bool ok = col < W;
+        bf[s] = ok ? colval((int64_t)nb * NP + comp) : 0.0;
+      }
+      // own values of p_new for the dot product p.q (and the p write of mode 1): C-fragment positions
+      const int ca = __shfl_sync(0xffffffffu, mycell, 8 * lk), cb = __shfl_sync(0xffffffffu, mycell, 8 * lk + 4);
+      const bool va = i0 + 2 * lk < n, vb = i0 + 2 * lk + 1 < n;
+      double pa[MT], pb[MT];
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const int row = 8 * t + lr;
+        pa[t] = 0.0;
+        pb[t] = 0.0;
+        if (pcg && row < NP) {
+          if (va) pa[t] = colval((int64_t)ca * NP + row);
+          if (vb) pb[t] = colval((int64_t)cb * NP + row);
+        }
+      }
+      double c0[MT], c1[MT];
+#pragma unroll
+      for (int t = 0; t < MT; ++t) { c0[t] = 0.0; c1[t] = 0.0; }
+#pragma unroll
+      for (int s = 0; s < KSM; ++s)
+#pragma unroll
+        for (int t = 0; t < MT; ++t) dmma884s(c0[t], c1[t], af[t][s], bf[s]);
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const int row = 8 * t + lr;
+        if (row < NP) {
+          if (va) {
+            const size_t id = (size_t)ca * NP + row;
+            y[id] = c0[t];
+            if (pcg) { if (mode == 1) pnew[id] = pa[t]; mydot += pa[t] * c0[t]; }
+          }
+          if (vb) {
+            const size_t id = (size_t)cb * NP + row;
+            y[id] = c1[t];
+            if (pcg) { if (mode == 1) pnew[id] = pb[t]; mydot += pb[t] * c1[t]; }
+          }
+        }
+      }
+    }
+  }
+  if (!pcg) return;
+  spmv_pq_epilogue<NTT>(mydot, wdot, red, st, partials, alpha_hist, it);
+}
+
 #define DISPATCH_P15S(P, ...)                               \
   switch (P) {                                              \
     case 1: { constexpr int NP_ = 3; __VA_ARGS__; } break;  \
@@ -644,7 +772,11 @@ void launch_spmv_ring(dgas_ctx ctx, int mode, const double* x, double* y, PcgSta
     mode = 3;
   }
   if (ctx->d_cls_items) {
-    if (ctx->cls_minb == 2) {
+    if (ctx->cls_tc) {
+      DISPATCH_P15S(ctx->p, (k_spmv_cls_t<NP_><<<ctx->cls_grid, SR_NW * 32, 0, s>>>(
+                                mode, ctx->cls_nitems, ctx->d_cls_items, ctx->d_cls_off, ctx->d_cls_cells, ctx->d_cls_nb,
+                                ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha)));
+    } else if (ctx->cls_minb == 2) {
       DISPATCH_P15S(ctx->p, (k_spmv_cls<NP_, 2><<<ctx->cls_grid, SR_NW * 32, 0, s>>>(
                                 mode, ctx->cls_nitems, ctx->d_cls_items, ctx->d_cls_off, ctx->d_cls_cells, ctx->d_cls_nb,
                                 ctx->d_A, x, y, ctx->d_z, ctx->d_pbuf, st, ctx->d_partials, ctx->d_alpha)));
@@ -705,8 +837,14 @@ int spmv_cls_setup(dgas_ctx ctx, const std::vector<int64_t>& dd) {
   int minb = ctx->np <= 10 ? 2 : 1;
   if (const char* e = std::getenv("DGAS_CLS_MINB")) minb = std::atoi(e) == 2 ? 2 : 1;
   ctx->cls_minb = minb;
+  int tc = 1;  // tensor-core variant (k_spmv_cls_t; config 3: 0.077 -> 0.057 ms, 2989 -> 3097 PCG it/s): DGAS_CLS_TC=0 disables
+  if (const char* e = std::getenv("DGAS_CLS_TC")) tc = std::atoi(e) != 0;
+  if (ctx->np > 10) tc = 0;  // n_p = 15: the A fragments (46 doubles per lane) spill at the 128-register cap
+  ctx->cls_tc = tc;
   int cps = 1;  // resident CTAs per SM (register-bound: the row-block lives in registers)
-  if (minb == 2) {
+  if (tc) {
+    DISPATCH_P15S(ctx->p, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_spmv_cls_t<NP_>, SR_NW * 32, 0)));
+  } else if (minb == 2) {
     DISPATCH_P15S(ctx->p, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_spmv_cls<NP_, 2>, SR_NW * 32, 0)));
   } else {
     DISPATCH_P15S(ctx->p, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_spmv_cls<NP_, 1>, SR_NW * 32, 0)));

@@ -640,9 +640,10 @@ def test_dedup_is_bitwise_identical(monkeypatch):
     # runs: no de-duplication (byte ring) | de-duplicated A read through L2 by k_spmv_dd (the byte ring's
     # arithmetic order) | de-duplicated A with the class-sorted k_spmv_cls (its own slice order: same
     # operator, sums in another order, so equal to rounding only)
-    for dd, cls in (("0", "0"), ("1", "0"), ("1", "1")):
+    for dd, cls, tc in (("0", "0", "0"), ("1", "0", "0"), ("1", "1", "0"), ("1", "1", "1")):
         monkeypatch.setenv("DGAS_DEDUP", dd)
         monkeypatch.setenv("DGAS_SPMV_CLS", cls)
+        monkeypatch.setenv("DGAS_CLS_TC", tc)  # 1: the tensor-core class SpMV (k_spmv_cls_t, the default)
         monkeypatch.setenv("DGAS_DD_CPS", "2")
         S = _solver(P)
         info = S.get_info()
@@ -655,7 +656,7 @@ def test_dedup_is_bitwise_identical(monkeypatch):
         out.append((x.cpu().numpy(), it, c, st, S.spmv(b).cpu().numpy()))
         out_b = b.cpu().numpy()
         S.close()
-    (x0, i0, c0, s0, y0), (x1, i1, c1, s1, y1), (x2, i2, c2, s2, y2) = out
+    (x0, i0, c0, s0, y0), (x1, i1, c1, s1, y1), (x2, i2, c2, s2, y2), (x3, i3, c3, s3, y3) = out
     assert s0 == s1 == 0 and i0 == i1 and c0 == c1
     assert np.array_equal(y0, y1)
     assert np.array_equal(x0, x1)
@@ -664,6 +665,10 @@ def test_dedup_is_bitwise_identical(monkeypatch):
     assert s2 == 0 and abs(i2 - i0) <= 2
     scale = O.Oracle(P).spmv_abs(out_b)
     assert np.all(np.abs(y2 - y0) <= 64 * _EPS * scale)
+    # tensor-core class SpMV (DMMA sums over k inside the instruction): the same bounds
+    assert s3 == 0 and abs(i3 - i0) <= 2
+    assert np.all(np.abs(y3 - y0) <= 64 * _EPS * scale)
+    assert np.linalg.norm(x3 - x0) <= 1e-7 * np.linalg.norm(x0)
     assert np.linalg.norm(x2 - x0) <= 1e-7 * np.linalg.norm(x0)
 
 
