@@ -19,7 +19,7 @@ done
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo "bench reference rc $?" >> $L
 if [ -z "$SKIP_NCU" ]; then
   DGAS_EAGER=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s ${NCU_SKIP:-500} -c 80 --csv --log-file gpurun_out/launches_default.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu.log 2>&1; echo "ncu launches rc $?" >> $L
-  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_local_mrhs_t|k_spmv_cls|k_restrict_chunk|k_prolong" -s 4 -c 4 -o gpurun_out/prof_default -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --kernel-reps 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc $?" >> $L
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_local_mrhs_t|k_spmv_cls_t|k_restrict_chunk|k_prolong" -s 4 -c 4 -o gpurun_out/prof_default -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --kernel-reps 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc $?" >> $L
 fi
 cat $L
 # config 2 launch list (its setup builds the explicit inverses with ~1,200 launches: skip past them)

@@ -16,7 +16,7 @@ KEEP = ["Memory Throughput", "DRAM Throughput", "Duration", "Compute (SM) Throug
         "Dynamic Shared Memory Per Block", "Theoretical Occupancy", "Achieved Occupancy"]
 ROLE = {"k_local": "local", "k_local_panel": "local", "k_local_warp": "local", "k_local_inv": "local",
         "k_local_mrhs": "local", "k_local_mrhs_w": "local", "k_local_mrhs_r": "local", "k_local_mrhs_t": "local",
-        "k_spmv3": "spmv", "k_spmv_ring": "spmv", "k_spmv_dd": "spmv", "k_spmv_cls": "spmv"}
+        "k_spmv3": "spmv", "k_spmv_ring": "spmv", "k_spmv_dd": "spmv", "k_spmv_cls": "spmv", "k_spmv_cls_t": "spmv"}
 
 
 def run(args):

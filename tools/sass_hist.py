@@ -20,7 +20,8 @@ LIB = os.path.join(ROOT, "paper_1903_11357_b200", "libdgas.so")
 # kernel-name regexes (demangled) -> where they run
 HOT = [
     (r"k_spmv_ring<15>", "I1 SpMV, config 4 (byte ring)"),
-    (r"k_spmv_cls<10, 2>", "I1 SpMV, config 3 (class-sorted, de-duplicated A, 2 CTAs/SM)"),
+    (r"k_spmv_cls_t<10>", "I1 SpMV, config 3 (class-sorted, de-duplicated A, FP64 tensor cores, default)"),
+    (r"k_spmv_cls<10, 2>", "I1 SpMV, class-sorted on the CUDA cores (variant)"),
     (r"k_spmv_ring<28>", "I1 SpMV, config 5 p=6"),
     (r"k_local_mrhs_t<10>", "I5 local solves, config 3 (multi-RHS warp chains on the FP64 tensor cores, default)"),
     (r"k_local_mrhs_w<10, 2>", "I5 local solves, multi-RHS warp chains, K-slice lanes (variant)"),
