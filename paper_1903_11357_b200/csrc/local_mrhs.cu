@@ -1031,7 +1031,8 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_t(int mode, int nbatch, c
 #pragma unroll
           for (int t = 0; t < MT; ++t) {
             const double pv = pA[4 * u * NP + 8 * t];  // rows beyond NP: masked below (reads stay inside the ring + its 128-byte pad)
-            av[u][t] = rowok[t] ? pv : 0.0;
+            if (8 * t + 7 < NP) av[u][t] = pv;  // every row of this m-tile exists (compile time)
+            else av[u][t] = rowok[t] ? pv : 0.0;
           }
         }
 #pragma unroll
@@ -1144,8 +1145,12 @@ __global__ void __launch_bounds__(32 * 9) k_local_mrhs_t(int mode, int nbatch, c
           cv[u] = *wp[u];
 #pragma unroll
           for (int kt = 0; kt < KT; ++kt) {
-            const double pv = pB[8 * u * NP + (kok[kt] ? 4 * kt : 0)];
-            av[u][kt] = kok[kt] ? pv : 0.0;
+            if (4 * kt + 3 < NP) {  // every k index of this k-step exists (compile time)
+              av[u][kt] = pB[8 * u * NP + 4 * kt];
+            } else {
+              const double pv = pB[8 * u * NP + (kok[kt] ? 4 * kt : 0)];
+              av[u][kt] = kok[kt] ? pv : 0.0;
+            }
           }
         }
 #pragma unroll
