@@ -1,5 +1,6 @@
 #!/bin/bash
-# one-off: eager in-situ phase timings for variants
+# in-loop phase times (eager path, CUDA events around every phase of every PCG iteration: DGAS_EAGER_TIMING) for
+# configs (XC) x env variants (XV, ';'-separated)
 cd $GRAFT_REPO_ROOT
 IFS=';' read -ra VS <<< "${XV:--}"
 for c in ${XC:-cfg3}; do
