@@ -361,15 +361,20 @@ def main():
     except Exception:
         pass
     spmv_apply_gbs = (alg["spmv"] + alg["apply_total"]) / ((kt["spmv"] + kt["apply_total"]) * 1e-3) / 1e9
-    # fp64 arithmetic of the dominant kernel against the CUDA-core FP64 peak (148 SMs x 64 FMA/clk x 2 flop at
-    # the SM clock: 37.2 TFLOP/s at 1965 MHz): every stored operator entry is one FMA per use
+    # fp64 arithmetic of the dominant kernel against the FP64 peak from the unit counts (148 SMs x 64 FMA/clk x 2
+    # flop at the SM clock: 37.2 TFLOP/s at 1965 MHz): every stored operator entry is one FMA per use
     # (SpMV: all stored blocks; local solves: factor + D triangles, forward and backward sweep)
     props = torch.cuda.get_device_properties(local)
     fp64_peak = props.multi_processor_count * 64 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     flops = {"spmv": 2.0 * nnzb * npp * npp, "local": 4.0 * (info["bytes_U"] + dinv_tri) / 8.0}
     alu = {"bound": "alu", "achieved": flops[dom] / (kt[dom] * 1e-3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
            "frac": flops[dom] / (kt[dom] * 1e-3) / 1e12 / fp64_peak,
-           "note": "fp64 FMA work of the same kernel against the CUDA-core FP64 peak (no tensor cores on this path)"}
+           "note": ("fp64 FMA work of the same kernel against the FP64 peak derived from the unit counts (148 SMs x 64 "
+                    "FMA/clk x 2 flop x SM clock; the guides give no separate FP64 tensor figure). "
+                    + ("This kernel issues mma.sync.m8n8k4.f64 (FP64 tensor cores): a dense multi-right-hand-side "
+                       "contraction; it is bound by the latency of its dependent chain, not by the math rate."
+                       if dom == "local" and info["local_kernel"] == 5 else
+                       "CUDA-core DFMA kernel (single right-hand side, GEMV-class)."))}
 
     line = {
         "metric": METRIC, "value": value, "unit": "PCG it/s", "n_gpus": world, "steps": args.steps,
