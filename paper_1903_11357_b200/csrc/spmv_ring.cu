@@ -636,7 +636,8 @@ __global__ void __launch_bounds__(SR_NW * 32, 2) k_spmv_cls_t(
         const int nb = hi ? ids[j0 + 1 < CLS_MAXDEG ? j0 + 1 : j0] : ids[j0];
         const int comp = col - NP * (hi ? j0 + 1 : j0);
         const bool ok = col < W;
-        bf[s] = ok ? colval((int64_t)nb * NP + comp) : 0.0;
+        bf[s] = 0.0;
+        if (4 * s < W) bf[s] = ok ? colval((int64_t)nb * NP + comp) : 0.0;  // (warp-uniform: k-steps beyond W skipped)
       }
       // own values of p_new for the dot product p.q (and the p write of mode 1): C-fragment positions
       const int ca = __shfl_sync(0xffffffffu, mycell, 8 * lk), cb = __shfl_sync(0xffffffffu, mycell, 8 * lk + 4);
@@ -657,8 +658,10 @@ __global__ void __launch_bounds__(SR_NW * 32, 2) k_spmv_cls_t(
       for (int t = 0; t < MT; ++t) { c0[t] = 0.0; c1[t] = 0.0; }
 #pragma unroll
       for (int s = 0; s < KSM; ++s)
+        if (4 * s < W) {
 #pragma unroll
-        for (int t = 0; t < MT; ++t) dmma884s(c0[t], c1[t], af[t][s], bf[s]);
+          for (int t = 0; t < MT; ++t) dmma884s(c0[t], c1[t], af[t][s], bf[s]);
+        }
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const int row = 8 * t + lr;
